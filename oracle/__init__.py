@@ -1,0 +1,454 @@
+"""fp64 CPU oracle for the stateful-session attention hot path (arXiv 2605.13784).
+
+TEST INFRASTRUCTURE.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  It shares no code with ``paper_2605_13784_b200`` (the CUDA path) and
+imports nothing from it; the two meet only in ``streams.py`` (seeded inputs).
+
+What it computes:
+
+* ``attention_rows`` — Eq. (attention) softmax(QK^T/sqrt(d_k))V, PAPER.md
+  P:143-148, for explicit rows and visible-key counts (C, ``ssa_oracle.c``).
+* ``segment_rows`` — Eq. (query-attention): the rows of a new
+  segment X (an append D_k, Alg. 1 L282 P:282; a query q, Alg. 2 L295 P:295;
+  a Flash Query f_i, Alg. 3 L542 P:542) attend to the cached keys
+  [S; D_1..D_{k-1}] followed by X[0..i] (causal; reading R-2), with the
+  GQA head map of reading R-5.
+* ``full_recompute`` — the naive approach of P:42: causal attention over the
+  whole concatenation [S; D_1..D_k; Q_j] from scratch, no session state.
+* ``merge_partials`` — split-KV log-sum-exp merge (reading R-11).
+* ``OracleStore`` — the session model: retained tokens, versions ("data
+  version t"), the page allocator replica (lowest free id first, R0 padded to a
+  page boundary; reading R-9) and the FNV-1a-64 digest.
+
+Pins: ``tests/test_oracle_pins.py`` (mpmath brute force, closed forms,
+invariants, golden fixtures under ``tests/golden/``).
+"""
+from __future__ import annotations
+
+import ctypes
+import heapq
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build() -> str:
+    """Compile ssa_oracle.c with gcc (plain -O2, no fast-math)."""
+    import subprocess
+    src = os.path.join(_HERE, "ssa_oracle.c")
+    if (not os.path.exists(_LIB_PATH)) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-o", _LIB_PATH, src, "-lm"])
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        dp = ctypes.POINTER(ctypes.c_double)
+        i64 = ctypes.c_int64
+        L.oracle_attention_rows.argtypes = [i64, i64, i64, dp, i64, i64, dp, i64, dp, i64,
+                                            ctypes.POINTER(i64), ctypes.c_double, dp, dp]
+        L.oracle_attention_rows.restype = ctypes.c_int
+        L.oracle_merge_partials.argtypes = [i64, i64, i64, dp, dp, dp, dp]
+        L.oracle_merge_partials.restype = ctypes.c_int
+        L.oracle_fnv1a64.argtypes = [ctypes.c_void_p, i64, ctypes.c_uint64]
+        L.oracle_fnv1a64.restype = ctypes.c_uint64
+        L.oracle_fnv1a64_offset_basis.argtypes = []
+        L.oracle_fnv1a64_offset_basis.restype = ctypes.c_uint64
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+# ----------------------------------------------------------------------------
+# exact decode of stored values (reading R-10: inputs are bf16 or fp32 bits)
+# ----------------------------------------------------------------------------
+def to_f64(x: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) or float32 -> float64, exactly."""
+    x = np.asarray(x)
+    if x.dtype == np.uint16:
+        return (x.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+    if x.dtype == np.float32:
+        return x.astype(np.float64)
+    if x.dtype == np.float64:
+        return x
+    raise TypeError(f"unsupported storage dtype {x.dtype}")
+
+
+# ----------------------------------------------------------------------------
+# definitions
+# ----------------------------------------------------------------------------
+def attention_rows(q: np.ndarray, k: np.ndarray, v: np.ndarray, nvis, scale: float):
+    """Eq. (attention) P:145 for rows q[r] over keys k[0:nvis[r]], v[0:nvis[r]].
+
+    q: [nr][d], k: [nk][d], v: [nk][dv] (float64).  Returns (o [nr][dv], lse [nr]).
+    """
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    nr, d = q.shape
+    nk = k.shape[0]
+    dv = v.shape[1]
+    nvis = np.ascontiguousarray(np.broadcast_to(np.asarray(nvis, dtype=np.int64), (nr,)))
+    o = np.zeros((nr, dv), dtype=np.float64)
+    lse = np.zeros((nr,), dtype=np.float64)
+    if nr == 0:
+        return o, lse
+    kk = k if nk else np.zeros((1, d))
+    vv = v if nk else np.zeros((1, dv))
+    rc = lib().oracle_attention_rows(nr, d, dv, _dp(q), d, nk, _dp(kk), d, _dp(vv), dv,
+                                     nvis.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                     float(scale), _dp(o), _dp(lse))
+    if rc != 0:
+        raise ValueError("oracle_attention_rows: bad arguments")
+    return o, lse
+
+
+def merge_partials(o_parts: np.ndarray, lse_parts: np.ndarray):
+    """Split-KV merge (reading R-11).  o_parts [G][nr][dv], lse_parts [G][nr]."""
+    o_parts = np.ascontiguousarray(o_parts, dtype=np.float64)
+    lse_parts = np.ascontiguousarray(lse_parts, dtype=np.float64)
+    G, nr, dv = o_parts.shape
+    o = np.zeros((nr, dv))
+    lse = np.zeros((nr,))
+    rc = lib().oracle_merge_partials(G, nr, dv, _dp(o_parts), _dp(lse_parts), _dp(o), _dp(lse))
+    if rc != 0:
+        raise ValueError("oracle_merge_partials: bad arguments")
+    return o, lse
+
+
+def fnv1a64(data: bytes, h: int | None = None) -> int:
+    L = lib()
+    if h is None:
+        h = L.oracle_fnv1a64_offset_basis()
+    buf = (ctypes.c_uint8 * len(data)).from_buffer_copy(data) if data else None
+    return int(L.oracle_fnv1a64(buf, len(data), ctypes.c_uint64(h)))
+
+
+def derive_seed(tokens) -> int:
+    """Eq. seed(P) = FNV1a(P) mod 2^32; tokens as int32 LE."""
+    data = np.asarray(list(tokens), dtype="<i4").tobytes()
+    return fnv1a64(data) % (1 << 32)
+
+
+def default_scale(d: int) -> float:
+    """1/sqrt(d_k), Eq. (attention) P:145 (reading R-1)."""
+    return 1.0 / math.sqrt(d)
+
+
+def segment_rows(k_cache, v_cache, q_new, k_new, v_new, num_kv_heads: int, scale: float,
+                 tokens=None, heads=None):
+    """Rows of a new segment X against cache ++ X (causal), Eq. query-attention P:152.
+
+    k_cache/v_cache: [n][Hkv][d] (any storage dtype; n may be 0)
+    q_new: [m][Hq][d], k_new/v_new: [m][Hkv][d]
+    Row (t, h) attends to all n cached keys and new keys 0..t of kv head
+    h // (Hq/Hkv) (readings R-2, R-5).  ``tokens``/``heads`` select a subset.
+    Returns (o [len(tokens)][len(heads)][d], lse [len(tokens)][len(heads)]) fp64.
+    """
+    kc, vc = to_f64(k_cache), to_f64(v_cache)
+    qn, kn, vn = to_f64(q_new), to_f64(k_new), to_f64(v_new)
+    m, hq, d = qn.shape
+    n = kc.shape[0]
+    g = hq // num_kv_heads
+    tokens = list(range(m)) if tokens is None else list(tokens)
+    heads = list(range(hq)) if heads is None else list(heads)
+    dv = vn.shape[2]
+    o = np.zeros((len(tokens), len(heads), dv))
+    lse = np.zeros((len(tokens), len(heads)))
+    for hi, h in enumerate(heads):
+        kvh = h // g
+        keys = np.concatenate([kc[:, kvh, :].reshape(n, kn.shape[2]), kn[:, kvh, :]], axis=0)
+        vals = np.concatenate([vc[:, kvh, :].reshape(n, dv), vn[:, kvh, :]], axis=0)
+        qrows = qn[tokens, h, :]
+        nvis = np.array([n + t + 1 for t in tokens], dtype=np.int64)
+        oh, lh = attention_rows(qrows, keys, vals, nvis, scale)
+        o[:, hi, :] = oh
+        lse[:, hi] = lh
+    return o, lse
+
+
+def full_recompute(q_all, k_all, v_all, num_kv_heads: int, scale: float, rows=None):
+    """Naive approach of P:42: causal attention over the whole sequence, from scratch.
+
+    q_all: [N][Hq][d], k_all/v_all: [N][Hkv][d].  Row i sees keys 0..i.
+    Returns o [len(rows)][Hq][d] fp64 (rows default: all).
+    """
+    q, k, v = to_f64(q_all), to_f64(k_all), to_f64(v_all)
+    N, hq, d = q.shape
+    g = hq // num_kv_heads
+    rows = list(range(N)) if rows is None else list(rows)
+    o = np.zeros((len(rows), hq, v.shape[2]))
+    for h in range(hq):
+        oh, _ = attention_rows(q[rows, h, :], k[:, h // g, :], v[:, h // g, :],
+                               np.array([i + 1 for i in rows], dtype=np.int64), scale)
+        o[:, h, :] = oh
+    return o
+
+
+# ----------------------------------------------------------------------------
+# session model
+# ----------------------------------------------------------------------------
+class OracleError(Exception):
+    def __init__(self, code: str):
+        super().__init__(code)
+        self.code = code
+
+
+@dataclass
+class _Session:
+    n_prefix: int
+    k: list = field(default_factory=list)     # per layer: np array [n][Hkv][d]
+    v: list = field(default_factory=list)
+    n_tokens: int = 0
+    version: int = 0
+    pages: list = field(default_factory=list)
+
+
+class OracleStore:
+    """Session model of DESIGN.md §3.
+
+    * create(S)   — Region 0 processed once; version 1.
+    * append(D_k) — "only the delta is processed and appended", Alg. 1;
+                    version += 1 ("incremented after each data ingestion batch").
+    * query(q)    — Alg. 2; no state change (R2 cleared; reading R-3).
+    * flash_query_batch(f_1..f_k) — Eq. flash-eval P:406 for each f_i against K_t, each
+                    seeing only the cache and its own tokens (reading R-4); no state change.
+    * truncate(p) — SeqRemove(s, p, inf), P:438 / Alg. 3 L540.
+    * pages       — P-token pages, lowest free id first, R0 padded to a page boundary
+                    (reading R-9); the page table is compared bit-exactly with the GPU store.
+    """
+
+    def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
+                 dtype="bf16", softmax_scale=0.0, max_sessions=1024):
+        self.L, self.hq, self.hkv, self.d = num_layers, num_q_heads, num_kv_heads, head_dim
+        self.P, self.num_pages, self.dtype = page_size, num_pages, dtype
+        self.scale = softmax_scale if softmax_scale > 0 else default_scale(head_dim)
+        self.max_sessions = max_sessions
+        self.free = list(range(num_pages))
+        heapq.heapify(self.free)
+        self.sessions: dict[int, _Session] = {}
+        self.next_id = 0
+
+    # -- page model (reading R-9) --------------------------------------------
+    def slots_for(self, n_prefix: int, n_tokens: int) -> int:
+        """Slots occupied by n_tokens tokens: R0 is padded to a page boundary."""
+        if n_tokens <= n_prefix:
+            return n_tokens
+        pad = -(-n_prefix // self.P) * self.P
+        return pad + (n_tokens - n_prefix)
+
+    def pages_for(self, n_prefix: int, n_tokens: int) -> int:
+        return -(-self.slots_for(n_prefix, n_tokens) // self.P)
+
+    def _reserve(self, s: _Session, n_new: int) -> list:
+        need = self.pages_for(s.n_prefix, s.n_tokens + n_new) - len(s.pages)
+        if need > len(self.free):
+            raise OracleError("POOL_EXHAUSTED")
+        return [heapq.heappop(self.free) for _ in range(need)]
+
+    def occupancy(self):
+        return self.num_pages - len(self.free), self.num_pages
+
+    # -- helpers ---------------------------------------------------------------
+    def _check(self, sid):
+        if sid not in self.sessions:
+            raise OracleError("UNKNOWN_SESSION")
+        return self.sessions[sid]
+
+    def _layers(self, layer):
+        return range(self.L) if layer < 0 else [layer]
+
+    def _rows(self, s: _Session, layer: int, Q, K, V, tokens=None, heads=None):
+        d = self.d
+        kc = s.k[layer] if s.n_tokens else np.zeros((0, self.hkv, d), dtype=K.dtype)
+        vc = s.v[layer] if s.n_tokens else np.zeros((0, self.hkv, d), dtype=V.dtype)
+        return segment_rows(kc[:s.n_tokens], vc[:s.n_tokens], Q, K, V, self.hkv, self.scale,
+                            tokens, heads)
+
+    # -- API -------------------------------------------------------------------
+    def session_create(self, n_prefix, Q, K, V, compute=True):
+        """Q/K/V: [L][n][H][d] storage arrays.  Returns (sid, O [L][n][Hq][d] or None)."""
+        if n_prefix <= 0:
+            raise OracleError("INVALID_ARG")
+        if len(self.sessions) >= self.max_sessions:
+            raise OracleError("SESSION_LIMIT")
+        s = _Session(n_prefix=n_prefix)
+        s.pages = []
+        s.pages = self._reserve(s, n_prefix)
+        sid = self.next_id
+        self.next_id += 1
+        O = self._compute(s, Q, K, V, -1) if compute else None
+        s.k = [np.array(K[l]) for l in range(self.L)]
+        s.v = [np.array(V[l]) for l in range(self.L)]
+        s.n_tokens = n_prefix
+        s.version = 1
+        self.sessions[sid] = s
+        return sid, O
+
+    def _compute(self, s, Q, K, V, layer):
+        outs = []
+        for l in self._layers(layer):
+            li = 0 if layer >= 0 else l
+            o, _ = self._rows(s, l, Q[li], K[li], V[li])
+            outs.append(o)
+        return np.stack(outs)
+
+    def session_append(self, sid, Q, K, V, compute=True):
+        s = self._check(sid)
+        m = K.shape[1]
+        if m <= 0:
+            raise OracleError("INVALID_ARG")
+        new_pages = self._reserve(s, m)
+        O = self._compute(s, Q, K, V, -1) if compute else None
+        s.pages.extend(new_pages)
+        for l in range(self.L):
+            s.k[l] = np.concatenate([s.k[l][:s.n_tokens], K[l]], axis=0)
+            s.v[l] = np.concatenate([s.v[l][:s.n_tokens], V[l]], axis=0)
+        s.n_tokens += m
+        s.version += 1
+        return O, s.version
+
+    def session_query(self, sid, Q, K, V, layer=-1, tokens=None, heads=None):
+        """Query plane: Q/K/V [L'][m][H][d] (L' = L, or 1 when layer >= 0). No state change."""
+        s = self._check(sid)
+        if K.shape[1] <= 0:
+            raise OracleError("INVALID_ARG")
+        outs = []
+        for i, l in enumerate(self._layers(layer)):
+            o, _ = self._rows(s, l, Q[i], K[i], V[i], tokens, heads)
+            outs.append(o)
+        return np.stack(outs)
+
+    def flash_query_batch(self, sid, questions, layer):
+        """questions: list of (Q [m_i][Hq][d], K, V [m_i][Hkv][d]) for one layer.
+
+        Each f_i sees cache version t plus its own tokens only (reading R-4)."""
+        s = self._check(sid)
+        return [self._rows(s, layer, q, k, v)[0] for (q, k, v) in questions]
+
+    def batch_run(self, items, layer=-1):
+        """Multi-tenant batch with snapshot semantics (reading R-7).
+
+        items: list of dicts {kind: 'append'|'query'|'stateless', session, Q, K, V}
+        with per-layer arrays [L'][m][H][d].  Every item reads version t; appends
+        publish t+1 after all items are computed.  Pages for appends are reserved
+        in item order.  Returns list of O arrays.
+        """
+        seen = set()
+        for it in items:
+            if it["kind"] == "append":
+                if it["session"] in seen:
+                    raise OracleError("INVALID_ARG")
+                seen.add(it["session"])
+                self._check(it["session"])
+        reserved = {}
+        for it in items:
+            if it["kind"] == "append":
+                s = self.sessions[it["session"]]
+                try:
+                    reserved[it["session"]] = self._reserve(s, it["K"].shape[1])
+                except OracleError:
+                    for pages in reserved.values():
+                        for p in pages:
+                            heapq.heappush(self.free, p)
+                    raise
+        outs = []
+        for it in items:
+            Q, K, V = it["Q"], it["K"], it["V"]
+            if it["kind"] == "stateless":
+                tmp = _Session(n_prefix=0)
+                outs.append(np.stack([self._rows(tmp, l, Q[i], K[i], V[i])[0]
+                                      for i, l in enumerate(self._layers(layer))]))
+            else:
+                s = self._check(it["session"])
+                outs.append(np.stack([self._rows(s, l, Q[i], K[i], V[i])[0]
+                                      for i, l in enumerate(self._layers(layer))]))
+        if layer < 0 or layer == self.L - 1:
+            for it in items:
+                if it["kind"] == "append":
+                    s = self.sessions[it["session"]]
+                    s.pages.extend(reserved[it["session"]])
+                    K, V = it["K"], it["V"]
+                    for l in range(self.L):
+                        li = l if K.shape[0] == self.L else 0
+                        s.k[l] = np.concatenate([s.k[l][:s.n_tokens], K[li]], axis=0)
+                        s.v[l] = np.concatenate([s.v[l][:s.n_tokens], V[li]], axis=0)
+                    s.n_tokens += K.shape[1]
+                    s.version += 1
+        return outs
+
+    def truncate(self, sid, p):
+        """SeqRemove(s, p, inf) (Alg. 3 L540/L547): drop tokens >= p, free pages."""
+        s = self._check(sid)
+        if p < 0 or p > s.n_tokens:
+            raise OracleError("INVALID_ARG")
+        if p == s.n_tokens:
+            return s.version
+        s.n_tokens = p
+        keep = self.pages_for(s.n_prefix, p)
+        for pg in s.pages[keep:]:
+            heapq.heappush(self.free, pg)
+        s.pages = s.pages[:keep]
+        s.version += 1
+        return s.version
+
+    def session_destroy(self, sid):
+        s = self._check(sid)
+        for pg in s.pages:
+            heapq.heappush(self.free, pg)
+        del self.sessions[sid]
+
+    def page_table(self, sid):
+        return list(self._check(sid).pages)
+
+    def info(self, sid):
+        s = self._check(sid)
+        return dict(n_tokens=s.n_tokens, n_prefix=s.n_prefix, n_pages=len(s.pages), version=s.version)
+
+    def digest(self, sid) -> int:
+        """FNV-1a-64 over, layer-major then token order, the records
+        int32 LE layer || int64 LE token || K bytes || V bytes."""
+        s = self._check(sid)
+        return session_digest(s.k, s.v, s.n_tokens)
+
+
+def session_digest(k_layers, v_layers, n_tokens) -> int:
+    h = None
+    for l, (K, V) in enumerate(zip(k_layers, v_layers)):
+        K = np.ascontiguousarray(K[:n_tokens])
+        V = np.ascontiguousarray(V[:n_tokens])
+        kb = K.reshape(n_tokens, -1).view(np.uint8)
+        vb = V.reshape(n_tokens, -1).view(np.uint8)
+        rec = np.empty((n_tokens, 12 + kb.shape[1] + vb.shape[1]), dtype=np.uint8)
+        rec[:, 0:4] = np.frombuffer(np.int32(l).astype("<i4").tobytes(), dtype=np.uint8)
+        rec[:, 4:12] = np.arange(n_tokens, dtype="<i8").view(np.uint8).reshape(n_tokens, 8)
+        rec[:, 12:12 + kb.shape[1]] = kb
+        rec[:, 12 + kb.shape[1]:] = vb
+        h = fnv1a64(rec.tobytes(), h)
+    if h is None:
+        h = fnv1a64(b"")
+    return h
+
+
+def memory_model_bytes(num_layers, d, n_ctx, sizeof) -> int:
+    """Eq. (memory): M_KV = 2 * L * d * n_ctx * sizeof(dtype)."""
+    return 2 * num_layers * d * n_ctx * sizeof
+
+
+def query_macs(n_cached: int, m: int, num_q_heads: int, d: int) -> int:
+    """MACs of QK^T for m new rows over n cached keys ("O(m*n)"):
+    Hq * d * sum_{i<m} (n + i + 1)  (the same count again for PV)."""
+    return num_q_heads * d * (m * n_cached + m * (m + 1) // 2)
