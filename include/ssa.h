@@ -1,0 +1,316 @@
+/*
+ * ssa.h — C ABI of the B200-native stateful-session attention library
+ * (libssa.so), the data-parallel hot path of arXiv 2605.13784 ("stateful
+ * sessions").  Citations "P:n" are lines of the paper text;
+ * "R-n" are the readings listed in DESIGN.md §3.
+ *
+ * The paper's problem statement (§2): a context
+ *     C = [S; D_1; ...; D_k]
+ * of a static prefix S and appended data segments D_i, against which queries
+ * Q_j are answered without re-processing C.  The library keeps C as a paged,
+ * append-only KV cache per session and computes, on the GPU:
+ *   - data plane:  the attention rows of each new segment D_k over all cached
+ *                  keys plus D_k itself, causally (Alg. 1), and
+ *                  appends D_k's K/V to the cache;
+ *   - query plane: the attention rows of a query q (Alg. 2) or of
+ *                  a batch of registered Flash Queries f_i (Eq. flash-eval
+ *                  P:406, Alg. 3) over the same cache, without
+ *                  changing it.
+ * Attention is Eq. (attention), softmax(Q K^T / sqrt(d_k)) V, with the
+ * cached-context decomposition of Eq. (query-attention) P:150-155.
+ *
+ * ----------------------------------------------------------------------------
+ * Conventions (apply to every call)
+ * ----------------------------------------------------------------------------
+ * Tensors.  Q/K/V/O are plain pointers to contiguous row-major arrays
+ *   [L'][n][H][d] of the store dtype (bf16 as uint16 bit patterns, or fp32),
+ *   where L' = num_layers for all-layer calls (layer == -1) and L' = 1 for
+ *   single-layer calls, n is the number of new tokens, H = num_q_heads for Q
+ *   and O and num_kv_heads for K and V, d = head_dim.  Inputs are post-RoPE
+ *   (R-6): positions only define order and causality.  Q head h attends with
+ *   KV head h / (num_q_heads / num_kv_heads) (GQA, R-5).
+ * Host or device.  Each pointer may be device memory or host memory (pinned
+ *   or pageable); the library detects which.  Host inputs are copied to
+ *   store-owned staging buffers on `stream`; a host O is copied back on
+ *   `stream` — synchronize `stream` before reading it.
+ * Streams.  `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *   stream).  All device work of a call is enqueued on it, in call order.
+ * Ownership.  The caller owns Q/K/V/O and `stream` and keeps device buffers
+ *   alive until the stream has passed the call.  The store owns the KV pool,
+ *   page tables, staging and scratch memory, and its NCCL communicator.
+ * Host metadata.  Page reservation, n_tokens and version change at call time
+ *   (the device work that fills the pages is stream-ordered after it).
+ * Errors.  Validation and capacity errors (INVALID_ARG, UNKNOWN_SESSION,
+ *   POOL_EXHAUSTED, SESSION_LIMIT, UNSUPPORTED) return synchronously and leave
+ *   NO state change; page reservation is all-or-none.  A CUDA or NCCL failure
+ *   marks the store failed (sticky): every later call returns SSA_ERR_STATE.
+ *   ssa_last_error() returns a message for the calling thread's last error.
+ * Threading.  One host thread at a time per store (external serialization —
+ *   the paper's single dispatch worker).  Distinct stores are
+ *   independent.  Sessions never see each other's keys.
+ */
+#ifndef SSA_H_
+#define SSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSA_ABI_VERSION 1
+
+typedef enum {
+    SSA_OK = 0,
+    SSA_ERR_INVALID_ARG = -1,     /* bad shape/pointer/argument; no state change */
+    SSA_ERR_UNKNOWN_SESSION = -2, /* session id not live          */
+    SSA_ERR_POOL_EXHAUSTED = -3,  /* not enough free pages           */
+    SSA_ERR_SESSION_LIMIT = -4,   /* max_sessions live sessions already          */
+    SSA_ERR_CUDA = -5,            /* CUDA runtime/launch failure (store failed)  */
+    SSA_ERR_NCCL = -6,            /* NCCL failure (store failed)                 */
+    SSA_ERR_UNSUPPORTED = -7,     /* shape/dtype not supported by this build     */
+    SSA_ERR_STATE = -8            /* store previously failed, or call order bad  */
+} ssa_status;
+
+typedef enum { SSA_BF16 = 0, SSA_FP32 = 1 } ssa_dtype;
+
+/* Store configuration.  The KV pool holds num_pages pages per layer; a page
+ * is page_size token slots of one (layer, kv head) — see DESIGN.md §5 for the
+ * HBM layout [L][num_pages][Hkv][page_size][d] of the K and V pools.
+ * softmax_scale <= 0 selects 1/sqrt(head_dim) (Eq. attention; R-1). */
+typedef struct {
+    int32_t num_layers;
+    int32_t num_q_heads;
+    int32_t num_kv_heads;   /* must divide num_q_heads */
+    int32_t head_dim;       /* fp32: <= 128; bf16: 64 or 128 */
+    int32_t page_size;      /* power of two, 16..256 (R-9) */
+    int64_t num_pages;      /* pages per layer */
+    int32_t max_sessions;
+    int32_t device;         /* CUDA device ordinal */
+    ssa_dtype dtype;
+    float softmax_scale;
+} ssa_store_config;
+
+typedef struct ssa_store *ssa_store_t;
+typedef int32_t ssa_session_t;
+
+/* Bytes of the K+V pools for `cfg`: 2 * L * num_pages * Hkv * page_size * d *
+ * sizeof(dtype) — the paged form of Eq. (memory), with the GQA
+ * KV width Hkv*d in place of the model dimension (R-13). 0 on bad config. */
+size_t ssa_store_pool_bytes(const ssa_store_config *cfg);
+
+/* Create a store on cfg->device: allocates and zero-fills the KV pools.
+ * *out receives the handle.  INVALID_ARG on a bad config; CUDA on allocation
+ * failure (nothing is leaked). */
+ssa_status ssa_store_create(const ssa_store_config *cfg, ssa_store_t *out);
+
+/* Synchronizes the device, then frees every resource of the store. */
+ssa_status ssa_store_destroy(ssa_store_t store);
+
+/* Pages in use / pages in the pool (per layer).  Occupancy in the paper's
+ * "cells" is used_pages * page_size * num_layers slots. */
+ssa_status ssa_store_occupancy(ssa_store_t store, int64_t *used_pages, int64_t *total_pages);
+
+/* ----------------------------------------------------------------------------
+ * Data plane
+ * -------------------------------------------------------------------------- */
+
+/* Create a session whose Region 0 (the static prefix S, processed once at
+ * initialization) is the n_prefix tokens given.  Q/K/V: [L][n_prefix]
+ * [H][d].  O (may be NULL): [L][n_prefix][Hq][d] — the causal self-attention
+ * rows of S.  K/V are written into freshly reserved pages (lowest free page
+ * id first; R0 is padded to a page boundary, R-9).  version becomes 1.
+ * Errors: INVALID_ARG (n_prefix <= 0, NULL K/V), SESSION_LIMIT,
+ * POOL_EXHAUSTED. */
+ssa_status ssa_session_create(ssa_store_t store, int32_t n_prefix,
+                              const void *Q, const void *K, const void *V, void *O,
+                              void *stream, ssa_session_t *out);
+
+/* Append data segment D_k of n_new tokens (Alg. 1 "K.append(Forward(
+ * tokens, K))"; "only the delta is processed and appended"):
+ * computes the attention rows of D_k over the cached keys and D_k itself
+ * (row t sees new tokens 0..t, R-2), writes O (may be NULL), scatters D_k's
+ * K/V into the session's pages (bit-exact copy), commits n_tokens += n_new
+ * and version += 1.  Q/K/V/O: [L][n_new][H][d].  *new_version may be
+ * NULL.  Errors: INVALID_ARG (n_new <= 0), UNKNOWN_SESSION, POOL_EXHAUSTED. */
+ssa_status ssa_session_append(ssa_store_t store, ssa_session_t session, int32_t n_new,
+                              const void *Q, const void *K, const void *V, void *O,
+                              void *stream, uint64_t *new_version);
+
+/* Per-layer form for a model whose layer l+1 input depends on layer l's O:
+ * begin reserves the pages for n_new tokens (all-or-none) and returns a
+ * ticket; layer(l) computes layer l's rows and scatters its K/V (Q/K/V/O:
+ * [1][n_new][H][d]); commit publishes n_tokens/version after every layer was
+ * run exactly once.  abort releases the reservation (no state change).
+ * Only one open ticket per session; errors: STATE on misuse. */
+ssa_status ssa_append_begin(ssa_store_t store, ssa_session_t session, int32_t n_new,
+                            int32_t *ticket);
+ssa_status ssa_append_layer(ssa_store_t store, ssa_session_t session, int32_t ticket,
+                            int32_t layer, const void *Q, const void *K, const void *V,
+                            void *O, void *stream);
+ssa_status ssa_append_commit(ssa_store_t store, ssa_session_t session, int32_t ticket,
+                             uint64_t *new_version);
+ssa_status ssa_append_abort(ssa_store_t store, ssa_session_t session, int32_t ticket);
+
+/* SeqRemove(s, p, inf) (Alg. 3 L540/L547): drop tokens at positions
+ * >= p (0 <= p <= n_tokens), free pages no longer needed (the first page is
+ * kept if any slot of it is still used), version += 1 when tokens were
+ * removed.  Host metadata only. */
+ssa_status ssa_session_truncate(ssa_store_t store, ssa_session_t session, int64_t p,
+                                uint64_t *new_version);
+
+/* Destroy a session, returning its pages to the pool. */
+ssa_status ssa_session_destroy(ssa_store_t store, ssa_session_t session);
+
+/* ----------------------------------------------------------------------------
+ * Query plane — never changes pages, page table, n_tokens or version (R-3)
+ * -------------------------------------------------------------------------- */
+
+/* Query q of n_q tokens (Alg. 2 "Forward(tokens_q, K)  O(|q|) not
+ * O(|K|)") against the session's cache: row t sees every cached token
+ * and q's tokens 0..t.  q's own K/V are read from the K/V arguments (Region 2
+ * scratch, "cleared between queries") and never written to pages.
+ * layer == -1: all layers, Q/K/V/O [L][n_q][H][d]; else that layer only,
+ * [1][n_q][H][d]. */
+ssa_status ssa_session_query(ssa_store_t store, ssa_session_t session, int32_t layer,
+                             int32_t n_q, const void *Q, const void *K, const void *V,
+                             void *O, void *stream);
+
+/* Flash Query batch (Eq. flash-eval; Alg. 3): k registered
+ * questions f_1..f_k evaluated against cache version t in ONE launch; f_i
+ * sees the cache plus its own tokens only, never another f_j (R-4).
+ * q_lens (host, k entries > 0); Q/K/V/O are packed varlen over the questions
+ * in order: [L'][sum q_lens][H][d], L' as for ssa_session_query. */
+ssa_status ssa_flash_query_batch(ssa_store_t store, ssa_session_t session, int32_t layer,
+                                 int32_t k, const int32_t *q_lens, const void *Q,
+                                 const void *K, const void *V, void *O, void *stream);
+
+/* ----------------------------------------------------------------------------
+ * Multi-tenant varlen batch (admit-many / run-few; R-7)
+ * -------------------------------------------------------------------------- */
+typedef enum {
+    SSA_WORK_APPEND = 0,     /* data-plane append D_k of `session`           */
+    SSA_WORK_QUERY = 1,      /* query-plane rows of `session`, no state change */
+    SSA_WORK_STATELESS = 2   /* stateless prompt: causal prefill over its own
+                                tokens only, K/V discarded (R-16) */
+} ssa_work_kind;
+
+typedef struct {
+    int32_t kind;            /* ssa_work_kind */
+    ssa_session_t session;   /* ignored for STATELESS */
+    int32_t n_tokens;        /* > 0 */
+    int32_t reserved;
+    int64_t row_offset;      /* first token row of this item in Q/K/V/O */
+} ssa_work_item;
+
+/* Run n_items heterogeneous items in one launch per layer.  Q/K/V/O are packed
+ * [L'][n_rows][H][d] with n_rows = max(row_offset + n_tokens) and L' as for
+ * ssa_session_query.  Snapshot semantics (R-7): every item reads the cache as
+ * of the call; APPEND items reserve their pages in item order (all-or-none
+ * over the batch) and publish n_tokens/version when the call returns (layer ==
+ * -1) or on the call for layer num_layers-1 (per-layer use: call layers 0..L-1
+ * in order with the same items).  At most one APPEND item per session. */
+ssa_status ssa_batch_run(ssa_store_t store, int32_t layer, int32_t n_items,
+                         const ssa_work_item *items, const void *Q, const void *K,
+                         const void *V, void *O, void *stream);
+
+/* ----------------------------------------------------------------------------
+ * Introspection (tests, not hot path)
+ * -------------------------------------------------------------------------- */
+typedef struct {
+    int64_t n_tokens;   /* retained tokens */
+    int64_t n_prefix;   /* Region 0 length */
+    int64_t n_pages;    /* pages held (per layer) */
+    uint64_t version;   /* data version t */
+} ssa_session_info;
+
+ssa_status ssa_session_get_info(ssa_store_t store, ssa_session_t session, ssa_session_info *out);
+
+/* Copy the session's page table (int32 page ids, in slot order) to host
+ * `out` (capacity `cap`); *n_out = number of entries. */
+ssa_status ssa_session_page_table(ssa_store_t store, ssa_session_t session, int32_t *out,
+                                  int64_t cap, int64_t *n_out);
+
+/* Gather tokens [start, start+count) of `layer` from the pages into
+ * K_out/V_out [count][Hkv][d] (host or device), bit-exact; synchronous. */
+ssa_status ssa_session_read_kv(ssa_store_t store, ssa_session_t session, int32_t layer,
+                               int64_t start, int64_t count, void *K_out, void *V_out);
+
+/* Bulk import of `count` tokens appended to the session without computing
+ * attention (building a long session, e.g. the 128k split-KV config):
+ * K/V [L][count][Hkv][d].  Reserves pages, scatters, version += 1. */
+ssa_status ssa_session_load_kv(ssa_store_t store, ssa_session_t session, int64_t count,
+                               const void *K, const void *V, void *stream);
+
+/* FNV-1a-64 digest of the retained K/V: over layers, then tokens, the
+ * records int32 LE layer || int64 LE token || K bytes || V bytes (SPEC
+ * S:158-166).  Reads the pages back; synchronous. */
+ssa_status ssa_session_digest(ssa_store_t store, ssa_session_t session, uint64_t *out);
+
+/* Counters since store creation (or the last reset). */
+typedef struct {
+    int64_t kernel_launches;     /* kernels this library launched */
+    int64_t rows_computed;       /* attention rows = tokens * num_q_heads * layers */
+    int64_t query_rows;          /* subset of rows_computed from the query plane */
+    int64_t tokens_appended;     /* tokens written to pages (per layer counted once) */
+    int64_t pages_reserved;
+    int64_t h2d_bytes;           /* host staging copies */
+    int64_t d2h_bytes;
+} ssa_stats;
+
+ssa_status ssa_store_stats(ssa_store_t store, ssa_stats *out, int32_t reset);
+
+/* Options (tests / benchmarking). */
+typedef enum {
+    SSA_OPT_ATTN_BACKEND = 1,   /* 0 auto, 1 SIMT kernels only, 2 tcgen05 when eligible */
+    SSA_OPT_MAX_SPLITS = 2,     /* cap on split-KV factor (0 = auto) */
+    SSA_OPT_FAULT_INJECT = 3,   /* negative controls: 0 none, 1 drop last key tile,
+                                   2 causal off-by-one (row t misses its own key) */
+    SSA_OPT_TC_Q_TILES = 4      /* tcgen05 Q tiles per CTA (1 or 2; 0 = auto) */
+} ssa_option;
+ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
+
+/* ----------------------------------------------------------------------------
+ * Multi-GPU split-KV for one long session (R-12)
+ * -------------------------------------------------------------------------- */
+/* NCCL unique id (128 bytes) for rank 0 to broadcast through any channel
+ * (e.g. a torch.distributed process group). */
+ssa_status ssa_comm_unique_id(uint8_t out[128]);
+
+/* Join the store to a `world`-rank NCCL communicator on its device. */
+ssa_status ssa_comm_init(ssa_store_t store, int32_t rank, int32_t world, const uint8_t id[128]);
+
+/* Query against a session sharded by contiguous token ranges over the ranks
+ * (each rank's store holds its shard as an ordinary session, rank r holding
+ * tokens [r*n/G, (r+1)*n/G)).  Each rank computes the partial (O_r, lse_r)
+ * of all n_q rows over its shard; the tail owner (rank world-1) also covers
+ * q's own tokens; partials are exchanged with one ncclAllGather on `stream`
+ * and merged (log-sum-exp) so every rank returns the full O. */
+ssa_status ssa_sharded_query(ssa_store_t store, ssa_session_t session, int32_t layer,
+                             int32_t n_q, const void *Q, const void *K, const void *V,
+                             void *O, void *stream);
+
+ssa_status ssa_comm_destroy(ssa_store_t store);
+
+/* ----------------------------------------------------------------------------
+ * Diagnostics
+ * -------------------------------------------------------------------------- */
+const char *ssa_status_str(ssa_status s);
+const char *ssa_last_error(void);
+int32_t ssa_abi_version(void);
+
+/* Host-only planner introspection (tests; no GPU needed): plans the split-KV
+ * work units for n_segs segments of seg_m[i] new tokens over seg_slots[i]
+ * cached slots and writes up to cap_units units as 8 int32 each
+ * (seg, kv_head, q_tok0, q_ntok, tile_lo, tile_hi, group, split) into
+ * units_out (may be NULL).  Returns the number of units. */
+int32_t ssa_debug_plan(int32_t n_segs, const int32_t *seg_m, const int32_t *seg_slots,
+                       int32_t Hkv, int32_t q_tile_tokens, int32_t key_tile, int32_t n_layers,
+                       int32_t num_sms, int32_t ctas_per_sm, int32_t max_splits,
+                       int32_t *units_out, int32_t cap_units);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSA_H_ */

@@ -1,0 +1,314 @@
+"""Python binding of libssa — B200-native stateful-session attention.
+
+Thin marshalling over the C ABI in ``include/ssa.h`` (same names, minus the
+``ssa_`` prefix): every step of the hot path runs in the library's sm_100a
+kernels.  Arguments may be torch tensors (CUDA or CPU), numpy arrays or raw
+integer pointers.  There is no fallback: if ``libssa.so`` is missing or fails to
+load, importing this package raises.
+
+Shapes follow the ABI: Q/O ``[L'][n][Hq][d]``, K/V ``[L'][n][Hkv][d]`` with
+L' = num_layers for all-layer calls (``layer=-1``) and 1 for single-layer calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", "WORK_STATELESS",
+           "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "debug_plan"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libssa.so")
+
+WORK_APPEND, WORK_QUERY, WORK_STATELESS = 0, 1, 2
+OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES = 1, 2, 3, 4
+BF16, FP32 = 0, 1
+
+_STATUS = {0: "SSA_OK", -1: "SSA_ERR_INVALID_ARG", -2: "SSA_ERR_UNKNOWN_SESSION", -3: "SSA_ERR_POOL_EXHAUSTED",
+           -4: "SSA_ERR_SESSION_LIMIT", -5: "SSA_ERR_CUDA", -6: "SSA_ERR_NCCL", -7: "SSA_ERR_UNSUPPORTED",
+           -8: "SSA_ERR_STATE"}
+
+
+class SsaError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: {_STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = _STATUS.get(code, str(code))
+
+
+class StoreConfig(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("num_pages", ctypes.c_int64),
+                ("max_sessions", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
+
+
+class SessionInfo(ctypes.Structure):
+    _fields_ = [("n_tokens", ctypes.c_int64), ("n_prefix", ctypes.c_int64),
+                ("n_pages", ctypes.c_int64), ("version", ctypes.c_uint64)]
+
+
+class WorkItem(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("session", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("row_offset", ctypes.c_int64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("kernel_launches", "rows_computed", "query_rows",
+                                              "tokens_appended", "pages_reserved", "h2d_bytes", "d2h_bytes")]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libssa.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+    P = ctypes.POINTER
+    sig = {
+        "ssa_store_pool_bytes": (ctypes.c_size_t, [P(StoreConfig)]),
+        "ssa_store_create": (i32, [P(StoreConfig), P(vp)]),
+        "ssa_store_destroy": (i32, [vp]),
+        "ssa_store_occupancy": (i32, [vp, P(i64), P(i64)]),
+        "ssa_session_create": (i32, [vp, i32, vp, vp, vp, vp, vp, P(i32)]),
+        "ssa_session_append": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, P(u64)]),
+        "ssa_append_begin": (i32, [vp, i32, i32, P(i32)]),
+        "ssa_append_layer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "ssa_append_commit": (i32, [vp, i32, i32, P(u64)]),
+        "ssa_append_abort": (i32, [vp, i32, i32]),
+        "ssa_session_truncate": (i32, [vp, i32, i64, P(u64)]),
+        "ssa_session_destroy": (i32, [vp, i32]),
+        "ssa_session_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "ssa_flash_query_batch": (i32, [vp, i32, i32, i32, P(i32), vp, vp, vp, vp, vp]),
+        "ssa_batch_run": (i32, [vp, i32, i32, P(WorkItem), vp, vp, vp, vp, vp]),
+        "ssa_session_get_info": (i32, [vp, i32, P(SessionInfo)]),
+        "ssa_session_page_table": (i32, [vp, i32, P(i32), i64, P(i64)]),
+        "ssa_session_read_kv": (i32, [vp, i32, i32, i64, i64, vp, vp]),
+        "ssa_session_load_kv": (i32, [vp, i32, i64, vp, vp, vp]),
+        "ssa_session_digest": (i32, [vp, i32, P(u64)]),
+        "ssa_store_stats": (i32, [vp, P(Stats), i32]),
+        "ssa_store_set_option": (i32, [vp, i32, i64]),
+        "ssa_comm_unique_id": (i32, [P(ctypes.c_uint8)]),
+        "ssa_comm_init": (i32, [vp, i32, i32, P(ctypes.c_uint8)]),
+        "ssa_sharded_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "ssa_comm_destroy": (i32, [vp]),
+        "ssa_status_str": (ctypes.c_char_p, [i32]),
+        "ssa_last_error": (ctypes.c_char_p, []),
+        "ssa_abi_version": (i32, []),
+        "ssa_debug_plan": (i32, [i32, P(i32), P(i32), i32, i32, i32, i32, i32, i32, i32, P(i32), i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise SsaError(rc, where, (lib.ssa_last_error() or b"").decode())
+
+
+def _ptr(x):
+    """Raw address of a torch tensor / numpy array / int / None (no copies)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ntok(x, axis=1):
+    return int(x.shape[axis])
+
+
+class Store:
+    """A KV pool on one GPU plus its sessions (see include/ssa.h)."""
+
+    def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, page_size=64, num_pages=1024,
+                 max_sessions=64, device=0, dtype="bf16", softmax_scale=0.0):
+        self.cfg = StoreConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
+                               max_sessions, device, BF16 if dtype == "bf16" else FP32, softmax_scale)
+        self.dtype = dtype
+        self.L, self.hq, self.hkv, self.d, self.P = num_layers, num_q_heads, num_kv_heads, head_dim, page_size
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(lib.ssa_store_create(ctypes.byref(self.cfg), ctypes.byref(h)), "store_create")
+        self._h = h
+
+    @staticmethod
+    def pool_bytes(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages, dtype="bf16"):
+        c = StoreConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages, 1, 0,
+                        BF16 if dtype == "bf16" else FP32, 0.0)
+        return int(lib.ssa_store_pool_bytes(ctypes.byref(c)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ssa_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- data plane ---------------------------------------------------------
+    def session_create(self, Q, K, V, O=None, stream=None, n_prefix=None):
+        n = n_prefix if n_prefix is not None else _ntok(K)
+        sid = ctypes.c_int32()
+        _check(lib.ssa_session_create(self._h, n, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _stream(stream),
+                                      ctypes.byref(sid)), "session_create")
+        return sid.value
+
+    def session_append(self, sid, Q, K, V, O=None, stream=None, n_new=None):
+        n = n_new if n_new is not None else _ntok(K)
+        ver = ctypes.c_uint64()
+        _check(lib.ssa_session_append(self._h, sid, n, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _stream(stream),
+                                      ctypes.byref(ver)), "session_append")
+        return ver.value
+
+    def append_begin(self, sid, n_new):
+        t = ctypes.c_int32()
+        _check(lib.ssa_append_begin(self._h, sid, n_new, ctypes.byref(t)), "append_begin")
+        return t.value
+
+    def append_layer(self, sid, ticket, layer, Q, K, V, O=None, stream=None):
+        _check(lib.ssa_append_layer(self._h, sid, ticket, layer, _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
+                                    _stream(stream)), "append_layer")
+
+    def append_commit(self, sid, ticket):
+        ver = ctypes.c_uint64()
+        _check(lib.ssa_append_commit(self._h, sid, ticket, ctypes.byref(ver)), "append_commit")
+        return ver.value
+
+    def append_abort(self, sid, ticket):
+        _check(lib.ssa_append_abort(self._h, sid, ticket), "append_abort")
+
+    def session_truncate(self, sid, p):
+        ver = ctypes.c_uint64()
+        _check(lib.ssa_session_truncate(self._h, sid, p, ctypes.byref(ver)), "session_truncate")
+        return ver.value
+
+    def session_destroy(self, sid):
+        _check(lib.ssa_session_destroy(self._h, sid), "session_destroy")
+
+    # -- query plane ----------------------------------------------------------
+    def session_query(self, sid, Q, K, V, O, layer=-1, stream=None, n_q=None):
+        n = n_q if n_q is not None else _ntok(K)
+        _check(lib.ssa_session_query(self._h, sid, layer, n, _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
+                                     _stream(stream)), "session_query")
+
+    def flash_query_batch(self, sid, q_lens, Q, K, V, O, layer=-1, stream=None):
+        arr = (ctypes.c_int32 * len(q_lens))(*q_lens)
+        _check(lib.ssa_flash_query_batch(self._h, sid, layer, len(q_lens), arr, _ptr(Q), _ptr(K), _ptr(V),
+                                         _ptr(O), _stream(stream)), "flash_query_batch")
+
+    def batch_run(self, items, Q, K, V, O, layer=-1, stream=None):
+        """items: list of (kind, session, n_tokens, row_offset)."""
+        arr = (WorkItem * len(items))(*[WorkItem(k, s, n, 0, r) for (k, s, n, r) in items])
+        _check(lib.ssa_batch_run(self._h, layer, len(items), arr, _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
+                                 _stream(stream)), "batch_run")
+
+    # -- introspection --------------------------------------------------------
+    def info(self, sid):
+        i = SessionInfo()
+        _check(lib.ssa_session_get_info(self._h, sid, ctypes.byref(i)), "session_get_info")
+        return dict(n_tokens=i.n_tokens, n_prefix=i.n_prefix, n_pages=i.n_pages, version=i.version)
+
+    def page_table(self, sid):
+        n = ctypes.c_int64()
+        _check(lib.ssa_session_page_table(self._h, sid, None, 0, ctypes.byref(n)), "session_page_table")
+        buf = (ctypes.c_int32 * max(1, n.value))()
+        _check(lib.ssa_session_page_table(self._h, sid, buf, n.value, ctypes.byref(n)), "session_page_table")
+        return list(buf[:n.value])
+
+    def read_kv(self, sid, layer, start, count):
+        import numpy as np
+        dt = np.uint16 if self.dtype == "bf16" else np.float32
+        K = np.zeros((count, self.hkv, self.d), dtype=dt)
+        V = np.zeros_like(K)
+        _check(lib.ssa_session_read_kv(self._h, sid, layer, start, count, _ptr(K), _ptr(V)), "session_read_kv")
+        return K, V
+
+    def load_kv(self, sid, K, V, stream=None):
+        _check(lib.ssa_session_load_kv(self._h, sid, _ntok(K), _ptr(K), _ptr(V), _stream(stream)),
+               "session_load_kv")
+
+    def digest(self, sid):
+        h = ctypes.c_uint64()
+        _check(lib.ssa_session_digest(self._h, sid, ctypes.byref(h)), "session_digest")
+        return h.value
+
+    def occupancy(self):
+        u, t = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.ssa_store_occupancy(self._h, ctypes.byref(u), ctypes.byref(t)), "store_occupancy")
+        return u.value, t.value
+
+    def stats(self, reset=False):
+        s = Stats()
+        _check(lib.ssa_store_stats(self._h, ctypes.byref(s), int(reset)), "store_stats")
+        return {n: getattr(s, n) for n, _ in Stats._fields_}
+
+    def set_option(self, option, value):
+        _check(lib.ssa_store_set_option(self._h, option, value), "store_set_option")
+
+    # -- multi-GPU split-KV ---------------------------------------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib.ssa_comm_unique_id(buf), "comm_unique_id")
+        return bytes(buf)
+
+    def comm_init(self, rank, world, uid: bytes):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib.ssa_comm_init(self._h, rank, world, buf), "comm_init")
+
+    def sharded_query(self, sid, Q, K, V, O, layer=-1, stream=None, n_q=None):
+        n = n_q if n_q is not None else _ntok(K)
+        _check(lib.ssa_sharded_query(self._h, sid, layer, n, _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
+                                     _stream(stream)), "sharded_query")
+
+
+def debug_plan(seg_m, seg_slots, Hkv, q_tile_tokens, key_tile, n_layers=1, num_sms=148, ctas_per_sm=1,
+               max_splits=0):
+    """Planner introspection (host only): list of units (seg, kvh, tok0, ntok, tile_lo, tile_hi, group, split)."""
+    n = len(seg_m)
+    m = (ctypes.c_int32 * n)(*seg_m)
+    s = (ctypes.c_int32 * n)(*seg_slots)
+    cnt = lib.ssa_debug_plan(n, m, s, Hkv, q_tile_tokens, key_tile, n_layers, num_sms, ctas_per_sm, max_splits,
+                             None, 0)
+    buf = (ctypes.c_int32 * (8 * max(1, cnt)))()
+    lib.ssa_debug_plan(n, m, s, Hkv, q_tile_tokens, key_tile, n_layers, num_sms, ctas_per_sm, max_splits, buf, cnt)
+    return [tuple(buf[8 * i:8 * i + 8]) for i in range(cnt)]

@@ -1,0 +1,333 @@
+// kernels_simt.cu — CUDA-core kernels of the session-attention path (sm_100a).
+//
+//   attn_simt     split-KV attention of a q tile over paged cached keys plus the
+//                 segment's own keys (causal), online softmax in fp32.  Used for
+//                 fp32 mode (KS, 1e-5 parity) and for small-row bf16 work (KD,
+//                 e.g. 1-token queries at 4 FLOP/B where tensor cores do not pay).
+//   combine       log-sum-exp merge of split partials (KC; reading R-11).
+//   scatter       append of new K/V rows into pages (KA; bit-exact, Alg. 1).
+//   gather        read-back of pages (tests / digest only).
+//
+// Math (Eq. attention): s = scale*q.k, p = exp(s - m),
+// o = sum p v / sum p.  We fold scale*log2(e) into q and use exp2.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "ssa_internal.h"
+
+namespace ssa {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kBK = 64;   // keys per SIMT tile
+constexpr int kRT = 32;   // rows per SIMT unit
+
+__device__ __forceinline__ float ld_f(const float* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ float ld_f(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+__device__ __forceinline__ void st_f(float* p, int64_t i, float v) { p[i] = v; }
+__device__ __forceinline__ void st_f(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p) {
+  constexpr int NV = kRT * D / kThreads;      // O accumulators per thread
+  constexpr int KS = D + 1;                   // padded K row (bank-conflict free dots)
+  extern __shared__ float smem[];
+  float* Qs = smem;                           // [kRT][D]
+  float* Ks = Qs + kRT * D;                   // [kBK][D+1]
+  float* Vs = Ks + kBK * KS;                  // [kBK][D]
+  float* Ss = Vs + kBK * D;                   // [kRT][kBK]
+  float* mrow = Ss + kRT * kBK;               // running max (log2 domain)
+  float* lrow = mrow + kRT;                   // running sum
+  float* arow = lrow + kRT;                   // rescale factor of this tile
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int u = blockIdx.x, ly = blockIdx.y;
+  const WorkUnit wu = p.units[u];
+  const SegDesc sg = p.segs[wu.seg];
+  const int G = p.G;
+  const int rows = wu.q_ntok * G;
+  const int64_t layer = p.layer0 + ly;
+  const int64_t in_row0 = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0;
+  const T* Q = static_cast<const T*>(p.Q);
+  const T* Kt = static_cast<const T*>(p.Kt);
+  const T* Vt = static_cast<const T*>(p.Vt);
+  const T* PK = static_cast<const T*>(p.poolK);
+  const T* PV = static_cast<const T*>(p.poolV);
+
+  for (int idx = tid; idx < kRT * D; idx += kThreads) {
+    const int r = idx / D, e = idx % D;
+    float v = 0.f;
+    if (r < rows) {
+      const int64_t row = in_row0 + wu.q_tok0 + r / G;
+      const int h = wu.kv_head * G + r % G;
+      v = ld_f(Q, (row * p.Hq + h) * D + e) * p.scale_log2;
+    }
+    Qs[idx] = v;
+  }
+  if (tid < kRT) { mrow[tid] = -CUDART_INF_F; lrow[tid] = 0.f; }
+  float acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+
+  const int n_pool_tiles = (sg.n_slots + kBK - 1) / kBK;
+  for (int tile = wu.tile_lo; tile < wu.tile_hi; ++tile) {
+    const bool is_pool = tile < n_pool_tiles;
+    const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBK;
+    __syncthreads();
+    for (int idx = tid; idx < kBK * D; idx += kThreads) {
+      const int j = idx / D, e = idx % D;
+      float kv = 0.f, vv = 0.f;
+      const int key = key0 + j;
+      if (is_pool) {
+        if (key < sg.n_slots && !(key >= sg.hole_lo && key < sg.hole_hi)) {
+          const int64_t page = sg.pages[key / p.P];
+          const int64_t off = (((layer * p.num_pages + page) * p.Hkv + wu.kv_head) * p.P + key % p.P) * D + e;
+          kv = ld_f(PK, off);
+          vv = ld_f(PV, off);
+        }
+      } else if (key < sg.m) {
+        const int64_t off = ((in_row0 + key) * p.Hkv + wu.kv_head) * D + e;
+        kv = ld_f(Kt, off);
+        vv = ld_f(Vt, off);
+      }
+      Ks[j * KS + e] = kv;
+      Vs[j * D + e] = vv;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kRT * kBK; idx += kThreads) {
+      const int r = idx / kBK, j = idx % kBK;
+      const int key = key0 + j;
+      bool valid = r < rows;
+      if (is_pool) {
+        valid = valid && key < sg.n_slots && !(key >= sg.hole_lo && key < sg.hole_hi);
+      } else {
+        const int tok = wu.q_tok0 + r / G;
+        valid = valid && key < sg.m && (p.fault == 2 ? key < tok : key <= tok);
+      }
+      float s = -CUDART_INF_F;
+      if (valid) {
+        const float* q = Qs + r * D;
+        const float* k = Ks + j * KS;
+        float a = 0.f;
+#pragma unroll 16
+        for (int e = 0; e < D; ++e) a = fmaf(q[e], k[e], a);
+        s = a;
+      }
+      Ss[idx] = s;
+    }
+    __syncthreads();
+    for (int r = warp; r < kRT; r += kThreads / 32) {
+      const float s0 = Ss[r * kBK + lane], s1 = Ss[r * kBK + lane + 32];
+      const float m_old = mrow[r];
+      const float m_new = fmaxf(m_old, warp_max(fmaxf(s0, s1)));
+      float p0 = 0.f, p1 = 0.f, alpha = 1.f;
+      if (m_new != -CUDART_INF_F) {
+        p0 = exp2f(s0 - m_new);
+        p1 = exp2f(s1 - m_new);
+        alpha = exp2f(m_old - m_new);
+      }
+      const float sum = warp_sum(p0 + p1);
+      Ss[r * kBK + lane] = p0;
+      Ss[r * kBK + lane + 32] = p1;
+      if (lane == 0) {
+        lrow[r] = lrow[r] * alpha + sum;
+        mrow[r] = m_new;
+        arow[r] = alpha;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = tid + i * kThreads;
+      const int r = idx / D, e = idx % D;
+      float a = acc[i] * arow[r];
+      const float* pr = Ss + r * kBK;
+#pragma unroll 8
+      for (int j = 0; j < kBK; ++j) a = fmaf(pr[j], Vs[j * D + e], a);
+      acc[i] = a;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int idx = tid + i * kThreads;
+    const int r = idx / D, e = idx % D;
+    if (r >= rows) continue;
+    const float l = lrow[r];
+    const float o = l > 0.f ? acc[i] / l : 0.f;
+    if (wu.group < 0) {
+      const int64_t row = in_row0 + wu.q_tok0 + r / G;
+      const int h = wu.kv_head * G + r % G;
+      st_f(static_cast<T*>(p.O), (row * p.Hq + h) * D + e, o);
+    } else {
+      const int64_t slot = (int64_t)ly * p.n_units + u;
+      p.part_o[(slot * kRT + r) * D + e] = o;
+      if (e == 0) p.part_lse[slot * kRT + r] = l > 0.f ? mrow[r] + log2f(l) : -CUDART_INF_F;
+    }
+  }
+}
+
+// One warp per output row of a group; lanes stride over d.  Partials carry
+// (o_s normalized, lse_s in log2 units); o = sum_s 2^(lse_s - L) o_s / sum_s 2^(lse_s - L).
+template <typename T>
+__global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
+  const int g = blockIdx.x, ly = blockIdx.y;
+  const Group gr = p.groups[g];
+  const SegDesc sg = p.segs[gr.seg];
+  const int rows = gr.q_ntok * p.G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t in_row0 = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0;
+  for (int r = warp; r < rows; r += blockDim.x / 32) {
+    float L = -CUDART_INF_F;
+    for (int s = lane; s < gr.n_splits; s += 32) {
+      const int64_t slot = (int64_t)ly * p.n_units + gr.unit0 + s;
+      L = fmaxf(L, p.part_lse[slot * p.rows_tile + r]);
+    }
+    L = warp_max(L);
+    float wsum = 0.f;
+    for (int s = lane; s < gr.n_splits; s += 32) {
+      const int64_t slot = (int64_t)ly * p.n_units + gr.unit0 + s;
+      const float ls = p.part_lse[slot * p.rows_tile + r];
+      if (ls != -CUDART_INF_F) wsum += exp2f(ls - L);
+    }
+    wsum = warp_sum(wsum);
+    const int64_t row = in_row0 + gr.q_tok0 + r / p.G;
+    const int h = gr.kv_head * p.G + r % p.G;
+    for (int e = lane; e < p.D; e += 32) {
+      float acc = 0.f;
+      for (int s = 0; s < gr.n_splits; ++s) {
+        const int64_t slot = (int64_t)ly * p.n_units + gr.unit0 + s;
+        const float ls = p.part_lse[slot * p.rows_tile + r];
+        if (ls != -CUDART_INF_F) acc = fmaf(exp2f(ls - L), p.part_o[(slot * p.rows_tile + r) * p.D + e], acc);
+      }
+      if (p.write_o) st_f(static_cast<T*>(p.O), (row * p.Hq + h) * p.D + e, wsum > 0.f ? acc / wsum : 0.f);
+    }
+    if (p.lse_out && lane == 0)
+      p.lse_out[((int64_t)ly * p.n_groups + g) * p.rows_tile + r] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+  }
+}
+
+// 16-byte chunks: (token, kv head, chunk).  Bit-exact copy into pages.
+__global__ void __launch_bounds__(256) scatter_kernel(const ScatterParams p) {
+  const int ly = blockIdx.y;
+  const int64_t layer = p.layer0 + ly;
+  const int chunks = p.D * p.elem_bytes / 16;
+  const int64_t total = p.total_tokens * p.Hkv * chunks;
+  const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = idx % chunks;
+    const int h = (idx / chunks) % p.Hkv;
+    const int64_t t = idx / ((int64_t)chunks * p.Hkv);
+    int lo = 0, hi = p.n_segs;  // find seg with tok_prefix[s] <= t < tok_prefix[s+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (p.tok_prefix[mid] <= t) lo = mid; else hi = mid;
+    }
+    const SegDesc sg = p.segs[lo];
+    const int64_t tl = t - p.tok_prefix[lo];
+    const int64_t slot = sg.append_slot0 + tl;
+    const int64_t page = sg.pages[slot / p.P];
+    const int64_t src = ((in_l + sg.row0 + tl) * p.Hkv + h) * (int64_t)p.D * p.elem_bytes + c * 16;
+    const int64_t dst = (((layer * p.num_pages + page) * p.Hkv + h) * p.P + slot % p.P) * (int64_t)p.D * p.elem_bytes + c * 16;
+    const int4 kv = *reinterpret_cast<const int4*>(static_cast<const char*>(p.K) + src);
+    const int4 vv = *reinterpret_cast<const int4*>(static_cast<const char*>(p.V) + src);
+    *reinterpret_cast<int4*>(static_cast<char*>(p.poolK) + dst) = kv;
+    *reinterpret_cast<int4*>(static_cast<char*>(p.poolV) + dst) = vv;
+  }
+}
+
+__global__ void __launch_bounds__(256) gather_kernel(const GatherParams p) {
+  const int chunks = p.D * p.elem_bytes / 16;
+  const int64_t total = p.count * p.Hkv * chunks;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = idx % chunks;
+    const int h = (idx / chunks) % p.Hkv;
+    const int64_t tl = idx / ((int64_t)chunks * p.Hkv);
+    const int64_t t = p.start + tl;
+    const int64_t slot = (p.n_prefix_slots_pad >= 0 && t >= p.n_prefix) ? p.n_prefix_slots_pad + (t - p.n_prefix) : t;
+    const int64_t page = p.pages[slot / p.P];
+    const int64_t src = ((((int64_t)p.layer * p.num_pages + page) * p.Hkv + h) * p.P + slot % p.P) * (int64_t)p.D * p.elem_bytes + c * 16;
+    const int64_t dst = (tl * p.Hkv + h) * (int64_t)p.D * p.elem_bytes + c * 16;
+    *reinterpret_cast<int4*>(static_cast<char*>(p.K) + dst) = *reinterpret_cast<const int4*>(static_cast<const char*>(p.poolK) + src);
+    *reinterpret_cast<int4*>(static_cast<char*>(p.V) + dst) = *reinterpret_cast<const int4*>(static_cast<const char*>(p.poolV) + src);
+  }
+}
+
+template <typename T, int D>
+cudaError_t launch_simt_t(const AttnParams& p, int n_layers, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (kRT * D + kBK * (D + 1) + kBK * D + kRT * kBK + 3 * kRT);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_simt_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(p.n_units, n_layers);
+  attn_simt_kernel<T, D><<<grid, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int simt_rows_tile(int G, int D) { (void)G; (void)D; return kRT; }
+int simt_key_tile() { return kBK; }
+
+cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s) {
+  if (p.n_units == 0 || n_layers == 0) return cudaSuccess;
+  switch (p.D) {
+#define SSA_CASE(DD)                                                                  \
+  case DD:                                                                            \
+    return bf16 ? launch_simt_t<__nv_bfloat16, DD>(p, n_layers, s) : launch_simt_t<float, DD>(p, n_layers, s);
+    SSA_CASE(16)
+    SSA_CASE(32)
+    SSA_CASE(64)
+    SSA_CASE(128)
+#undef SSA_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s) {
+  if (p.n_groups == 0 || n_layers == 0) return cudaSuccess;
+  dim3 grid(p.n_groups, n_layers);
+  if (bf16) combine_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(p);
+  else combine_kernel<float><<<grid, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s) {
+  if (p.total_tokens == 0 || n_layers == 0) return cudaSuccess;
+  const int64_t work = p.total_tokens * p.Hkv * (p.D * p.elem_bytes / 16);
+  int blocks = (int)((work + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  dim3 grid(blocks, n_layers);
+  scatter_kernel<<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const GatherParams& p, cudaStream_t s) {
+  if (p.count == 0) return cudaSuccess;
+  const int64_t work = p.count * p.Hkv * (p.D * p.elem_bytes / 16);
+  int blocks = (int)((work + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gather_kernel<<<blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ssa

@@ -1,0 +1,103 @@
+// plan.cpp — split-KV work planner (host, integer only).
+//
+// Turns the segments of one call into CTA work units: for every segment,
+// every q tile of `q_tile_tokens` tokens and every KV head, the key tiles
+// (cached pool tiles, then the segment's own tiles up to the q tile's last
+// token — causal, reading R-2) are split into contiguous ranges so that the
+// launch fills the GPU (148 SMs on B200).  Units of one (segment, q tile, kv
+// head) form a Group merged by the combine kernel (log-sum-exp, reading R-11).
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "plan.h"
+
+namespace ssa {
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out) {
+  out->units.clear();
+  out->groups.clear();
+  struct Item { int seg, kvh, tok0, ntok; int64_t tiles, pool_tiles; };
+  std::vector<Item> items;
+  int64_t total_tiles = 0;
+  for (int s = 0; s < (int)segs.size(); ++s) {
+    const SegDesc& sg = segs[s];
+    const int64_t pool_tiles = ceil_div(sg.n_slots, c.key_tile);
+    for (int tok0 = 0; tok0 < sg.m; tok0 += c.q_tile_tokens) {
+      const int ntok = std::min(c.q_tile_tokens, sg.m - tok0);
+      const int64_t tail_tiles = ceil_div(tok0 + ntok, c.key_tile);
+      for (int h = 0; h < c.Hkv; ++h) {
+        items.push_back({s, h, tok0, ntok, pool_tiles + tail_tiles, pool_tiles});
+        total_tiles += pool_tiles + tail_tiles;
+      }
+    }
+  }
+  if (items.empty()) return;
+  // Makespan model: waves * (tiles per unit + fixed per-unit overhead).  Pick
+  // the tiles-per-unit that minimises it (ties -> fewer splits).
+  const int64_t slots = std::max<int64_t>(1, (int64_t)c.num_sms * c.ctas_per_sm);
+  int64_t max_tiles = 0;
+  for (auto& it : items) max_tiles = std::max(max_tiles, it.tiles);
+  int64_t best_tpu = max_tiles;
+  double best_cost = 1e300;
+  const int max_splits = c.max_splits > 0 ? c.max_splits : 1 << 20;
+  std::vector<int64_t> cands;
+  for (int64_t t = std::max<int64_t>(1, c.min_tiles_per_unit); t <= max_tiles;
+       t = t < 32 ? t + 1 : std::max<int64_t>(t + 1, (int64_t)(t * 1.06))) cands.push_back(t);
+  if (cands.empty() || cands.back() != max_tiles) cands.push_back(std::max<int64_t>(1, max_tiles));
+  for (int64_t tpu : cands) {
+    int64_t units = 0;
+    bool ok = true;
+    for (auto& it : items) {
+      const int64_t n = ceil_div(it.tiles, tpu);
+      if (n > max_splits) { ok = false; break; }
+      units += n;
+    }
+    if (!ok) continue;
+    units *= c.n_layers;
+    const double waves = (double)ceil_div(units, slots);
+    const double per_unit = (double)std::min<int64_t>(tpu, max_tiles) + c.unit_overhead_tiles;
+    const double cost = waves * per_unit + 1e-3 * (double)units / (double)slots;
+    if (cost < best_cost - 1e-9) { best_cost = cost; best_tpu = tpu; }
+    if (units <= c.n_layers * (int64_t)items.size()) break;  // no more splitting possible
+  }
+  if (best_cost > 1e299) {  // max_splits binds: split each item into max_splits
+    best_tpu = 0;
+  }
+  // Order groups by per-unit work, largest first (LPT over the CTA rasterizer).
+  std::vector<int> order(items.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  auto n_splits_of = [&](const Item& it) -> int64_t {
+    int64_t n = best_tpu > 0 ? ceil_div(it.tiles, best_tpu) : std::min<int64_t>(max_splits, it.tiles);
+    return std::max<int64_t>(1, std::min<int64_t>(n, std::max<int64_t>(1, it.tiles)));
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const double wa = (double)items[a].tiles / (double)n_splits_of(items[a]);
+    const double wb = (double)items[b].tiles / (double)n_splits_of(items[b]);
+    return wa > wb;
+  });
+  for (int idx : order) {
+    const Item& it = items[idx];
+    const int64_t n = n_splits_of(it);
+    const int unit0 = (int)out->units.size();
+    const int group = n > 1 ? (int)out->groups.size() : -1;
+    for (int64_t s = 0; s < n; ++s) {
+      WorkUnit u;
+      u.seg = it.seg;
+      u.kv_head = it.kvh;
+      u.q_tok0 = it.tok0;
+      u.q_ntok = it.ntok;
+      u.tile_lo = (int)(it.tiles * s / n);
+      u.tile_hi = (int)(it.tiles * (s + 1) / n);
+      u.group = group;
+      u.split = (int)s;
+      if (c.fault == 1 && s == n - 1) u.tile_hi = std::max(u.tile_lo, u.tile_hi - 1);
+      out->units.push_back(u);
+    }
+    if (group >= 0) out->groups.push_back({it.seg, it.kvh, it.tok0, it.ntok, unit0, (int)n});
+  }
+}
+
+}  // namespace ssa

@@ -1,0 +1,29 @@
+// plan.h — split-KV work planner (host).
+#pragma once
+#include <vector>
+
+#include "ssa_internal.h"
+
+namespace ssa {
+
+struct PlanConfig {
+  int Hkv = 1;
+  int q_tile_tokens = 1;     // tokens per q tile (rows_tile / G)
+  int key_tile = 64;         // keys per tile
+  int n_layers = 1;          // grid.y of the launch
+  int num_sms = 148;
+  int ctas_per_sm = 1;
+  int max_splits = 0;        // 0 = unlimited
+  int min_tiles_per_unit = 1;
+  double unit_overhead_tiles = 1.0;
+  int fault = 0;
+};
+
+struct Plan {
+  std::vector<WorkUnit> units;
+  std::vector<Group> groups;
+};
+
+void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out);
+
+}  // namespace ssa

@@ -1,0 +1,167 @@
+// ssa_internal.h — internal descriptors shared by the host core (store.cpp,
+// plan.cpp) and the sm_100a kernels (*.cu).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "ssa.h"
+
+namespace ssa {
+
+// A segment is a run of m new tokens of one session (or a stateless prompt)
+// whose rows attend to the session's cached keys followed by the segment's own
+// keys, causally (Eq. query-attention; reading R-2).
+struct SegDesc {
+  int64_t row0;          // first token row of the segment in the packed inputs
+  int32_t m;             // tokens in the segment (length of the "tail" key source)
+  int32_t n_slots;       // slot extent of the visible cached keys (0: none)
+  int32_t hole_lo;       // slots [hole_lo, hole_hi) hold no token (R0 page pad, R-9)
+  int32_t hole_hi;
+  int32_t append_slot0;  // slot of the first new token when the segment is appended, else -1
+  int32_t n_pages;       // entries of `pages` valid for this launch
+  const int32_t* pages;  // device page table of the session (slot/P -> page id)
+};
+
+// One CTA's work: q tile (tokens [q_tok0, q_tok0+q_ntok) of segment `seg`, all
+// G query heads of KV head `kv_head`) over key tiles [tile_lo, tile_hi) of the
+// segment's tile list (pool tiles first, then tail tiles).
+struct WorkUnit {
+  int32_t seg;
+  int32_t kv_head;
+  int32_t q_tok0;
+  int32_t q_ntok;
+  int32_t tile_lo;
+  int32_t tile_hi;
+  int32_t group;   // combine group (partial output) or -1 (write O directly)
+  int32_t split;   // index of this unit within its group
+};
+
+// Output group: the splits of one (segment, kv head, q tile) to be merged.
+struct Group {
+  int32_t seg;
+  int32_t kv_head;
+  int32_t q_tok0;
+  int32_t q_ntok;
+  int32_t unit0;     // first unit index (units of a group are contiguous)
+  int32_t n_splits;
+};
+
+struct AttnParams {
+  const void* Q;         // [n_layers_in][rows_per_layer][Hq][D]
+  const void* Kt;        // [n_layers_in][rows_per_layer][Hkv][D]  (segment "tail" keys)
+  const void* Vt;
+  void* O;               // like Q
+  int64_t rows_per_layer;
+  int32_t layer0;        // pool layer of grid.y == 0
+  int32_t in_layer_stride;  // 1 if inputs carry a layer dimension per grid.y, else 0
+  const void* poolK;     // [L][num_pages][Hkv][P][D]
+  const void* poolV;
+  int64_t num_pages;
+  int32_t Hq, Hkv, D, P, G;
+  float scale_log2;      // softmax_scale * log2(e)
+  const SegDesc* segs;
+  const WorkUnit* units;
+  int32_t n_units;       // per layer
+  const Group* groups;
+  int32_t n_groups;      // per layer
+  float* part_o;         // [layers][n_units][rows_tile][D]
+  float* part_lse;       // [layers][n_units][rows_tile]
+  int32_t rows_tile;     // rows per unit (q tile tokens * G)
+  int32_t key_tile;      // keys per tile (SIMT 64, tcgen05 128)
+  int32_t fault;         // SSA_OPT_FAULT_INJECT
+};
+
+// Append scatter (KA): copy new K/V rows into pages, bit-exact.
+struct ScatterParams {
+  const void* K;         // [n_layers][rows_per_layer][Hkv][D]
+  const void* V;
+  int64_t rows_per_layer;
+  int32_t layer0;
+  int32_t in_layer_stride;
+  void* poolK;
+  void* poolV;
+  int64_t num_pages;
+  int32_t Hkv, D, P, elem_bytes;
+  const SegDesc* segs;   // segments with append_slot0 >= 0
+  const int32_t* tok_prefix;  // [n_segs+1] prefix sums of m over segs
+  int32_t n_segs;
+  int64_t total_tokens;
+};
+
+// Gather (read-back) of tokens [start, start+count) of one layer.
+struct GatherParams {
+  const void* poolK;
+  const void* poolV;
+  void* K;               // [count][Hkv][D]
+  void* V;
+  int64_t num_pages;
+  int32_t layer, Hkv, D, P, elem_bytes;
+  int64_t start, count;
+  int32_t n_prefix_slots_pad;  // slot of token n_prefix (R0 padded) or -1
+  int64_t n_prefix;
+  const int32_t* pages;
+};
+
+// Merge of split partials into O.
+struct CombineParams {
+  const float* part_o;
+  const float* part_lse;
+  void* O;
+  float* lse_out;        // optional [layers][groups][rows_tile]
+  const SegDesc* segs;
+  const Group* groups;
+  int32_t n_groups;
+  int32_t n_units;
+  int32_t rows_tile;
+  int64_t rows_per_layer;
+  int32_t in_layer_stride;
+  int32_t Hq, G, D;
+  int32_t write_o;
+};
+
+// Kernel launchers (kernels_*.cu).  Return cudaGetLastError() after launch.
+cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s);
+cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s);
+cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
+cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
+int simt_rows_tile(int G, int D);     // rows per SIMT unit
+int simt_key_tile();                  // keys per SIMT tile
+
+// ---------------------------------------------------------------------------
+// Host-side helpers
+// ---------------------------------------------------------------------------
+
+// Pinned host ring with a device mirror for per-call uploads (work lists,
+// page-table deltas).  Regions are reused only after the event recorded
+// behind their consumers has completed.
+class UploadRing {
+ public:
+  ~UploadRing();
+  cudaError_t init(size_t cap);
+  // Reserve n bytes (256-aligned); returns offset or SIZE_MAX on failure.
+  size_t alloc(size_t n);
+  char* host(size_t off) { return h_ + off; }
+  char* dev(size_t off) { return d_ + off; }
+  cudaError_t to_device(size_t off, size_t n, cudaStream_t s) {
+    return cudaMemcpyAsync(d_ + off, h_ + off, n, cudaMemcpyHostToDevice, s);
+  }
+  // Mark [lo, hi) busy until work now enqueued on `s` completes.
+  cudaError_t fence(size_t lo, size_t hi, cudaStream_t s);
+  size_t capacity() const { return cap_; }
+
+ private:
+  struct Span { size_t lo, hi; cudaEvent_t ev; };
+  char* h_ = nullptr;
+  char* d_ = nullptr;
+  size_t cap_ = 0, head_ = 0;
+  std::deque<Span> busy_;
+  std::vector<cudaEvent_t> free_events_;
+  cudaError_t retire_overlapping(size_t lo, size_t hi);
+};
+
+}  // namespace ssa

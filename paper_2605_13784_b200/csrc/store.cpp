@@ -1,0 +1,1081 @@
+// store.cpp — host core of libssa: KV pool, deterministic page allocator,
+// sessions (Region 0 / Region 1 bookkeeping, data version t), call planning
+// and the C ABI of include/ssa.h.  All device work is enqueued on the
+// caller's stream; no computation of attention happens on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+#include "ssa.h"
+#include "ssa_internal.h"
+#include "store.h"
+
+namespace ssa {
+
+thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+// ---------------------------------------------------------------- UploadRing
+UploadRing::~UploadRing() {
+  for (auto& s : busy_) cudaEventDestroy(s.ev);
+  for (auto e : free_events_) cudaEventDestroy(e);
+  if (h_) cudaFreeHost(h_);
+  if (d_) cudaFree(d_);
+}
+
+cudaError_t UploadRing::init(size_t cap) {
+  cap_ = cap;
+  cudaError_t e = cudaMallocHost(&h_, cap);
+  if (e != cudaSuccess) return e;
+  return cudaMalloc(&d_, cap);
+}
+
+cudaError_t UploadRing::retire_overlapping(size_t lo, size_t hi) {
+  while (!busy_.empty()) {
+    Span& f = busy_.front();
+    if (f.hi <= lo || f.lo >= hi) break;
+    cudaError_t e = cudaEventSynchronize(f.ev);
+    if (e != cudaSuccess) return e;
+    free_events_.push_back(f.ev);
+    busy_.pop_front();
+  }
+  return cudaSuccess;
+}
+
+size_t UploadRing::alloc(size_t n) {
+  n = (n + 255) & ~size_t(255);
+  if (n > cap_) return SIZE_MAX;
+  if (head_ + n > cap_) head_ = 0;
+  // Retire every older span that overlaps [head_, head_+n) (in ring order).
+  while (!busy_.empty()) {
+    bool overlap = false;
+    for (auto& s : busy_)
+      if (!(s.hi <= head_ || s.lo >= head_ + n)) { overlap = true; break; }
+    if (!overlap) break;
+    Span f = busy_.front();
+    if (cudaEventSynchronize(f.ev) != cudaSuccess) return SIZE_MAX;
+    free_events_.push_back(f.ev);
+    busy_.pop_front();
+  }
+  const size_t off = head_;
+  head_ += n;
+  return off;
+}
+
+cudaError_t UploadRing::fence(size_t lo, size_t hi, cudaStream_t s) {
+  cudaEvent_t ev;
+  if (!free_events_.empty()) {
+    ev = free_events_.back();
+    free_events_.pop_back();
+  } else {
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaEventRecord(ev, s);
+  if (e != cudaSuccess) return e;
+  busy_.push_back({lo, hi, ev});
+  return cudaSuccess;
+}
+
+}  // namespace ssa
+
+using namespace ssa;
+
+// ============================================================================
+// helpers
+// ============================================================================
+#define SSA_CHECK_STORE(st)                                       \
+  do {                                                            \
+    if (!(st)) { set_error("null store"); return SSA_ERR_INVALID_ARG; } \
+    if ((st)->failed) { set_error("store failed earlier: %s", (st)->fail_msg.c_str()); return SSA_ERR_STATE; } \
+  } while (0)
+
+#define SSA_CUDA(st, expr)                                                   \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess) return (st)->cuda_fail(_e, #expr, __LINE__);      \
+  } while (0)
+
+ssa_status ssa_store::cuda_fail(cudaError_t e, const char* what, int line) {
+  failed = true;
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %s (%s) at store.cpp:%d in %s", cudaGetErrorName(e),
+           cudaGetErrorString(e), line, what);
+  fail_msg = buf;
+  set_error("%s", buf);
+  return SSA_ERR_CUDA;
+}
+
+static int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int64_t ssa_store::pad_prefix(int64_t n_prefix) const { return ceil_div64(n_prefix, cfg.page_size) * cfg.page_size; }
+
+// Slot of token t of a session (reading R-9: R0 padded to a page boundary).
+int64_t ssa_store::slot_of(const Session& s, int64_t t) const {
+  return t < s.n_prefix ? t : pad_prefix(s.n_prefix) + (t - s.n_prefix);
+}
+int64_t ssa_store::slots_for(const Session& s, int64_t n) const {
+  return n <= s.n_prefix ? n : pad_prefix(s.n_prefix) + (n - s.n_prefix);
+}
+int64_t ssa_store::pages_for(const Session& s, int64_t n) const {
+  return ceil_div64(slots_for(s, n), cfg.page_size);
+}
+
+Session* ssa_store::get(ssa_session_t id) {
+  if (id < 0 || id >= (int)sessions.size() || !sessions[id].live) return nullptr;
+  return &sessions[id];
+}
+
+// Reserve pages so that the session can hold n_total tokens; all-or-none.
+ssa_status ssa_store::reserve(Session& s, int64_t n_total, std::vector<int32_t>* got) {
+  const int64_t need = pages_for(s, n_total) - (int64_t)s.pages.size();
+  got->clear();
+  if (need <= 0) return SSA_OK;
+  if (need > (int64_t)free_pages.size()) {
+    set_error("pool exhausted: need %lld pages, %zu free", (long long)need, free_pages.size());
+    return SSA_ERR_POOL_EXHAUSTED;
+  }
+  for (int64_t i = 0; i < need; ++i) {
+    got->push_back(free_pages.top());
+    free_pages.pop();
+  }
+  stats.pages_reserved += need;
+  return SSA_OK;
+}
+
+void ssa_store::release(const std::vector<int32_t>& pages) {
+  for (int32_t p : pages) free_pages.push(p);
+}
+
+// Append page ids to the session's host table and upload the delta.
+ssa_status ssa_store::push_pages(Session& s, const std::vector<int32_t>& pages, cudaStream_t st) {
+  if (pages.empty()) return SSA_OK;
+  const int64_t old = (int64_t)s.pages.size();
+  s.pages.insert(s.pages.end(), pages.begin(), pages.end());
+  const int64_t n = (int64_t)s.pages.size();
+  if (n > s.d_cap) {
+    int64_t cap = std::max<int64_t>(64, s.d_cap);
+    while (cap < n) cap *= 2;
+    int32_t* nd = nullptr;
+    SSA_CUDA(this, cudaMallocAsync((void**)&nd, cap * sizeof(int32_t), st));
+    if (s.d_pages) {
+      SSA_CUDA(this, cudaMemcpyAsync(nd, s.d_pages, s.d_valid * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      SSA_CUDA(this, cudaFreeAsync(s.d_pages, st));
+    }
+    s.d_pages = nd;
+    s.d_cap = cap;
+  }
+  // Entries [min(old, d_valid), n) are (re)uploaded: truncate may have lowered d_valid.
+  const int64_t lo = std::min<int64_t>(old, s.d_valid);
+  const size_t bytes = (n - lo) * sizeof(int32_t);
+  const size_t off = ring.alloc(bytes);
+  if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(page table)", __LINE__);
+  memcpy(ring.host(off), s.pages.data() + lo, bytes);
+  SSA_CUDA(this, cudaMemcpyAsync(s.d_pages + lo, ring.host(off), bytes, cudaMemcpyHostToDevice, st));
+  SSA_CUDA(this, ring.fence(off, off + bytes, st));
+  s.d_valid = n;
+  return SSA_OK;
+}
+
+void ssa_store::fill_cached(const Session& s, SegDesc* sg) const {
+  sg->n_slots = (int32_t)slots_for(s, s.n_tokens);
+  if (s.n_tokens > s.n_prefix) {
+    sg->hole_lo = (int32_t)s.n_prefix;
+    sg->hole_hi = (int32_t)pad_prefix(s.n_prefix);
+  } else {
+    sg->hole_lo = sg->hole_hi = 0;
+  }
+  sg->pages = s.d_pages;
+  sg->n_pages = (int32_t)s.pages.size();
+}
+
+ssa_status ssa_store::ensure_scratch(size_t part_o_floats, size_t part_lse_floats, cudaStream_t st) {
+  if (part_o_floats > part_o_cap || part_lse_floats > part_lse_cap) {
+    SSA_CUDA(this, cudaStreamSynchronize(st));
+    SSA_CUDA(this, cudaDeviceSynchronize());
+    if (part_o) cudaFree(part_o);
+    if (part_lse) cudaFree(part_lse);
+    part_o = nullptr;
+    part_lse = nullptr;
+    part_o_cap = std::max(part_o_floats, part_o_cap * 2);
+    part_lse_cap = std::max(part_lse_floats, part_lse_cap * 2);
+    SSA_CUDA(this, cudaMalloc(&part_o, part_o_cap * sizeof(float)));
+    SSA_CUDA(this, cudaMalloc(&part_lse, part_lse_cap * sizeof(float)));
+  }
+  return SSA_OK;
+}
+
+// --------------------------------------------------------------- staging
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+ssa_status ssa_store::stage_inputs(IoSet* io, cudaStream_t st) {
+  // Place every host pointer of the call in one device staging buffer.
+  size_t need = 0;
+  auto plan_one = [&](IoBuf& b) {
+    b.dev = nullptr;
+    b.host = nullptr;
+    if (!b.user || b.bytes == 0) return;
+    if (is_device_ptr(b.user)) { b.dev = const_cast<void*>(b.user); return; }
+    b.host = const_cast<void*>(b.user);
+    b.stage_off = need;
+    need += (b.bytes + 255) & ~size_t(255);
+  };
+  plan_one(io->q); plan_one(io->k); plan_one(io->v); plan_one(io->o);
+  if (need > stage_cap) {
+    SSA_CUDA(this, cudaDeviceSynchronize());
+    if (stage) cudaFree(stage);
+    stage = nullptr;
+    stage_cap = std::max(need, stage_cap * 2);
+    SSA_CUDA(this, cudaMalloc(&stage, stage_cap));
+  }
+  for (IoBuf* b : {&io->q, &io->k, &io->v, &io->o}) {
+    if (!b->host) continue;
+    b->dev = static_cast<char*>(stage) + b->stage_off;
+    if (b != &io->o) {
+      SSA_CUDA(this, cudaMemcpyAsync(b->dev, b->host, b->bytes, cudaMemcpyHostToDevice, st));
+      stats.h2d_bytes += (int64_t)b->bytes;
+    }
+  }
+  return SSA_OK;
+}
+
+ssa_status ssa_store::unstage_output(IoSet* io, cudaStream_t st) {
+  if (io->o.host) {
+    SSA_CUDA(this, cudaMemcpyAsync(io->o.host, io->o.dev, io->o.bytes, cudaMemcpyDeviceToHost, st));
+    stats.d2h_bytes += (int64_t)io->o.bytes;
+  }
+  return SSA_OK;
+}
+
+// --------------------------------------------------------------- one launch
+// Runs KA (scatter of appended segments) and the attention kernels for `segs`
+// over input layers [0, n_layers) mapped to pool layers layer0 + y.
+ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t rows_per_layer,
+                          int32_t layer0, int32_t n_layers, int32_t in_layer_stride, bool compute_o,
+                          bool query_plane, cudaStream_t st) {
+  const int G = cfg.num_q_heads / cfg.num_kv_heads;
+  const int D = cfg.head_dim;
+  // ---- plan attention
+  Plan plan;
+  PlanConfig pc;
+  const bool use_tc = compute_o && tc_eligible(segs);
+  if (compute_o) {
+    pc.Hkv = cfg.num_kv_heads;
+    pc.key_tile = use_tc ? tc_key_tile() : simt_key_tile();
+    pc.q_tile_tokens = std::max(1, (use_tc ? tc_rows_tile() : simt_rows_tile(G, D)) / G);
+    pc.n_layers = n_layers;
+    pc.num_sms = num_sms;
+    pc.ctas_per_sm = use_tc ? 1 : 2;
+    pc.max_splits = (int)opt_max_splits;
+    pc.min_tiles_per_unit = use_tc ? 2 : 2;
+    pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
+    pc.fault = (int)opt_fault;
+    plan_units(segs, pc, &plan);
+  }
+  // ---- append segments for the scatter
+  std::vector<int32_t> app_idx;
+  for (int i = 0; i < (int)segs.size(); ++i)
+    if (segs[i].append_slot0 >= 0) app_idx.push_back(i);
+  std::vector<SegDesc> app_segs;
+  std::vector<int32_t> prefix(1, 0);
+  for (int i : app_idx) {
+    app_segs.push_back(segs[i]);
+    prefix.push_back(prefix.back() + segs[i].m);
+  }
+  // ---- upload descriptors through the ring (one span)
+  const size_t b_segs = segs.size() * sizeof(SegDesc);
+  const size_t b_units = plan.units.size() * sizeof(WorkUnit);
+  const size_t b_groups = plan.groups.size() * sizeof(Group);
+  const size_t b_app = app_segs.size() * sizeof(SegDesc);
+  const size_t b_pre = prefix.size() * sizeof(int32_t);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre);
+  const size_t off = ring.alloc(total);
+  if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
+  size_t o = off;
+  auto put = [&](const void* src, size_t b) {
+    const size_t here = o;
+    if (b) memcpy(ring.host(here), src, b);
+    o += al(b);
+    return ring.dev(here);
+  };
+  auto d_segs = reinterpret_cast<const SegDesc*>(put(segs.data(), b_segs));
+  auto d_units = reinterpret_cast<const WorkUnit*>(put(plan.units.data(), b_units));
+  auto d_groups = reinterpret_cast<const Group*>(put(plan.groups.data(), b_groups));
+  auto d_app = reinterpret_cast<const SegDesc*>(put(app_segs.data(), b_app));
+  auto d_pre = reinterpret_cast<const int32_t*>(put(prefix.data(), b_pre));
+  SSA_CUDA(this, ring.to_device(off, total, st));
+
+  // ---- KA: scatter new K/V into pages
+  if (!app_segs.empty()) {
+    ScatterParams sp{};
+    sp.K = io.k.dev;
+    sp.V = io.v.dev;
+    sp.rows_per_layer = rows_per_layer;
+    sp.layer0 = layer0;
+    sp.in_layer_stride = in_layer_stride;
+    sp.poolK = poolK;
+    sp.poolV = poolV;
+    sp.num_pages = cfg.num_pages;
+    sp.Hkv = cfg.num_kv_heads;
+    sp.D = D;
+    sp.P = cfg.page_size;
+    sp.elem_bytes = elem;
+    sp.segs = d_app;
+    sp.tok_prefix = d_pre;
+    sp.n_segs = (int32_t)app_segs.size();
+    sp.total_tokens = prefix.back();
+    SSA_CUDA(this, launch_scatter(sp, n_layers, st));
+    stats.kernel_launches++;
+  }
+  // ---- attention (+ combine)
+  if (compute_o && !plan.units.empty()) {
+    const int rows_tile = use_tc ? tc_rows_tile() : simt_rows_tile(G, D);
+    if (!plan.groups.empty()) {
+      const size_t n_po = (size_t)n_layers * plan.units.size() * rows_tile * D;
+      const size_t n_pl = (size_t)n_layers * plan.units.size() * rows_tile;
+      ssa_status s = ensure_scratch(n_po, n_pl, st);
+      if (s != SSA_OK) return s;
+    }
+    AttnParams ap{};
+    ap.Q = io.q.dev;
+    ap.Kt = io.k.dev;
+    ap.Vt = io.v.dev;
+    ap.O = io.o.dev;
+    ap.rows_per_layer = rows_per_layer;
+    ap.layer0 = layer0;
+    ap.in_layer_stride = in_layer_stride;
+    ap.poolK = poolK;
+    ap.poolV = poolV;
+    ap.num_pages = cfg.num_pages;
+    ap.Hq = cfg.num_q_heads;
+    ap.Hkv = cfg.num_kv_heads;
+    ap.D = D;
+    ap.P = cfg.page_size;
+    ap.G = G;
+    ap.scale_log2 = scale * 1.4426950408889634f;
+    ap.segs = d_segs;
+    ap.units = d_units;
+    ap.n_units = (int32_t)plan.units.size();
+    ap.groups = d_groups;
+    ap.n_groups = (int32_t)plan.groups.size();
+    ap.part_o = part_o;
+    ap.part_lse = part_lse;
+    ap.rows_tile = rows_tile;
+    ap.key_tile = pc.key_tile;
+    ap.fault = (int32_t)opt_fault;
+    if (use_tc) {
+      SSA_CUDA(this, launch_attn_tc(ap, n_layers, (int)opt_tc_qtiles, st));
+    } else {
+      SSA_CUDA(this, launch_attn_simt(ap, n_layers, cfg.dtype == SSA_BF16, st));
+    }
+    stats.kernel_launches++;
+    if (!plan.groups.empty()) {
+      CombineParams cp{};
+      cp.part_o = part_o;
+      cp.part_lse = part_lse;
+      cp.O = io.o.dev;
+      cp.lse_out = nullptr;
+      cp.segs = d_segs;
+      cp.groups = d_groups;
+      cp.n_groups = (int32_t)plan.groups.size();
+      cp.n_units = (int32_t)plan.units.size();
+      cp.rows_tile = rows_tile;
+      cp.rows_per_layer = rows_per_layer;
+      cp.in_layer_stride = in_layer_stride;
+      cp.Hq = cfg.num_q_heads;
+      cp.G = G;
+      cp.D = D;
+      cp.write_o = 1;
+      SSA_CUDA(this, launch_combine(cp, n_layers, cfg.dtype == SSA_BF16, st));
+      stats.kernel_launches++;
+    }
+    int64_t rows = 0;
+    for (auto& sg : segs) rows += (int64_t)sg.m * cfg.num_q_heads * n_layers;
+    stats.rows_computed += rows;
+    if (query_plane) stats.query_rows += rows;
+  }
+  SSA_CUDA(this, ring.fence(off, off + total, st));
+  last_plan_units = (int64_t)plan.units.size();
+  last_plan_groups = (int64_t)plan.groups.size();
+  last_used_tc = use_tc;
+  return SSA_OK;
+}
+
+bool ssa_store::tc_eligible(const std::vector<SegDesc>& segs) const {
+  if (opt_backend == 1 || !sm100) return false;
+  const int G = cfg.num_q_heads / cfg.num_kv_heads;
+  if (!tc_supported_shape(cfg.head_dim, G, cfg.dtype == SSA_BF16)) return false;
+  if (opt_backend == 2) return true;
+  // auto: tensor cores once a q tile packs >= 16 rows per KV head (SURVEY §0
+  // finding 1); 1-token GQA decode (4 rows) stays on the SIMT split-KV kernel.
+  int max_m = 0;
+  for (auto& s : segs) max_m = std::max(max_m, s.m);
+  return (int64_t)std::min(max_m, tc_rows_tile() / G) * G >= 16;
+}
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int32_t ssa_abi_version(void) { return SSA_ABI_VERSION; }
+
+const char* ssa_status_str(ssa_status s) {
+  switch (s) {
+    case SSA_OK: return "SSA_OK";
+    case SSA_ERR_INVALID_ARG: return "SSA_ERR_INVALID_ARG";
+    case SSA_ERR_UNKNOWN_SESSION: return "SSA_ERR_UNKNOWN_SESSION";
+    case SSA_ERR_POOL_EXHAUSTED: return "SSA_ERR_POOL_EXHAUSTED";
+    case SSA_ERR_SESSION_LIMIT: return "SSA_ERR_SESSION_LIMIT";
+    case SSA_ERR_CUDA: return "SSA_ERR_CUDA";
+    case SSA_ERR_NCCL: return "SSA_ERR_NCCL";
+    case SSA_ERR_UNSUPPORTED: return "SSA_ERR_UNSUPPORTED";
+    case SSA_ERR_STATE: return "SSA_ERR_STATE";
+  }
+  return "SSA_ERR_?";
+}
+
+const char* ssa_last_error(void) { return g_last_error.c_str(); }
+
+static bool valid_config(const ssa_store_config* c) {
+  if (!c) return false;
+  if (c->num_layers <= 0 || c->num_q_heads <= 0 || c->num_kv_heads <= 0) return false;
+  if (c->num_q_heads % c->num_kv_heads) return false;
+  if (c->page_size < 16 || c->page_size > 256 || (c->page_size & (c->page_size - 1))) return false;
+  if (c->num_pages <= 0 || c->max_sessions <= 0) return false;
+  if (c->dtype != SSA_BF16 && c->dtype != SSA_FP32) return false;
+  const int d = c->head_dim;
+  if (d != 16 && d != 32 && d != 64 && d != 128) return false;
+  if ((int64_t)c->num_pages * c->num_kv_heads * c->page_size >= (1LL << 31)) return false;
+  return true;
+}
+
+size_t ssa_store_pool_bytes(const ssa_store_config* c) {
+  if (!valid_config(c)) return 0;
+  const size_t elem = c->dtype == SSA_BF16 ? 2 : 4;
+  return 2 * (size_t)c->num_layers * c->num_pages * c->num_kv_heads * c->page_size * c->head_dim * elem;
+}
+
+ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
+  if (!out || !valid_config(cfg)) {
+    set_error("invalid store config");
+    return SSA_ERR_INVALID_ARG;
+  }
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
+    cudaGetLastError();
+    set_error("CUDA device %d not available (%d devices)", cfg->device, ndev);
+    return SSA_ERR_CUDA;
+  }
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) { set_error("cudaSetDevice: %s", cudaGetErrorString(e)); return SSA_ERR_CUDA; }
+  ssa_store* st = new ssa_store();
+  st->cfg = *cfg;
+  st->elem = cfg->dtype == SSA_BF16 ? 2 : 4;
+  st->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : (float)(1.0 / std::sqrt((double)cfg->head_dim));
+  cudaDeviceGetAttribute(&st->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cfg->device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cfg->device);
+  st->sm100 = (major == 10 && minor == 0);
+  const size_t half = ssa_store_pool_bytes(cfg) / 2;
+  st->pool_half_bytes = half;
+  if ((e = cudaMalloc(&st->poolK, half)) != cudaSuccess || (e = cudaMalloc(&st->poolV, half)) != cudaSuccess ||
+      (e = cudaMemset(st->poolK, 0, half)) != cudaSuccess || (e = cudaMemset(st->poolV, 0, half)) != cudaSuccess ||
+      (e = st->ring.init(8u << 20)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    set_error("store allocation failed: %s", cudaGetErrorString(e));
+    delete st;
+    return SSA_ERR_CUDA;
+  }
+  for (int64_t p = 0; p < cfg->num_pages; ++p) st->free_pages.push((int32_t)p);
+  st->sessions.reserve(std::min(cfg->max_sessions, 4096));
+  *out = st;
+  return SSA_OK;
+}
+
+ssa_store::~ssa_store() {
+  cudaDeviceSynchronize();
+  for (auto& s : sessions)
+    if (s.d_pages) cudaFree(s.d_pages);
+  if (poolK) cudaFree(poolK);
+  if (poolV) cudaFree(poolV);
+  if (part_o) cudaFree(part_o);
+  if (part_lse) cudaFree(part_lse);
+  if (stage) cudaFree(stage);
+  destroy_comm();
+}
+
+ssa_status ssa_store_destroy(ssa_store_t st) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  delete st;
+  return SSA_OK;
+}
+
+ssa_status ssa_store_occupancy(ssa_store_t st, int64_t* used, int64_t* total) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  if (used) *used = st->cfg.num_pages - (int64_t)st->free_pages.size();
+  if (total) *total = st->cfg.num_pages;
+  return SSA_OK;
+}
+
+ssa_status ssa_store_stats(ssa_store_t st, ssa_stats* out, int32_t reset) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  if (out) *out = st->stats;
+  if (reset) st->stats = ssa_stats{};
+  return SSA_OK;
+}
+
+ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  switch (option) {
+    case SSA_OPT_ATTN_BACKEND: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_backend = value; break;
+    case SSA_OPT_MAX_SPLITS: if (value < 0) return SSA_ERR_INVALID_ARG; st->opt_max_splits = value; break;
+    case SSA_OPT_FAULT_INJECT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_fault = value; break;
+    case SSA_OPT_TC_Q_TILES: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_tc_qtiles = value; break;
+    default: return SSA_ERR_INVALID_ARG;
+  }
+  return SSA_OK;
+}
+
+static size_t tensor_bytes(const ssa_store* st, int64_t layers, int64_t rows, int heads) {
+  return (size_t)layers * rows * heads * st->cfg.head_dim * st->elem;
+}
+
+// Create / append share this path: reserve, upload pages, scatter + attention, commit.
+static ssa_status do_append(ssa_store* st, Session& s, int32_t n_new, const void* Q, const void* K,
+                            const void* V, void* O, cudaStream_t stream) {
+  const int L = st->cfg.num_layers;
+  std::vector<int32_t> got;
+  ssa_status rc = st->reserve(s, s.n_tokens + n_new, &got);
+  if (rc != SSA_OK) return rc;
+  IoSet io;
+  io.q = {Q, tensor_bytes(st, L, n_new, st->cfg.num_q_heads)};
+  io.k = {K, tensor_bytes(st, L, n_new, st->cfg.num_kv_heads)};
+  io.v = {V, tensor_bytes(st, L, n_new, st->cfg.num_kv_heads)};
+  io.o = {O, tensor_bytes(st, L, n_new, st->cfg.num_q_heads)};
+  if (!O) io.q.user = nullptr;  // Q unused when no rows are requested
+  if ((rc = st->stage_inputs(&io, stream)) != SSA_OK) return rc;
+  if ((rc = st->push_pages(s, got, stream)) != SSA_OK) return rc;
+  SegDesc sg{};
+  sg.row0 = 0;
+  sg.m = n_new;
+  st->fill_cached(s, &sg);
+  sg.append_slot0 = (int32_t)st->slot_of(s, s.n_tokens);
+  std::vector<SegDesc> segs{sg};
+  if ((rc = st->run(segs, io, n_new, 0, L, 1, O != nullptr, false, stream)) != SSA_OK) return rc;
+  if ((rc = st->unstage_output(&io, stream)) != SSA_OK) return rc;
+  s.n_tokens += n_new;
+  s.version += 1;
+  st->stats.tokens_appended += n_new;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_create(ssa_store_t st, int32_t n_prefix, const void* Q, const void* K, const void* V,
+                              void* O, void* stream, ssa_session_t* out) {
+  SSA_CHECK_STORE(st);
+  if (!out || n_prefix <= 0 || !K || !V || (O && !Q)) {
+    set_error("session_create: invalid arguments");
+    return SSA_ERR_INVALID_ARG;
+  }
+  cudaSetDevice(st->cfg.device);
+  int live = 0;
+  int32_t id = -1;
+  for (int i = 0; i < (int)st->sessions.size(); ++i) {
+    if (st->sessions[i].live) live++;
+    else if (id < 0) id = i;
+  }
+  if (live >= st->cfg.max_sessions) {
+    set_error("session limit %d reached", st->cfg.max_sessions);
+    return SSA_ERR_SESSION_LIMIT;
+  }
+  if (id < 0) {
+    id = (int32_t)st->sessions.size();
+    st->sessions.emplace_back();
+  }
+  Session& s = st->sessions[id];
+  int32_t* keep_d = s.d_pages;
+  int64_t keep_cap = s.d_cap;
+  s = Session();
+  s.d_pages = keep_d;      // reuse the device table allocation of a dead slot
+  s.d_cap = keep_cap;
+  s.d_valid = 0;
+  s.n_prefix = n_prefix;
+  s.live = true;
+  ssa_status rc = do_append(st, s, n_prefix, Q, K, V, O, (cudaStream_t)stream);
+  if (rc != SSA_OK) {
+    s.live = false;
+    st->release(s.pages);
+    s.pages.clear();
+    return rc;
+  }
+  s.version = 1;
+  *out = id;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_append(ssa_store_t st, ssa_session_t id, int32_t n_new, const void* Q, const void* K,
+                              const void* V, void* O, void* stream, uint64_t* new_version) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (n_new <= 0 || !K || !V || (O && !Q)) { set_error("append: invalid arguments"); return SSA_ERR_INVALID_ARG; }
+  if (s->ticket_open) { set_error("append: a per-layer append is open"); return SSA_ERR_STATE; }
+  cudaSetDevice(st->cfg.device);
+  ssa_status rc = do_append(st, *s, n_new, Q, K, V, O, (cudaStream_t)stream);
+  if (rc == SSA_OK && new_version) *new_version = s->version;
+  return rc;
+}
+
+// ---- per-layer append tickets
+ssa_status ssa_append_begin(ssa_store_t st, ssa_session_t id, int32_t n_new, int32_t* ticket) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (n_new <= 0 || !ticket) return SSA_ERR_INVALID_ARG;
+  if (s->ticket_open) { set_error("append_begin: ticket already open"); return SSA_ERR_STATE; }
+  cudaSetDevice(st->cfg.device);
+  std::vector<int32_t> got;
+  ssa_status rc = st->reserve(*s, s->n_tokens + n_new, &got);
+  if (rc != SSA_OK) return rc;
+  const size_t before = s->pages.size();
+  if ((rc = st->push_pages(*s, got, nullptr)) != SSA_OK) return rc;
+  s->ticket_open = true;
+  s->ticket_id = ++st->ticket_seq;
+  s->ticket_n_new = n_new;
+  s->ticket_pages = (int64_t)(s->pages.size() - before);
+  s->ticket_done.assign(st->cfg.num_layers, 0);
+  *ticket = s->ticket_id;
+  return SSA_OK;
+}
+
+static Session* check_ticket(ssa_store* st, ssa_session_t id, int32_t ticket, ssa_status* rc) {
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); *rc = SSA_ERR_UNKNOWN_SESSION; return nullptr; }
+  if (!s->ticket_open || s->ticket_id != ticket) { set_error("bad ticket"); *rc = SSA_ERR_STATE; return nullptr; }
+  return s;
+}
+
+ssa_status ssa_append_layer(ssa_store_t st, ssa_session_t id, int32_t ticket, int32_t layer, const void* Q,
+                            const void* K, const void* V, void* O, void* stream) {
+  SSA_CHECK_STORE(st);
+  ssa_status rc = SSA_OK;
+  Session* s = check_ticket(st, id, ticket, &rc);
+  if (!s) return rc;
+  if (layer < 0 || layer >= st->cfg.num_layers || !K || !V || (O && !Q)) return SSA_ERR_INVALID_ARG;
+  if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
+  cudaSetDevice(st->cfg.device);
+  const int32_t n_new = s->ticket_n_new;
+  IoSet io;
+  io.q = {O ? Q : nullptr, tensor_bytes(st, 1, n_new, st->cfg.num_q_heads)};
+  io.k = {K, tensor_bytes(st, 1, n_new, st->cfg.num_kv_heads)};
+  io.v = {V, tensor_bytes(st, 1, n_new, st->cfg.num_kv_heads)};
+  io.o = {O, tensor_bytes(st, 1, n_new, st->cfg.num_q_heads)};
+  cudaStream_t cs = (cudaStream_t)stream;
+  if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
+  SegDesc sg{};
+  sg.m = n_new;
+  st->fill_cached(*s, &sg);
+  sg.append_slot0 = (int32_t)st->slot_of(*s, s->n_tokens);
+  std::vector<SegDesc> segs{sg};
+  if ((rc = st->run(segs, io, n_new, layer, 1, 0, O != nullptr, false, cs)) != SSA_OK) return rc;
+  if ((rc = st->unstage_output(&io, cs)) != SSA_OK) return rc;
+  s->ticket_done[layer] = 1;
+  return SSA_OK;
+}
+
+ssa_status ssa_append_commit(ssa_store_t st, ssa_session_t id, int32_t ticket, uint64_t* new_version) {
+  SSA_CHECK_STORE(st);
+  ssa_status rc = SSA_OK;
+  Session* s = check_ticket(st, id, ticket, &rc);
+  if (!s) return rc;
+  for (auto d : s->ticket_done)
+    if (!d) { set_error("append_commit: not every layer was appended"); return SSA_ERR_STATE; }
+  s->n_tokens += s->ticket_n_new;
+  s->version += 1;
+  st->stats.tokens_appended += s->ticket_n_new;
+  s->ticket_open = false;
+  if (new_version) *new_version = s->version;
+  return SSA_OK;
+}
+
+ssa_status ssa_append_abort(ssa_store_t st, ssa_session_t id, int32_t ticket) {
+  SSA_CHECK_STORE(st);
+  ssa_status rc = SSA_OK;
+  Session* s = check_ticket(st, id, ticket, &rc);
+  if (!s) return rc;
+  std::vector<int32_t> back(s->pages.end() - s->ticket_pages, s->pages.end());
+  s->pages.resize(s->pages.size() - s->ticket_pages);
+  s->d_valid = std::min<int64_t>(s->d_valid, (int64_t)s->pages.size());
+  st->release(back);
+  s->ticket_open = false;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_truncate(ssa_store_t st, ssa_session_t id, int64_t p, uint64_t* new_version) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (s->ticket_open) return SSA_ERR_STATE;
+  if (p < s->n_prefix || p > s->n_tokens) {
+    set_error("truncate: p=%lld outside [n_prefix=%lld, n_tokens=%lld]", (long long)p, (long long)s->n_prefix,
+              (long long)s->n_tokens);
+    return SSA_ERR_INVALID_ARG;
+  }
+  if (p < s->n_tokens) {
+    const int64_t keep = st->pages_for(*s, p);
+    std::vector<int32_t> back(s->pages.begin() + keep, s->pages.end());
+    s->pages.resize(keep);
+    s->d_valid = std::min<int64_t>(s->d_valid, keep);
+    st->release(back);
+    s->n_tokens = p;
+    s->version += 1;
+  }
+  if (new_version) *new_version = s->version;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_destroy(ssa_store_t st, ssa_session_t id) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  st->release(s->pages);
+  s->pages.clear();
+  s->d_valid = 0;
+  s->live = false;
+  s->ticket_open = false;
+  return SSA_OK;
+}
+
+// ---- query plane
+ssa_status ssa_session_query(ssa_store_t st, ssa_session_t id, int32_t layer, int32_t n_q, const void* Q,
+                             const void* K, const void* V, void* O, void* stream) {
+  int32_t len = n_q;
+  return ssa_flash_query_batch(st, id, layer, 1, &len, Q, K, V, O, stream);
+}
+
+ssa_status ssa_flash_query_batch(ssa_store_t st, ssa_session_t id, int32_t layer, int32_t k,
+                                 const int32_t* q_lens, const void* Q, const void* K, const void* V, void* O,
+                                 void* stream) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (k <= 0 || !q_lens || !Q || !K || !V || !O || layer < -1 || layer >= st->cfg.num_layers) {
+    set_error("query: invalid arguments");
+    return SSA_ERR_INVALID_ARG;
+  }
+  int64_t total = 0;
+  for (int i = 0; i < k; ++i) {
+    if (q_lens[i] <= 0) { set_error("query: q_lens[%d] <= 0", i); return SSA_ERR_INVALID_ARG; }
+    total += q_lens[i];
+  }
+  if (total >= (1LL << 31)) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;
+  IoSet io;
+  io.q = {Q, tensor_bytes(st, Lin, total, st->cfg.num_q_heads)};
+  io.k = {K, tensor_bytes(st, Lin, total, st->cfg.num_kv_heads)};
+  io.v = {V, tensor_bytes(st, Lin, total, st->cfg.num_kv_heads)};
+  io.o = {O, tensor_bytes(st, Lin, total, st->cfg.num_q_heads)};
+  cudaStream_t cs = (cudaStream_t)stream;
+  ssa_status rc = st->stage_inputs(&io, cs);
+  if (rc != SSA_OK) return rc;
+  std::vector<SegDesc> segs;
+  int64_t row = 0;
+  for (int i = 0; i < k; ++i) {
+    SegDesc sg{};
+    sg.row0 = row;
+    sg.m = q_lens[i];
+    st->fill_cached(*s, &sg);
+    sg.append_slot0 = -1;
+    segs.push_back(sg);
+    row += q_lens[i];
+  }
+  if ((rc = st->run(segs, io, total, layer < 0 ? 0 : layer, (int32_t)Lin, 1, true, true, cs)) != SSA_OK) return rc;
+  return st->unstage_output(&io, cs);
+}
+
+// ---- multi-tenant batch
+ssa_status ssa_batch_run(ssa_store_t st, int32_t layer, int32_t n_items, const ssa_work_item* items, const void* Q,
+                         const void* K, const void* V, void* O, void* stream) {
+  SSA_CHECK_STORE(st);
+  const int L = st->cfg.num_layers;
+  if (n_items <= 0 || !items || !Q || !K || !V || !O || layer < -1 || layer >= L) {
+    set_error("batch_run: invalid arguments");
+    return SSA_ERR_INVALID_ARG;
+  }
+  int64_t n_rows = 0;
+  std::vector<int32_t> app_sessions;
+  for (int i = 0; i < n_items; ++i) {
+    const ssa_work_item& it = items[i];
+    if (it.n_tokens <= 0 || it.row_offset < 0 || it.kind < 0 || it.kind > 2) return SSA_ERR_INVALID_ARG;
+    n_rows = std::max<int64_t>(n_rows, it.row_offset + it.n_tokens);
+    if (it.kind != SSA_WORK_STATELESS) {
+      Session* s = st->get(it.session);
+      if (!s) { set_error("batch_run: unknown session %d", it.session); return SSA_ERR_UNKNOWN_SESSION; }
+      if (it.kind == SSA_WORK_APPEND) {
+        if (std::find(app_sessions.begin(), app_sessions.end(), it.session) != app_sessions.end()) {
+          set_error("batch_run: two APPEND items for session %d", it.session);
+          return SSA_ERR_INVALID_ARG;
+        }
+        app_sessions.push_back(it.session);
+        const bool first = layer <= 0;
+        if (first && s->ticket_open) { set_error("batch_run: append already open"); return SSA_ERR_STATE; }
+        if (!first && (!s->ticket_open || s->ticket_n_new != it.n_tokens || !s->batch_ticket)) {
+          set_error("batch_run: per-layer batch must start at layer 0 with the same items");
+          return SSA_ERR_STATE;
+        }
+      }
+    }
+  }
+  if (n_rows >= (1LL << 31)) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  // Reserve pages for every APPEND item, in item order, all-or-none (R-7).
+  ssa_status rc = SSA_OK;
+  if (layer <= 0) {
+    std::vector<std::pair<Session*, std::vector<int32_t>>> res;
+    for (int i = 0; i < n_items; ++i) {
+      if (items[i].kind != SSA_WORK_APPEND) continue;
+      Session* s = st->get(items[i].session);
+      std::vector<int32_t> got;
+      rc = st->reserve(*s, s->n_tokens + items[i].n_tokens, &got);
+      if (rc != SSA_OK) {
+        for (auto& r : res) st->release(r.second);
+        return rc;
+      }
+      res.push_back({s, got});
+    }
+    for (auto& r : res) {
+      Session* s = r.first;
+      const size_t before = s->pages.size();
+      if ((rc = st->push_pages(*s, r.second, cs)) != SSA_OK) return rc;
+      s->ticket_open = true;
+      s->batch_ticket = true;
+      s->ticket_id = ++st->ticket_seq;
+      s->ticket_pages = (int64_t)(s->pages.size() - before);
+      s->ticket_done.assign(L, 0);
+    }
+    for (int i = 0; i < n_items; ++i)
+      if (items[i].kind == SSA_WORK_APPEND) st->get(items[i].session)->ticket_n_new = items[i].n_tokens;
+  }
+  const int64_t Lin = layer < 0 ? L : 1;
+  IoSet io;
+  io.q = {Q, tensor_bytes(st, Lin, n_rows, st->cfg.num_q_heads)};
+  io.k = {K, tensor_bytes(st, Lin, n_rows, st->cfg.num_kv_heads)};
+  io.v = {V, tensor_bytes(st, Lin, n_rows, st->cfg.num_kv_heads)};
+  io.o = {O, tensor_bytes(st, Lin, n_rows, st->cfg.num_q_heads)};
+  if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
+  std::vector<SegDesc> segs;
+  for (int i = 0; i < n_items; ++i) {
+    const ssa_work_item& it = items[i];
+    SegDesc sg{};
+    sg.row0 = it.row_offset;
+    sg.m = it.n_tokens;
+    sg.append_slot0 = -1;
+    if (it.kind == SSA_WORK_STATELESS) {
+      sg.n_slots = 0;
+      sg.pages = nullptr;
+    } else {
+      Session* s = st->get(it.session);
+      st->fill_cached(*s, &sg);  // snapshot: n_tokens of version t
+      if (it.kind == SSA_WORK_APPEND) sg.append_slot0 = (int32_t)st->slot_of(*s, s->n_tokens);
+    }
+    segs.push_back(sg);
+  }
+  if ((rc = st->run(segs, io, n_rows, layer < 0 ? 0 : layer, (int32_t)Lin, 1, true, false, cs)) != SSA_OK) return rc;
+  if ((rc = st->unstage_output(&io, cs)) != SSA_OK) return rc;
+  // Commit appends after the last layer (snapshot semantics).
+  if (layer < 0 || layer == L - 1) {
+    for (int i = 0; i < n_items; ++i) {
+      if (items[i].kind != SSA_WORK_APPEND) continue;
+      Session* s = st->get(items[i].session);
+      s->n_tokens += items[i].n_tokens;
+      s->version += 1;
+      s->ticket_open = false;
+      s->batch_ticket = false;
+      st->stats.tokens_appended += items[i].n_tokens;
+    }
+  }
+  return SSA_OK;
+}
+
+// ---- introspection
+ssa_status ssa_session_get_info(ssa_store_t st, ssa_session_t id, ssa_session_info* out) {
+  if (!st || !out) return SSA_ERR_INVALID_ARG;
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  out->n_tokens = s->n_tokens;
+  out->n_prefix = s->n_prefix;
+  out->n_pages = (int64_t)s->pages.size();
+  out->version = s->version;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_page_table(ssa_store_t st, ssa_session_t id, int32_t* out, int64_t cap, int64_t* n_out) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  const int64_t n = (int64_t)s->pages.size();
+  if (n_out) *n_out = n;
+  if (out) {
+    if (cap < n) return SSA_ERR_INVALID_ARG;
+    std::copy(s->pages.begin(), s->pages.end(), out);
+  }
+  return SSA_OK;
+}
+
+ssa_status ssa_session_read_kv(ssa_store_t st, ssa_session_t id, int32_t layer, int64_t start, int64_t count,
+                               void* K_out, void* V_out) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (layer < 0 || layer >= st->cfg.num_layers || start < 0 || count < 0 || start + count > s->n_tokens || !K_out ||
+      !V_out)
+    return SSA_ERR_INVALID_ARG;
+  if (count == 0) return SSA_OK;
+  cudaSetDevice(st->cfg.device);
+  const size_t bytes = (size_t)count * st->cfg.num_kv_heads * st->cfg.head_dim * st->elem;
+  const bool kdev = is_device_ptr(K_out), vdev = is_device_ptr(V_out);
+  void* dk = K_out;
+  void* dv = V_out;
+  void* tmp = nullptr;
+  if (!kdev || !vdev) {
+    SSA_CUDA(st, cudaMalloc(&tmp, 2 * bytes));
+    dk = tmp;
+    dv = static_cast<char*>(tmp) + bytes;
+  }
+  GatherParams gp{};
+  gp.poolK = st->poolK;
+  gp.poolV = st->poolV;
+  gp.K = dk;
+  gp.V = dv;
+  gp.num_pages = st->cfg.num_pages;
+  gp.layer = layer;
+  gp.Hkv = st->cfg.num_kv_heads;
+  gp.D = st->cfg.head_dim;
+  gp.P = st->cfg.page_size;
+  gp.elem_bytes = st->elem;
+  gp.start = start;
+  gp.count = count;
+  gp.n_prefix = s->n_prefix;
+  gp.n_prefix_slots_pad = (int32_t)st->pad_prefix(s->n_prefix);
+  gp.pages = s->d_pages;
+  SSA_CUDA(st, cudaDeviceSynchronize());
+  SSA_CUDA(st, launch_gather(gp, nullptr));
+  st->stats.kernel_launches++;
+  SSA_CUDA(st, cudaDeviceSynchronize());
+  if (tmp) {
+    SSA_CUDA(st, cudaMemcpy(K_out, dk, bytes, kdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    SSA_CUDA(st, cudaMemcpy(V_out, dv, bytes, vdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    cudaFree(tmp);
+  }
+  return SSA_OK;
+}
+
+ssa_status ssa_session_load_kv(ssa_store_t st, ssa_session_t id, int64_t count, const void* K, const void* V,
+                               void* stream) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (count <= 0 || count >= (1LL << 31) || !K || !V) return SSA_ERR_INVALID_ARG;
+  if (s->ticket_open) return SSA_ERR_STATE;
+  cudaSetDevice(st->cfg.device);
+  return do_append(st, *s, (int32_t)count, nullptr, K, V, nullptr, (cudaStream_t)stream);
+}
+
+// FNV-1a 64 over the session's records (library's own implementation; the
+// oracle has an independent one).
+static uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h) {
+  for (size_t i = 0; i < n; ++i) { h ^= p[i]; h *= 0x100000001b3ULL; }
+  return h;
+}
+
+ssa_status ssa_session_digest(ssa_store_t st, ssa_session_t id, uint64_t* out) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (!out) return SSA_ERR_INVALID_ARG;
+  uint64_t h = 0xcbf29ce484222325ULL;
+  const int64_t n = s->n_tokens;
+  const size_t row = (size_t)st->cfg.num_kv_heads * st->cfg.head_dim * st->elem;
+  std::vector<uint8_t> k(n * row), v(n * row);
+  for (int32_t l = 0; l < st->cfg.num_layers; ++l) {
+    if (n) {
+      ssa_status rc = ssa_session_read_kv(st, id, l, 0, n, k.data(), v.data());
+      if (rc != SSA_OK) return rc;
+    }
+    for (int64_t t = 0; t < n; ++t) {
+      uint8_t hdr[12];
+      const int32_t l32 = l;
+      memcpy(hdr, &l32, 4);       // little-endian host (x86-64)
+      memcpy(hdr + 4, &t, 8);
+      h = fnv1a(hdr, 12, h);
+      h = fnv1a(k.data() + t * row, row, h);
+      h = fnv1a(v.data() + t * row, row, h);
+    }
+  }
+  *out = h;
+  return SSA_OK;
+}
+
+// Planner introspection for host-logic tests (no GPU needed).
+int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_slots, int32_t Hkv,
+                       int32_t q_tile_tokens, int32_t key_tile, int32_t n_layers, int32_t num_sms,
+                       int32_t ctas_per_sm, int32_t max_splits, int32_t* units_out, int32_t cap_units) {
+  std::vector<SegDesc> segs(n_segs);
+  for (int i = 0; i < n_segs; ++i) {
+    segs[i] = SegDesc{};
+    segs[i].m = seg_m[i];
+    segs[i].n_slots = seg_slots[i];
+  }
+  PlanConfig pc;
+  pc.Hkv = Hkv;
+  pc.q_tile_tokens = q_tile_tokens;
+  pc.key_tile = key_tile;
+  pc.n_layers = n_layers;
+  pc.num_sms = num_sms;
+  pc.ctas_per_sm = ctas_per_sm;
+  pc.max_splits = max_splits;
+  Plan plan;
+  plan_units(segs, pc, &plan);
+  const int32_t n = (int32_t)plan.units.size();
+  if (units_out) {
+    for (int i = 0; i < n && i < cap_units; ++i) {
+      const WorkUnit& u = plan.units[i];
+      int32_t* o = units_out + 8 * i;
+      o[0] = u.seg; o[1] = u.kv_head; o[2] = u.q_tok0; o[3] = u.q_ntok;
+      o[4] = u.tile_lo; o[5] = u.tile_hi; o[6] = u.group; o[7] = u.split;
+    }
+  }
+  return n;
+}
+
+}  // extern "C"

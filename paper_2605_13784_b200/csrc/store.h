@@ -1,0 +1,105 @@
+// store.h — the store and session objects behind the opaque ssa_store_t.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "ssa.h"
+#include "ssa_internal.h"
+
+namespace ssa {
+
+void set_error(const char* fmt, ...);
+
+struct Session {
+  bool live = false;
+  int64_t n_prefix = 0;   // Region 0 length
+  int64_t n_tokens = 0;   // retained tokens (R0 + R1)
+  uint64_t version = 0;   // data version t
+  std::vector<int32_t> pages;   // host page table: slot / P -> page id
+  int32_t* d_pages = nullptr;   // device mirror
+  int64_t d_cap = 0;
+  int64_t d_valid = 0;
+  // open append (per-layer ticket or per-layer batch)
+  bool ticket_open = false;
+  bool batch_ticket = false;
+  int32_t ticket_id = 0;
+  int32_t ticket_n_new = 0;
+  int64_t ticket_pages = 0;
+  std::vector<uint8_t> ticket_done;
+};
+
+struct IoBuf {
+  const void* user = nullptr;  // caller pointer
+  size_t bytes = 0;
+  void* dev = nullptr;         // device pointer the kernels use
+  void* host = nullptr;        // non-null when `user` is host memory
+  size_t stage_off = 0;
+  IoBuf() = default;
+  IoBuf(const void* u, size_t b) : user(u), bytes(b) {}
+};
+
+struct IoSet {
+  IoBuf q, k, v, o;
+};
+
+// tcgen05 path (kernels_tc.cu)
+int tc_key_tile();
+int tc_rows_tile();
+cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, cudaStream_t s);
+bool tc_supported_shape(int D, int G, bool bf16);
+
+}  // namespace ssa
+
+struct CommState;
+
+struct ssa_store {
+  ssa_store_config cfg{};
+  int elem = 2;
+  float scale = 1.f;
+  int num_sms = 148;
+  bool sm100 = false;
+  void* poolK = nullptr;
+  void* poolV = nullptr;
+  size_t pool_half_bytes = 0;
+  std::vector<ssa::Session> sessions;
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_pages;
+  bool failed = false;
+  std::string fail_msg;
+  ssa::UploadRing ring;
+  float* part_o = nullptr;
+  size_t part_o_cap = 0;
+  float* part_lse = nullptr;
+  size_t part_lse_cap = 0;
+  void* stage = nullptr;
+  size_t stage_cap = 0;
+  int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0;
+  ssa_stats stats{};
+  int32_t ticket_seq = 0;
+  int64_t last_plan_units = 0, last_plan_groups = 0;
+  bool last_used_tc = false;
+  CommState* comm = nullptr;
+
+  ~ssa_store();
+  ssa_status cuda_fail(cudaError_t e, const char* what, int line);
+  int64_t pad_prefix(int64_t n_prefix) const;
+  int64_t slot_of(const ssa::Session& s, int64_t t) const;
+  int64_t slots_for(const ssa::Session& s, int64_t n) const;
+  int64_t pages_for(const ssa::Session& s, int64_t n) const;
+  ssa::Session* get(ssa_session_t id);
+  ssa_status reserve(ssa::Session& s, int64_t n_total, std::vector<int32_t>* got);
+  void release(const std::vector<int32_t>& pages);
+  ssa_status push_pages(ssa::Session& s, const std::vector<int32_t>& pages, cudaStream_t st);
+  void fill_cached(const ssa::Session& s, ssa::SegDesc* sg) const;
+  ssa_status ensure_scratch(size_t part_o_floats, size_t part_lse_floats, cudaStream_t st);
+  ssa_status stage_inputs(ssa::IoSet* io, cudaStream_t st);
+  ssa_status unstage_output(ssa::IoSet* io, cudaStream_t st);
+  ssa_status run(std::vector<ssa::SegDesc>& segs, const ssa::IoSet& io, int64_t rows_per_layer, int32_t layer0,
+                 int32_t n_layers, int32_t in_layer_stride, bool compute_o, bool query_plane, cudaStream_t st);
+  bool tc_eligible(const std::vector<ssa::SegDesc>& segs) const;
+  void destroy_comm();
+};

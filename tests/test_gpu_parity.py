@@ -1,0 +1,365 @@
+"""GPU parity of the CUDA path against the fp64 oracle.
+
+Every test drives libssa through the C ABI (Python binding) and compares with
+the oracle on the same seeded inputs (streams.py): KV append and page indexing
+bit-exact; attention within the north-star tolerances (bf16 max-abs 2e-2 /
+mean-abs 2e-3; fp32 1e-5).  Negative controls (fault injection) must FAIL.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import streams
+from helpers import TOL, errors, f64, from_dev, gen_qkv, to_dev, within
+
+pytestmark = pytest.mark.gpu
+
+
+def _ssa():
+    import paper_2605_13784_b200 as ssa
+    return ssa
+
+
+def _rows_ref(ref, sid, layer, Q, K, V, tokens=None, heads=None):
+    """Oracle rows of a new segment against the session's current cache (one layer)."""
+    s = ref.sessions[sid]
+    return oracle.segment_rows(s.k[layer][:s.n_tokens], s.v[layer][:s.n_tokens], Q, K, V, ref.hkv, ref.scale,
+                               tokens, heads)[0]
+
+
+# --------------------------------------------------------------------------- config 1 (toy fp32)
+@pytest.mark.parametrize("page_size", [16, 64])
+def test_config1_toy_fp32(cuda, page_size):
+    """BJ.configs[0]: 1 layer, 4 heads d=64 fp32; S=128, 8 appends of 64, |q|=16 query after each."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d = 1, 4, 4, 64
+    spec = streams.StreamSpec("peaked", seed=1)
+    st = ssa.Store(L, hq, hkv, d, page_size=page_size, num_pages=64, dtype="fp32")
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=page_size, num_pages=64, dtype="fp32")
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 128, "fp32")
+    O = torch.empty(Q.shape, dtype=torch.float32, device=cuda)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    rsid, Oref = ref.session_create(128, Q, K, V)
+    worst = errors(from_dev(O), Oref)
+    tok = 128
+    for i in range(8):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, tok, 64, "fp32")
+        O = torch.empty(Q.shape, dtype=torch.float32, device=cuda)
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        Oref, _ = ref.session_append(rsid, Q, K, V)
+        worst = max(worst, errors(from_dev(O), Oref))
+        tok += 64
+        Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1 + i, 0, 16, "fp32")
+        Oq = torch.empty(Qq.shape, dtype=torch.float32, device=cuda)
+        st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+        worst = max(worst, errors(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq)))
+        assert st.page_table(sid) == ref.page_table(rsid)
+    assert worst[0] <= TOL["fp32"][0], worst
+    assert st.digest(sid) == ref.digest(rsid)
+    assert st.info(sid) == ref.info(rsid)
+
+
+def test_ragged_appends_r0_padding_fp32(cuda):
+    """Odd sizes: R0 of 100 tokens padded to a page boundary (hole masked), partial pages."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 4, 2, 32, 16
+    spec = streams.StreamSpec("market", seed=7, iid_prefix=100)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=128, dtype="fp32")
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=128, dtype="fp32")
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 100, "fp32")
+    O = torch.empty(Q.shape, device=cuda)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    rsid, Oref = ref.session_create(100, Q, K, V)
+    worst = errors(from_dev(O), Oref)
+    tok = 100
+    for m in (37, 91, 1, 5, 64, 129):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, tok, m, "fp32")
+        O = torch.empty(Q.shape, device=cuda)
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        Oref, _ = ref.session_append(rsid, Q, K, V)
+        worst = max(worst, errors(from_dev(O), Oref))
+        tok += m
+        assert st.page_table(sid) == ref.page_table(rsid)
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 3, "fp32")
+    Oq = torch.empty(Qq.shape, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    worst = max(worst, errors(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq)))
+    assert worst[0] <= TOL["fp32"][0], worst
+    for l in range(L):
+        Kb, Vb = st.read_kv(sid, l, 0, tok)
+        assert np.array_equal(Kb, ref.sessions[rsid].k[l]) and np.array_equal(Vb, ref.sessions[rsid].v[l])
+    assert st.digest(sid) == ref.digest(rsid)
+
+
+# --------------------------------------------------------------------------- Llama-shaped bf16
+LL = dict(L=2, hq=32, hkv=8, d=128, P=64)
+
+
+def _llama_session(cuda, spec, n0=512, appends=(256, 256), num_pages=256, backend=0):
+    import torch
+    ssa = _ssa()
+    st = ssa.Store(LL["L"], LL["hq"], LL["hkv"], LL["d"], page_size=LL["P"], num_pages=num_pages, dtype="bf16")
+    if backend:
+        st.set_option(ssa.OPT_ATTN_BACKEND, backend)
+    ref = oracle.OracleStore(LL["L"], LL["hq"], LL["hkv"], LL["d"], page_size=LL["P"], num_pages=num_pages)
+    Q, K, V = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 0, 0, n0)
+    sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    rsid, _ = ref.session_create(n0, Q, K, V, compute=False)
+    tok = n0
+    outs = []
+    for m in appends:
+        Q, K, V = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 0, tok, m)
+        O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+        Ref_rows = [_rows_ref(ref, rsid, l, Q[l], K[l], V[l], heads=[0, 9, 31]) for l in range(LL["L"])]
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        ref.session_append(rsid, Q, K, V, compute=False)
+        outs.append((from_dev(O)[:, :, [0, 9, 31]], np.stack(Ref_rows)))
+        tok += m
+    return st, ref, sid, rsid, tok, outs
+
+
+@pytest.mark.parametrize("stream_name", ["peaked", "market", "flat"])
+@pytest.mark.parametrize("backend", [0, 1])
+def test_llama_append_and_query_bf16(cuda, stream_name, backend):
+    import torch
+    spec = streams.StreamSpec(stream_name, seed=2)
+    st, ref, sid, rsid, tok, outs = _llama_session(cuda, spec, backend=backend)
+    for got, want in outs:
+        ok, e = within(got, want, "bf16")
+        assert ok, ("append", e)
+    Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, ("query", e)
+    assert st.page_table(sid) == ref.page_table(rsid)
+    assert st.digest(sid) == ref.digest(rsid)
+
+
+@pytest.mark.parametrize("nq", [1, 4, 32, 33, 100])
+def test_query_lengths_bf16(cuda, nq):
+    """|q| = 1 (SIMT decode path) .. 100 (several q tiles, ragged tail)."""
+    import torch
+    spec = streams.StreamSpec("peaked", seed=3)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=700, appends=(300,))
+    Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, nq)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, e
+
+
+def test_needle_probes_at_boundaries(cuda):
+    """Needles at slot 0, P-1, P, split boundaries and n-1 must be retrieved (O = v_j)."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 1, 32, 8, 128, 64
+    n = 2048
+    for pos in (0, 63, 64, 127, 128, 1000, n - 1):
+        spec = streams.StreamSpec("needle", seed=4, needles=(pos,))
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+        ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+        sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+        rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+        Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 32)
+        Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+        want = ref.session_query(rsid, Qq, Kq, Vq)
+        ok, e = within(from_dev(Oq), want, "bf16")
+        assert ok, (pos, e)
+        # the oracle itself returns v_needle (weight ~1): the probe is live
+        vn = f64(V[0, pos])
+        assert np.abs(want[0] - np.repeat(vn, hq // hkv, axis=0)[None]).max() < 1e-6
+        st.close()
+
+
+@pytest.mark.parametrize("fault", [1, 2])
+def test_negative_controls_fail(cuda, fault):
+    """A kernel that drops the last key tile / misses its own key must fail the tolerance."""
+    import torch
+    ssa = _ssa()
+    spec = streams.StreamSpec("peaked", seed=5)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=512, appends=(128,))
+    st.set_option(ssa.OPT_FAULT_INJECT, fault)
+    Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert not ok, ("negative control passed", fault, e)
+
+
+# --------------------------------------------------------------------------- flash queries / batch
+def test_flash_query_batch(cuda):
+    import torch
+    spec = streams.StreamSpec("market", seed=6)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=640, appends=(256,))
+    dg = st.digest(sid)
+    lens = [32, 7, 32, 19, 1, 32, 50]
+    qs = [gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], streams.FLASH_DOMAIN + i, 0, m)
+          for i, m in enumerate(lens)]
+    for layer in (0, 1):
+        Q = np.concatenate([q[0][layer:layer + 1] for q in qs], axis=1)
+        K = np.concatenate([q[1][layer:layer + 1] for q in qs], axis=1)
+        V = np.concatenate([q[2][layer:layer + 1] for q in qs], axis=1)
+        O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+        st.flash_query_batch(sid, lens, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O, layer=layer)
+        want = ref.flash_query_batch(rsid, [(q[0][layer], q[1][layer], q[2][layer]) for q in qs], layer)
+        ok, e = within(from_dev(O)[0], np.concatenate(want), "bf16")
+        assert ok, e
+    assert st.digest(sid) == dg     # state neutrality
+
+
+def test_batch_run_snapshot(cuda):
+    """One launch: appends + queries of several sessions + stateless prompts (R-7)."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    spec = streams.StreamSpec("market", seed=8)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=512)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=512)
+    sids = []
+    for s, n in enumerate([300, 1024, 777]):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n, session=s)
+        sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+        rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+        assert sid == rsid
+        sids.append((sid, n))
+    # items: append s0, query s0 (same batch -> sees old state), query s1, append s2, stateless
+    plan = [("append", 0, 64), ("query", 0, 32), ("query", 1, 32), ("append", 2, 100), ("stateless", -1, 200)]
+    Qs, Ks, Vs, items, ref_items, row = [], [], [], [], [], 0
+    for i, (kind, s, m) in enumerate(plan):
+        if kind == "append":
+            Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, sids[s][1], m, session=s)
+        else:
+            Q, K, V = gen_qkv(spec, L, hq, hkv, d, 50 + i, 0, m, session=max(s, 0))
+        Qs.append(Q); Ks.append(K); Vs.append(V)
+        items.append(({"append": ssa.WORK_APPEND, "query": ssa.WORK_QUERY, "stateless": ssa.WORK_STATELESS}[kind],
+                      s, m, row))
+        ref_items.append(dict(kind=kind, session=s, Q=Q, K=K, V=V))
+        row += m
+    Q, K, V = (np.concatenate(x, axis=1) for x in (Qs, Ks, Vs))
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    st.batch_run(items, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    want = np.concatenate(ref.batch_run(ref_items), axis=1)
+    ok, e = within(from_dev(O), want, "bf16")
+    assert ok, e
+    for sid, _ in sids:
+        assert st.info(sid) == ref.info(sid)
+        assert st.page_table(sid) == ref.page_table(sid)
+        assert st.digest(sid) == ref.digest(sid)
+
+
+def test_per_layer_append_equals_all_layer(cuda):
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 3, 8, 2, 128, 64
+    spec = streams.StreamSpec("peaked", seed=9)
+    a = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+    b = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 200)
+    sa = a.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    sb = b.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 200, 90)
+    Oa = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    a.session_append(sa, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), Oa)
+    t = b.append_begin(sb, 90)
+    Ob = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    for l in range(L):
+        b.append_layer(sb, t, l, to_dev(Q[l:l + 1], cuda), to_dev(K[l:l + 1], cuda), to_dev(V[l:l + 1], cuda), Ob[l:l + 1])
+    with pytest.raises(ssa.SsaError):
+        b.append_layer(sb, t, 0, to_dev(Q[:1], cuda), to_dev(K[:1], cuda), to_dev(V[:1], cuda), Ob[:1])
+    b.append_commit(sb, t)
+    assert torch.equal(Oa.view(torch.int16), Ob.view(torch.int16))
+    assert a.digest(sa) == b.digest(sb) and a.info(sa) == b.info(sb)
+
+
+# --------------------------------------------------------------------------- store contract
+def test_host_pointers_equal_device_pointers(cuda):
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 8, 2, 128, 64
+    spec = streams.StreamSpec("peaked", seed=10)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 300)
+    a = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+    b = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+    Od = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    sa = a.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), Od)
+    Oh = np.zeros(Q.shape, dtype=np.uint16)
+    sb = b.session_create(Q, K, V, Oh)        # pageable host numpy buffers
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(Od), Oh)
+    Qp = torch.from_numpy(Q.view(np.int16)).pin_memory()
+    Op = torch.zeros(Q.shape, dtype=torch.int16).pin_memory()
+    Q2, K2, V2 = gen_qkv(spec, L, hq, hkv, d, 1, 0, 32)
+    O2d = torch.empty(Q2.shape, dtype=torch.bfloat16, device=cuda)
+    a.session_query(sa, to_dev(Q2, cuda), to_dev(K2, cuda), to_dev(V2, cuda), O2d)
+    O2h = torch.zeros(Q2.shape, dtype=torch.int16).pin_memory()
+    b.session_query(sb, torch.from_numpy(Q2.view(np.int16)).pin_memory(), torch.from_numpy(K2.view(np.int16)).pin_memory(),
+                    torch.from_numpy(V2.view(np.int16)).pin_memory(), O2h)
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(O2d), O2h.numpy().view(np.uint16))
+    assert b.stats()["h2d_bytes"] > 0
+    del Qp, Op
+
+
+def test_errors_leave_no_state_change(cuda):
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 1, 4, 4, 64, 16
+    spec = streams.StreamSpec("flat", seed=11)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=6, max_sessions=2, dtype="fp32")
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 64, "fp32")
+    sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    before = (st.info(sid), st.page_table(sid), st.occupancy(), st.digest(sid))
+    Q2, K2, V2 = gen_qkv(spec, L, hq, hkv, d, 0, 64, 40, "fp32")
+    with pytest.raises(ssa.SsaError) as e:
+        st.session_append(sid, None, to_dev(K2, cuda), to_dev(V2, cuda))
+    assert e.value.name == "SSA_ERR_POOL_EXHAUSTED"
+    with pytest.raises(ssa.SsaError) as e:
+        st.session_append(77, None, to_dev(K2, cuda), to_dev(V2, cuda))
+    assert e.value.name == "SSA_ERR_UNKNOWN_SESSION"
+    with pytest.raises(ssa.SsaError) as e:
+        st.session_query(sid, to_dev(Q2, cuda), to_dev(K2, cuda), to_dev(V2, cuda), None)
+    assert e.value.name == "SSA_ERR_INVALID_ARG"
+    assert (st.info(sid), st.page_table(sid), st.occupancy(), st.digest(sid)) == before
+    s2 = st.session_create(None, to_dev(K[:, :16], cuda), to_dev(V[:, :16], cuda))
+    with pytest.raises(ssa.SsaError) as e:
+        st.session_create(None, to_dev(K[:, :16], cuda), to_dev(V[:, :16], cuda))
+    assert e.value.name in ("SSA_ERR_SESSION_LIMIT", "SSA_ERR_POOL_EXHAUSTED")
+    st.session_destroy(s2)
+
+
+def test_query_cost_invariance(cuda):
+    """Rows computed per query = |q| * Hq * L at every context size."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    spec = streams.StreamSpec("market", seed=12)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=512)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 512)
+    sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    tok = 512
+    Qq, Kq, Vq = (to_dev(x, cuda) for x in gen_qkv(spec, L, hq, hkv, d, 1, 0, 30))
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    for step in range(5):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, tok, 1000)
+        st.load_kv(sid, to_dev(K, cuda), to_dev(V, cuda))
+        tok += 1000
+        d0 = st.info(sid)
+        st.stats(reset=True)
+        st.session_query(sid, Qq, Kq, Vq, Oq)
+        s = st.stats()
+        assert s["query_rows"] == 30 * hq * L and s["tokens_appended"] == 0 and s["pages_reserved"] == 0
+        assert st.info(sid) == d0
+
+
+def test_streams_torch_matches_numpy_on_gpu(cuda):
+    import torch
+    for name in streams.STREAMS:
+        spec = streams.StreamSpec(name, seed=13, needles=(3, 70))
+        a = streams.gen_tensor_np(spec, 2, 0, 1, streams.TENSOR_K, 50, 40, 8, 128, hkv=8)
+        b = streams.gen_tensor_torch(spec, 2, 0, 1, streams.TENSOR_K, 50, 40, 8, 128, hkv=8, device=cuda)
+        assert np.array_equal(a, from_dev(b))
