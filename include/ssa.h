@@ -267,9 +267,21 @@ typedef enum {
     SSA_OPT_MAX_SPLITS = 2,     /* cap on split-KV factor (0 = auto) */
     SSA_OPT_FAULT_INJECT = 3,   /* negative controls: 0 none, 1 drop last key tile,
                                    2 causal off-by-one (row t misses its own key) */
-    SSA_OPT_TC_Q_TILES = 4      /* tcgen05 Q tiles per CTA (1 or 2; 0 = auto) */
+    SSA_OPT_TC_Q_TILES = 4,     /* tcgen05 Q tiles per CTA (1 or 2; 0 = auto) */
+    SSA_OPT_TIMING = 5          /* 1: record CUDA events around every kernel launch
+                                   (on the call's stream) for ssa_store_timing */
 } ssa_option;
 ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
+
+/* Kernel timing recorded while SSA_OPT_TIMING is on, per kernel class
+ * (SSA_TIMING_KINDS entries): [0] data-plane attention (create/append/batch),
+ * [1] query-plane attention (query/flash/sharded), [2] data-plane split-KV
+ * combine, [3] query-plane combine, [4] KV append scatter.
+ * ms[i] = summed device time of launches of class i, count[i] = launches.
+ * Synchronizes the recorded events; reset != 0 clears the record. */
+#define SSA_TIMING_KINDS 5
+ssa_status ssa_store_timing(ssa_store_t store, double ms[SSA_TIMING_KINDS],
+                            int64_t count[SSA_TIMING_KINDS], int32_t reset);
 
 /* ----------------------------------------------------------------------------
  * Multi-GPU split-KV for one long session (R-12)

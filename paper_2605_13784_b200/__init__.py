@@ -15,13 +15,15 @@ import ctypes
 import os
 
 __all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", "WORK_STATELESS",
-           "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "debug_plan"]
+           "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING",
+           "debug_plan", "TIMING_KINDS"]
+TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libssa.so")
 
 WORK_APPEND, WORK_QUERY, WORK_STATELESS = 0, 1, 2
-OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES = 1, 2, 3, 4
+OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES, OPT_TIMING = 1, 2, 3, 4, 5
 BF16, FP32 = 0, 1
 
 _STATUS = {0: "SSA_OK", -1: "SSA_ERR_INVALID_ARG", -2: "SSA_ERR_UNKNOWN_SESSION", -3: "SSA_ERR_POOL_EXHAUSTED",
@@ -88,6 +90,7 @@ def _load():
         "ssa_session_digest": (i32, [vp, i32, P(u64)]),
         "ssa_store_stats": (i32, [vp, P(Stats), i32]),
         "ssa_store_set_option": (i32, [vp, i32, i64]),
+        "ssa_store_timing": (i32, [vp, P(ctypes.c_double), P(i64), i32]),
         "ssa_comm_unique_id": (i32, [P(ctypes.c_uint8)]),
         "ssa_comm_init": (i32, [vp, i32, i32, P(ctypes.c_uint8)]),
         "ssa_sharded_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
@@ -283,6 +286,13 @@ class Store:
 
     def set_option(self, option, value):
         _check(lib.ssa_store_set_option(self._h, option, value), "store_set_option")
+
+    def timing(self, reset=False):
+        """{kind: (ms_total, launches)} recorded under OPT_TIMING (syncs)."""
+        ms = (ctypes.c_double * len(TIMING_KINDS))()
+        n = (ctypes.c_int64 * len(TIMING_KINDS))()
+        _check(lib.ssa_store_timing(self._h, ms, n, int(reset)), "store_timing")
+        return {k: (ms[i], n[i]) for i, k in enumerate(TIMING_KINDS)}
 
     # -- multi-GPU split-KV ---------------------------------------------------
     @staticmethod

@@ -125,6 +125,36 @@ ssa_status ssa_store::cuda_fail(cudaError_t e, const char* what, int line) {
 
 static int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+cudaEvent_t ssa_store::tick(cudaStream_t st) {
+  if (!opt_timing) return nullptr;
+  cudaEvent_t e = nullptr;
+  if (!spare_events.empty()) {
+    e = spare_events.back();
+    spare_events.pop_back();
+  } else if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaEventRecord(e, st);
+  return e;
+}
+
+ssa_status ssa_store::drain_timing() {
+  for (auto& t : timed) {
+    if (t.a && t.b) {
+      SSA_CUDA(this, cudaEventSynchronize(t.b));
+      float ms = 0.f;
+      SSA_CUDA(this, cudaEventElapsedTime(&ms, t.a, t.b));
+      timing_ms[t.kind] += ms;
+      timing_n[t.kind] += 1;
+    }
+    if (t.a) spare_events.push_back(t.a);
+    if (t.b) spare_events.push_back(t.b);
+  }
+  timed.clear();
+  return SSA_OK;
+}
+
 int64_t ssa_store::pad_prefix(int64_t n_prefix) const { return ceil_div64(n_prefix, cfg.page_size) * cfg.page_size; }
 
 // Slot of token t of a session (reading R-9: R0 padded to a page boundary).
@@ -350,7 +380,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     sp.tok_prefix = d_pre;
     sp.n_segs = (int32_t)app_segs.size();
     sp.total_tokens = prefix.back();
+    cudaEvent_t t0 = tick(st);
     SSA_CUDA(this, launch_scatter(sp, n_layers, st));
+    if (t0) timed_push(4, t0, tick(st));
     stats.kernel_launches++;
   }
   // ---- attention (+ combine)
@@ -389,11 +421,13 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.rows_tile = rows_tile;
     ap.key_tile = pc.key_tile;
     ap.fault = (int32_t)opt_fault;
+    cudaEvent_t t0 = tick(st);
     if (use_tc) {
       SSA_CUDA(this, launch_attn_tc(ap, n_layers, (int)opt_tc_qtiles, st));
     } else {
       SSA_CUDA(this, launch_attn_simt(ap, n_layers, cfg.dtype == SSA_BF16, st));
     }
+    if (t0) timed_push(query_plane ? 1 : 0, t0, tick(st));
     stats.kernel_launches++;
     if (!plan.groups.empty()) {
       CombineParams cp{};
@@ -412,7 +446,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       cp.G = G;
       cp.D = D;
       cp.write_o = 1;
+      cudaEvent_t t1 = tick(st);
       SSA_CUDA(this, launch_combine(cp, n_layers, cfg.dtype == SSA_BF16, st));
+      if (t1) timed_push(query_plane ? 3 : 2, t1, tick(st));
       stats.kernel_launches++;
     }
     int64_t rows = 0;
@@ -522,6 +558,8 @@ ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
 
 ssa_store::~ssa_store() {
   cudaDeviceSynchronize();
+  for (auto& t : timed) { if (t.a) cudaEventDestroy(t.a); if (t.b) cudaEventDestroy(t.b); }
+  for (auto e : spare_events) cudaEventDestroy(e);
   for (auto& s : sessions)
     if (s.d_pages) cudaFree(s.d_pages);
   if (poolK) cudaFree(poolK);
@@ -560,7 +598,21 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
     case SSA_OPT_MAX_SPLITS: if (value < 0) return SSA_ERR_INVALID_ARG; st->opt_max_splits = value; break;
     case SSA_OPT_FAULT_INJECT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_fault = value; break;
     case SSA_OPT_TC_Q_TILES: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_tc_qtiles = value; break;
+    case SSA_OPT_TIMING: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_timing = value; break;
     default: return SSA_ERR_INVALID_ARG;
+  }
+  return SSA_OK;
+}
+
+ssa_status ssa_store_timing(ssa_store_t st, double ms[SSA_TIMING_KINDS], int64_t count[SSA_TIMING_KINDS], int32_t reset) {
+  if (!st) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  ssa_status rc = st->drain_timing();
+  if (rc != SSA_OK) return rc;
+  for (int i = 0; i < SSA_TIMING_KINDS; ++i) {
+    if (ms) ms[i] = st->timing_ms[i];
+    if (count) count[i] = st->timing_n[i];
+    if (reset) { st->timing_ms[i] = 0; st->timing_n[i] = 0; }
   }
   return SSA_OK;
 }

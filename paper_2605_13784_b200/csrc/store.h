@@ -83,6 +83,16 @@ struct ssa_store {
   int64_t last_plan_units = 0, last_plan_groups = 0;
   bool last_used_tc = false;
   CommState* comm = nullptr;
+  // SSA_OPT_TIMING
+  int64_t opt_timing = 0;
+  struct TimedLaunch { int kind; cudaEvent_t a, b; };
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> spare_events;
+  double timing_ms[SSA_TIMING_KINDS] = {};
+  int64_t timing_n[SSA_TIMING_KINDS] = {};
+  cudaEvent_t tick(cudaStream_t st);
+  void timed_push(int kind, cudaEvent_t a, cudaEvent_t b) { timed.push_back({kind, a, b}); }
+  ssa_status drain_timing();
 
   ~ssa_store();
   ssa_status cuda_fail(cudaError_t e, const char* what, int line);
