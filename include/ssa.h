@@ -257,6 +257,7 @@ typedef struct {
     int64_t pages_reserved;
     int64_t h2d_bytes;           /* host staging copies */
     int64_t d2h_bytes;
+    int64_t tc_launches;         /* attention launches on the tcgen05 kernel */
 } ssa_stats;
 
 ssa_status ssa_store_stats(ssa_store_t store, ssa_stats *out, int32_t reset);

@@ -58,7 +58,8 @@ class WorkItem(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("kernel_launches", "rows_computed", "query_rows",
-                                              "tokens_appended", "pages_reserved", "h2d_bytes", "d2h_bytes")]
+                                              "tokens_appended", "pages_reserved", "h2d_bytes", "d2h_bytes",
+                                              "tc_launches")]
 
 
 def _load():

@@ -429,6 +429,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     }
     if (t0) timed_push(query_plane ? 1 : 0, t0, tick(st));
     stats.kernel_launches++;
+    if (use_tc) stats.tc_launches++;
     if (!plan.groups.empty()) {
       CombineParams cp{};
       cp.part_o = part_o;

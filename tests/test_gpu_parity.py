@@ -121,11 +121,13 @@ def _llama_session(cuda, spec, n0=512, appends=(256, 256), num_pages=256, backen
 
 
 @pytest.mark.parametrize("stream_name", ["peaked", "market", "flat"])
-@pytest.mark.parametrize("backend", [0, 1])
+@pytest.mark.parametrize("backend", [2, 1])
 def test_llama_append_and_query_bf16(cuda, stream_name, backend):
+    """backend 2 = tcgen05 kernel, 1 = SIMT kernel; both against the oracle."""
     import torch
     spec = streams.StreamSpec(stream_name, seed=2)
     st, ref, sid, rsid, tok, outs = _llama_session(cuda, spec, backend=backend)
+    assert (st.stats()["tc_launches"] > 0) == (backend == 2)
     for got, want in outs:
         ok, e = within(got, want, "bf16")
         assert ok, ("append", e)
@@ -138,12 +140,13 @@ def test_llama_append_and_query_bf16(cuda, stream_name, backend):
     assert st.digest(sid) == ref.digest(rsid)
 
 
+@pytest.mark.parametrize("backend", [0, 2])
 @pytest.mark.parametrize("nq", [1, 4, 32, 33, 100])
-def test_query_lengths_bf16(cuda, nq):
-    """|q| = 1 (SIMT decode path) .. 100 (several q tiles, ragged tail)."""
+def test_query_lengths_bf16(cuda, nq, backend):
+    """|q| = 1 (SIMT decode path under auto) .. 100 (several q tiles, ragged tail)."""
     import torch
     spec = streams.StreamSpec("peaked", seed=3)
-    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=700, appends=(300,))
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=700, appends=(300,), backend=backend)
     Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, nq)
     Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
     st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
@@ -176,13 +179,14 @@ def test_needle_probes_at_boundaries(cuda):
         st.close()
 
 
+@pytest.mark.parametrize("backend", [1, 2])
 @pytest.mark.parametrize("fault", [1, 2])
-def test_negative_controls_fail(cuda, fault):
+def test_negative_controls_fail(cuda, fault, backend):
     """A kernel that drops the last key tile / misses its own key must fail the tolerance."""
     import torch
     ssa = _ssa()
     spec = streams.StreamSpec("peaked", seed=5)
-    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=512, appends=(128,))
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=512, appends=(128,), backend=backend)
     st.set_option(ssa.OPT_FAULT_INJECT, fault)
     Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
     Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
