@@ -180,43 +180,56 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
   }
 }
 
-// One warp per output row of a group; lanes stride over d.  Partials carry
-// (o_s normalized, lse_s in log2 units); o = sum_s 2^(lse_s - L) o_s / sum_s 2^(lse_s - L).
+// Split-KV merge (KC).  One CTA per (group, layer): per-row weights
+// w_s = 2^(lse_s - L) / sum_s 2^(lse_s - L) are computed once into smem, then
+// the 128-bit-vectorized weighted sum runs over all (row, 4-column) pairs.
+// Partials carry normalized o_s and lse_s in log2 units (reading R-11).
 template <typename T>
-__global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
+__global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
+  extern __shared__ float wsm[];                       // [n_splits][rows_tile]
   const int g = blockIdx.x, ly = blockIdx.y;
   const Group gr = p.groups[g];
   const SegDesc sg = p.segs[gr.seg];
   const int rows = gr.q_ntok * p.G;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t in_row0 = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0;
-  for (int r = warp; r < rows; r += blockDim.x / 32) {
+  const int RT = p.rows_tile;
+  const int64_t slot0 = (int64_t)ly * p.n_units + gr.unit0;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
     float L = -CUDART_INF_F;
-    for (int s = lane; s < gr.n_splits; s += 32) {
-      const int64_t slot = (int64_t)ly * p.n_units + gr.unit0 + s;
-      L = fmaxf(L, p.part_lse[slot * p.rows_tile + r]);
-    }
-    L = warp_max(L);
+    for (int s = 0; s < gr.n_splits; ++s) L = fmaxf(L, p.part_lse[(slot0 + s) * RT + r]);
     float wsum = 0.f;
-    for (int s = lane; s < gr.n_splits; s += 32) {
-      const int64_t slot = (int64_t)ly * p.n_units + gr.unit0 + s;
-      const float ls = p.part_lse[slot * p.rows_tile + r];
-      if (ls != -CUDART_INF_F) wsum += exp2f(ls - L);
+    for (int s = 0; s < gr.n_splits; ++s) {
+      const float ls = p.part_lse[(slot0 + s) * RT + r];
+      const float w = ls == -CUDART_INF_F ? 0.f : exp2f(ls - L);
+      wsm[s * RT + r] = w;
+      wsum += w;
     }
-    wsum = warp_sum(wsum);
+    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    for (int s = 0; s < gr.n_splits; ++s) wsm[s * RT + r] *= inv;
+    if (p.lse_out)
+      p.lse_out[((int64_t)ly * p.n_groups + g) * RT + r] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+  }
+  __syncthreads();
+  if (!p.write_o) return;
+  const int64_t in_row0 = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0;
+  const int d4 = p.D / 4;
+  for (int idx = threadIdx.x; idx < rows * d4; idx += blockDim.x) {
+    const int r = idx / d4, e = (idx % d4) * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < gr.n_splits; ++s) {
+      const float w = wsm[s * RT + r];
+      const float4 v = *reinterpret_cast<const float4*>(p.part_o + ((slot0 + s) * RT + r) * p.D + e);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+      acc.z = fmaf(w, v.z, acc.z);
+      acc.w = fmaf(w, v.w, acc.w);
+    }
     const int64_t row = in_row0 + gr.q_tok0 + r / p.G;
     const int h = gr.kv_head * p.G + r % p.G;
-    for (int e = lane; e < p.D; e += 32) {
-      float acc = 0.f;
-      for (int s = 0; s < gr.n_splits; ++s) {
-        const int64_t slot = (int64_t)ly * p.n_units + gr.unit0 + s;
-        const float ls = p.part_lse[slot * p.rows_tile + r];
-        if (ls != -CUDART_INF_F) acc = fmaf(exp2f(ls - L), p.part_o[(slot * p.rows_tile + r) * p.D + e], acc);
-      }
-      if (p.write_o) st_f(static_cast<T*>(p.O), (row * p.Hq + h) * p.D + e, wsum > 0.f ? acc / wsum : 0.f);
-    }
-    if (p.lse_out && lane == 0)
-      p.lse_out[((int64_t)ly * p.n_groups + g) * p.rows_tile + r] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+    T* out = static_cast<T*>(p.O) + (row * p.Hq + h) * p.D + e;
+    st_f(out, 0, acc.x);
+    st_f(out, 1, acc.y);
+    st_f(out, 2, acc.z);
+    st_f(out, 3, acc.w);
   }
 }
 
@@ -303,11 +316,17 @@ cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaS
   }
 }
 
-cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s) {
+cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits) {
   if (p.n_groups == 0 || n_layers == 0) return cudaSuccess;
   dim3 grid(p.n_groups, n_layers);
-  if (bf16) combine_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(p);
-  else combine_kernel<float><<<grid, 128, 0, s>>>(p);
+  const size_t smem = sizeof(float) * (size_t)max_splits * p.rows_tile;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(bf16 ? (const void*)combine_kernel<__nv_bfloat16> : (const void*)combine_kernel<float>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if (bf16) combine_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(p);
+  else combine_kernel<float><<<grid, 256, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -1,22 +1,22 @@
 // kernels_tc.cu — tensor-core (tcgen05 / TMEM / TMA) attention for sm_100a.
 //
-// One CTA computes one work unit (plan.cpp): a q tile of 128 rows — 128/G tokens
-// x the G query heads sharing one KV head (GQA packing, reading R-5) — against
-// key tiles [tile_lo, tile_hi) of its segment: paged cached keys first (Eq.
-// query-attention), then the segment's own keys with the causal mask
-// (reading R-2).  Per key tile of 128 keys:
-//     S = Q K^T            tcgen05.mma  M=128 N=128 K=128, S in TMEM (fp32)
-//     P = exp2(S*c - m)    online softmax in registers, P -> smem (bf16)
-//     O += P V             tcgen05.mma  M=128 N=128 K=128, O in TMEM (fp32)
-// Warp roles (256 threads):
-//     warp 0      TMA producer: Q once, then K/V tiles (paged: one box per page
-//                 run; tail: dense input) into an NS-stage ring
-//     warp 1      MMA issuer (one elected lane)
-//     warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//     warps 4-7   softmax + epilogue, one thread per row (TMEM lane)
-// S is double-buffered in TMEM so QK^T of tile j+1 overlaps the softmax of tile
-// j.  The running max is updated lazily (only when it grows by > 8 in log2
-// units), so the O rescale (TMEM ld/st) is rare.
+// A CTA runs up to two work units ("slots", plan.cpp pair_units) with two
+// softmax warpgroups that ping-pong against one MMA issuer:
+//   SHARED  two q tiles over the same key tiles: each TMA-loaded K/V tile feeds
+//           256 query rows (halves L2->SM traffic for prefill / flash batches);
+//   SPLIT   one q tile over two key ranges (two split-KV partials; query plane);
+//   SINGLE  one slot.
+// Per slot and key tile of 128 keys (Eq. attention P:145 on the rows of Eq.
+// query-attention P:150-155; causal tail, reading R-2):
+//     S = Q K^T         tcgen05.mma M=128 N=128 K=128 -> TMEM (fp32)
+//     P = 2^(S*c - m)   softmax warpgroup, one thread per row (TMEM lane);
+//                       P (bf16) is written back into the S columns of TMEM
+//     O += P V          tcgen05.mma with A = P from TMEM, B = V from smem
+// TMEM (512 columns): slot k uses [256k, 256k+128) for S/P and
+// [256k+128, 256k+256) for O.  The running max is updated lazily (only when it
+// grows by more than 8 in log2 units), so O is rarely rescaled.
+// Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM
+// allocator, warps 4-7 softmax slot 0, warps 8-11 softmax slot 1.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -34,27 +34,24 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kM = 128;          // rows per q tile
+constexpr int kM = 128;          // rows per q tile (= TMEM lanes)
 constexpr int kBN = 128;         // keys per tile
-constexpr int kD = 128;          // head dim (two 64-column swizzle chunks)
-constexpr int kNS = 2;           // K/V pipeline stages
-constexpr int kThreads = 256;
-constexpr int kChunkBytes = kM * 128;                 // 128 rows x 128 B = 16 KB
-constexpr int kTileBytes = 2 * kChunkBytes;           // 128 x 128 bf16 = 32 KB
-constexpr float kRescaleThreshold = 8.0f;             // log2 units
+constexpr int kD = 128;          // head dim: two 64-column (128 B) swizzle chunks
+constexpr int kThreads = 384;
+constexpr int kChunkBytes = 128 * 128;          // 128 rows x 128 B
+constexpr int kSlotBytes = 2 * kChunkBytes;     // one 128 x 128 bf16 tile = 32 KB
+constexpr int kNumSlots = 7;                    // 224 KB of tiles
+constexpr int kMaxStages = 3;
+constexpr float kRescaleLog2 = 8.0f;
 
-struct TcSmem {
-  uint8_t q[kTileBytes];
-  uint8_t k[kNS][kTileBytes];
-  uint8_t v[kNS][kTileBytes];
-  uint8_t p[kTileBytes];
+struct Bars {
   uint64_t q_full;
-  uint64_t k_full[kNS];
-  uint64_t v_full[kNS];
-  uint64_t kv_empty[kNS];
+  uint64_t k_full[kMaxStages];
+  uint64_t v_full[kMaxStages];
+  uint64_t kv_empty[kMaxStages];
   uint64_t s_full[2];
-  uint64_t p_full;
-  uint64_t o_done;
+  uint64_t p_full[2];
+  uint64_t o_final[2];
   uint32_t tmem_base;
 };
 
@@ -70,22 +67,57 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem desc]  (A = P, K-major in TMEM).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+struct SlotInfo {
+  int tile_lo, nt;
+};
+
+// Load-event index of (slot k, tile j): SHARED loads tile j once for both slots;
+// SPLIT/SINGLE interleave the two slots' streams.
+__device__ __forceinline__ int event_of(int mode, int k, int j, int nt0, int nt1) {
+  if (mode == TC_SHARED) return j;
+  const int m = min(nt0, nt1);
+  return j < m ? 2 * j + k : 2 * m + (j - m);
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const int box_rows) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  TcSmem& sm = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars& bar = *reinterpret_cast<Bars*>(tiles + kNumSlots * kSlotBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x, ly = blockIdx.y;
-  const WorkUnit wu = p.units[u];
-  const SegDesc sg = p.segs[wu.seg];
-  const int G = p.G;
-  const int64_t layer = p.layer0 + ly;
-  const int64_t in_row0 = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0;
-  const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
-  const int nt = wu.tile_hi - wu.tile_lo;
+  const int ly = blockIdx.y;
+  const TcPair pr = p.pairs[blockIdx.x];
+  const int mode = pr.mode;
+  const WorkUnit w0 = p.units[pr.ua];
+  WorkUnit w1 = w0;
+  int nt1 = 0;
+  if (pr.ub >= 0) {
+    w1 = p.units[pr.ub];
+    nt1 = w1.tile_hi - w1.tile_lo;
+  }
+  const int nt0 = w0.tile_hi - w0.tile_lo;
+  const int NS = mode == TC_SHARED ? 2 : 3;
+  // smem tile slots
+  uint8_t* q_buf[2] = {tiles, mode == TC_SHARED ? tiles + kSlotBytes : tiles};
+  uint8_t* stage_base = tiles + (mode == TC_SHARED ? 2 : 1) * kSlotBytes;   // K(s) = base + 2s slots, V(s) = +1
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.q);
@@ -93,258 +125,296 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     tma_prefetch_desc(&maps.vt);
     tma_prefetch_desc(&maps.pk);
     tma_prefetch_desc(&maps.pv);
-    mbar_init(&sm.q_full, 1);
-    for (int s = 0; s < kNS; ++s) {
-      mbar_init(&sm.k_full[s], 1);
-      mbar_init(&sm.v_full[s], 1);
-      mbar_init(&sm.kv_empty[s], 1);
+    mbar_init(&bar.q_full, 1);
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&bar.k_full[s], 1);
+      mbar_init(&bar.v_full[s], 1);
+      mbar_init(&bar.kv_empty[s], 1);
     }
-    mbar_init(&sm.s_full[0], 1);
-    mbar_init(&sm.s_full[1], 1);
-    mbar_init(&sm.p_full, 4);
-    mbar_init(&sm.o_done, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&bar.s_full[k], 1);
+      mbar_init(&bar.p_full[k], 4);
+      mbar_init(&bar.o_final[k], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 2) tmem_alloc<512>(&bar.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
+  const uint32_t tmem = bar.tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------- TMA producer
-    if (elect_one()) {
-      const int T = kM / G;
-      mbar_arrive_expect_tx(&sm.q_full, kTileBytes);
-      const int32_t qrow = (int32_t)(in_row0 + wu.q_tok0);
-      for (int c = 0; c < 2; ++c)
-        tma_load_3d(sm.q + c * kChunkBytes, &maps.q, &sm.q_full, c * 64, wu.kv_head * G, qrow);
-      (void)T;
-      const int64_t head_base = layer * p.num_pages;  // page row base = ((head_base + page)*Hkv + h)*P
-      for (int j = 0; j < nt; ++j) {
-        const int s = j % kNS;
-        if (j >= kNS) mbar_wait(&sm.kv_empty[s], ((j / kNS) - 1) & 1);
-        const int tile = wu.tile_lo + j;
-        mbar_arrive_expect_tx(&sm.k_full[s], kTileBytes);
-        if (tile < n_pool_tiles) {
-          const int key0 = tile * kBN;
-          for (int b = 0; b < kBN / box_rows; ++b) {
-            const int slot = key0 + b * box_rows;
-            int32_t row;
-            if (slot < sg.n_slots) {
-              const int64_t page = __ldg(sg.pages + slot / p.P);
-              row = (int32_t)(((head_base + page) * p.Hkv + wu.kv_head) * p.P + (slot % p.P));
-            } else {
-              row = 0x7FFFFFF0;  // fully out of bounds -> TMA zero fill
-            }
-            for (int c = 0; c < 2; ++c)
-              tma_load_2d(sm.k[s] + c * kChunkBytes + b * box_rows * 128, &maps.pk, &sm.k_full[s], c * 64, row);
-          }
-          mbar_arrive_expect_tx(&sm.v_full[s], kTileBytes);
-          for (int b = 0; b < kBN / box_rows; ++b) {
-            const int slot = key0 + b * box_rows;
-            int32_t row;
-            if (slot < sg.n_slots) {
-              const int64_t page = __ldg(sg.pages + slot / p.P);
-              row = (int32_t)(((head_base + page) * p.Hkv + wu.kv_head) * p.P + (slot % p.P));
-            } else {
-              row = 0x7FFFFFF0;
-            }
-            for (int c = 0; c < 2; ++c)
-              tma_load_2d(sm.v[s] + c * kChunkBytes + b * box_rows * 128, &maps.pv, &sm.v_full[s], c * 64, row);
-          }
-        } else {
-          const int32_t krow = (int32_t)(in_row0 + (tile - n_pool_tiles) * kBN);
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == 0) {
+      // ----------------------------------------------------------- TMA producer
+      if (elect_one()) {
+        const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
+        const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+        const int nq = mode == TC_SHARED ? 2 : 1;
+        mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
+        for (int k = 0; k < nq; ++k) {
+          const WorkUnit& w = k ? w1 : w0;
+          const int32_t qrow = (int32_t)(in_l + p.segs[w.seg].row0 + w.q_tok0);
           for (int c = 0; c < 2; ++c)
-            tma_load_3d(sm.k[s] + c * kChunkBytes, &maps.kt, &sm.k_full[s], c * 64, wu.kv_head, krow);
-          mbar_arrive_expect_tx(&sm.v_full[s], kTileBytes);
-          for (int c = 0; c < 2; ++c)
-            tma_load_3d(sm.v[s] + c * kChunkBytes, &maps.vt, &sm.v_full[s], c * 64, wu.kv_head, krow);
+            tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
+        }
+        const int E = mode == TC_SHARED ? max(nt0, nt1) : nt0 + nt1;
+        const int m01 = min(nt0, nt1);
+        for (int e = 0; e < E; ++e) {
+          int k, j;
+          if (mode == TC_SHARED) { k = 0; j = e; }
+          else if (e < 2 * m01) { k = e & 1; j = e >> 1; }
+          else { k = nt0 > nt1 ? 0 : 1; j = m01 + (e - 2 * m01); }
+          const WorkUnit& w = k ? w1 : w0;
+          const SegDesc sg = p.segs[w.seg];
+          const int s = e % NS;
+          if (e >= NS) mbar_wait(&bar.kv_empty[s], ((e / NS) - 1) & 1);
+          uint8_t* kb = stage_base + (2 * s) * kSlotBytes;
+          uint8_t* vb = kb + kSlotBytes;
+          const int tile = w.tile_lo + j;
+          const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
+          mbar_arrive_expect_tx(&bar.k_full[s], kSlotBytes);
+          if (tile < n_pool_tiles) {
+            const int key0 = tile * kBN;
+            const int nb = kBN / box_rows;
+            auto row_of = [&](int b) -> int32_t {
+              const int slot = key0 + b * box_rows;
+              if (slot >= sg.n_slots) return 0x7FFFFFF0;   // past the tensor -> TMA zero fill
+              const int64_t page = __ldg(sg.pages + slot / p.P);
+              return (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
+            };
+            for (int b = 0; b < nb; ++b) {
+              const int32_t row = row_of(b);
+              for (int c = 0; c < 2; ++c)
+                tma_load_2d(kb + c * kChunkBytes + b * box_rows * 128, &maps.pk, &bar.k_full[s], c * 64, row);
+            }
+            mbar_arrive_expect_tx(&bar.v_full[s], kSlotBytes);
+            for (int b = 0; b < nb; ++b) {
+              const int32_t row = row_of(b);
+              for (int c = 0; c < 2; ++c)
+                tma_load_2d(vb + c * kChunkBytes + b * box_rows * 128, &maps.pv, &bar.v_full[s], c * 64, row);
+            }
+          } else {
+            const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
+            for (int c = 0; c < 2; ++c)
+              tma_load_3d(kb + c * kChunkBytes, &maps.kt, &bar.k_full[s], c * 64, w.kv_head, krow);
+            mbar_arrive_expect_tx(&bar.v_full[s], kSlotBytes);
+            for (int c = 0; c < 2; ++c)
+              tma_load_3d(vb + c * kChunkBytes, &maps.vt, &bar.v_full[s], c * 64, w.kv_head, krow);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ----------------------------------------------------------- MMA issuer
+      if (elect_one()) {
+        constexpr uint32_t idesc_s = idesc_bf16(kM, kBN, 0, 0);   // Q, K both K-major
+        constexpr uint32_t idesc_o = idesc_bf16(kM, kD, 0, 1);    // P K-major (TMEM), V MN-major
+        const int nt[2] = {nt0, nt1};
+        mbar_wait(&bar.q_full, 0);
+        tc_fence_after();
+        auto issue_s = [&](int k, int j) {
+          const int e = event_of(mode, k, j, nt0, nt1);
+          const int s = e % NS;
+          mbar_wait(&bar.k_full[s], (e / NS) & 1);
+          tc_fence_after();
+          const uint32_t q_addr = smem_u32(q_buf[k]);
+          const uint32_t k_addr = smem_u32(stage_base + (2 * s) * kSlotBytes);
+          const uint32_t d = tmem + 256u * k;
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
+            mma_bf16_ss(d, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), idesc_s,
+                        kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bar.s_full[k]);
+        };
+        auto issue_pv = [&](int k, int j) {
+          const int e = event_of(mode, k, j, nt0, nt1);
+          const int s = e % NS;
+          mbar_wait(&bar.p_full[k], j & 1);
+          mbar_wait(&bar.v_full[s], (e / NS) & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(stage_base + (2 * s + 1) * kSlotBytes);
+          const uint32_t o = tmem + 256u * k + 128u;
+          const uint32_t pa = tmem + 256u * k;
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            // B = V[16 keys][128 d], MN-major: 16 keys = 2048 B down each 64-column chunk
+            mma_bf16_ts(o, pa + 8 * kk, sdesc_sw128(v_addr + kk * 2048, kChunkBytes, 1024), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          // the stage is free after the last consumer's PV
+          const bool last = mode != TC_SHARED || k == 1 || j >= nt[1];
+          if (last) mma_commit(&bar.kv_empty[s]);
+          if (j == nt[k] - 1) mma_commit(&bar.o_final[k]);
+        };
+        for (int k = 0; k < 2; ++k)
+          if (nt[k] > 0) issue_s(k, 0);
+        const int jmax = max(nt0, nt1);
+        for (int j = 0; j < jmax; ++j) {
+          for (int k = 0; k < 2; ++k) {
+            if (j < nt[k]) {
+              issue_pv(k, j);
+              if (j + 1 < nt[k]) issue_s(k, j + 1);
+            }
+          }
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc_s = idesc_bf16(kM, kBN, 0, 0);   // Q K-major, K K-major
-    constexpr uint32_t idesc_o = idesc_bf16(kM, kD, 0, 1);    // P K-major, V MN-major
-    const uint32_t q_addr = smem_u32(sm.q);
-    const uint32_t p_addr = smem_u32(sm.p);
-    const bool leader = elect_one();
-    if (leader) mbar_wait(&sm.q_full, 0);
-    tc_fence_after();
-    auto issue_pv = [&](int i) {
-      const int s = i % kNS;
-      if (leader) {
-        mbar_wait(&sm.v_full[s], (i / kNS) & 1);
-        mbar_wait(&sm.p_full, i & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sm.v[s]);
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          // A = P[128 rows][16 keys]: key chunk kk/4, 32-byte step inside the swizzle atom
-          const uint64_t a = sdesc_sw128(p_addr + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
-          // B = V[16 keys][128 d] MN-major: 16 keys = 2048 B into each 64-column chunk
-          const uint64_t b = sdesc_sw128(v_addr + kk * 2048, kChunkBytes, 1024);
-          mma_bf16_ss(tmem + 256, a, b, idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(&sm.kv_empty[s]);
-        mma_commit(&sm.o_done);
-      }
-      __syncwarp();
-    };
-    for (int j = 0; j < nt; ++j) {
-      const int s = j % kNS;
-      if (leader) {
-        mbar_wait(&sm.k_full[s], (j / kNS) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sm.k[s]);
-        const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * 128;
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
-          const uint64_t a = sdesc_sw128(q_addr + off, 16, 1024);
-          const uint64_t b = sdesc_sw128(k_addr + off, 16, 1024);
-          mma_bf16_ss(d_tmem, a, b, idesc_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&sm.s_full[j & 1]);
-      }
-      __syncwarp();
-      if (j >= 1) issue_pv(j - 1);
-    }
-    if (nt > 0) issue_pv(nt - 1);
-  } else if (warp >= 4) {
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     // ------------------------------------------------------------- softmax + epilogue
-    const int r = threadIdx.x - 128;               // row == TMEM lane
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const float c = p.scale_log2;
-    const int tok = wu.q_tok0 + r / G;             // token of this row within the segment
-    float m_run = -CUDART_INF_F;                   // running max of raw scores
-    float l_run = 0.f;
-    uint8_t* prow = sm.p + r * 128;
-    const int sw = r & 7;
-    for (int j = 0; j < nt; ++j) {
-      const int tile = wu.tile_lo + j;
-      const bool is_pool = tile < n_pool_tiles;
-      const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBN;
-      mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      float sv[kBN];
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        uint32_t regs[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(j & 1) * 128 + q4 * 32, regs);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[q4 * 32 + i] = __uint_as_float(regs[i]);
-      }
-      // masking: pool tiles past n_slots / inside the R0 pad hole; tail tiles causal
-      int lim_lo = 0, lim_hi = kBN;        // valid key range [lim_lo, lim_hi) relative to key0
-      int hole_lo = 0, hole_hi = 0;
-      if (is_pool) {
-        lim_hi = min(kBN, sg.n_slots - key0);
-        hole_lo = max(0, sg.hole_lo - key0);
-        hole_hi = max(0, min(kBN, sg.hole_hi - key0));
-      } else {
-        const int last = p.fault == 2 ? tok - 1 : tok;   // row sees own keys 0..tok
-        lim_hi = max(0, min(kBN, min(sg.m, last + 1) - key0));
-      }
-      float mt = -CUDART_INF_F;
-#pragma unroll
-      for (int i = 0; i < kBN; ++i) {
-        const bool ok = i >= lim_lo && i < lim_hi && !(i >= hole_lo && i < hole_hi);
-        sv[i] = ok ? sv[i] : -CUDART_INF_F;
-        mt = fmaxf(mt, sv[i]);
-      }
-      const float m_new = fmaxf(m_run, mt);
-      const bool rescale = m_new > m_run + kRescaleThreshold / c || (m_run == -CUDART_INF_F);
-      float alpha = 1.f;
-      if (rescale) {
-        alpha = (m_run == -CUDART_INF_F) ? 0.f : exp2f((m_run - m_new) * c);
-        m_run = m_new;
-      }
-      const float mc = (m_run == -CUDART_INF_F) ? 0.f : m_run * c;
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < kBN; ++i) {
-        sv[i] = exp2f(fmaf(sv[i], c, -mc));
-        sum += sv[i];
-      }
-      // P buffer and O are free once PV(j-1) completed
-      if (j >= 1) {
-        mbar_wait(&sm.o_done, (j - 1) & 1);
+    const int k = (warp - 4) >> 2;                 // slot
+    const bool active = (k == 0) || pr.ub >= 0;
+    const WorkUnit w = k ? w1 : w0;
+    const int nt = k ? nt1 : nt0;
+    if (active) {
+      const SegDesc sg = p.segs[w.seg];
+      const int r = threadIdx.x - 128 - 128 * k;   // row == TMEM lane
+      const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+      const uint32_t s_col = tmem + lane_base + 256u * k;
+      const uint32_t o_col = s_col + 128u;
+      const float c = p.scale_log2;
+      const int G = p.G;
+      const int tok = w.q_tok0 + r / G;
+      const int last_key = min(sg.m - 1, p.fault == 2 ? tok - 1 : tok);   // own keys 0..tok (R-2)
+      const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
+      float m_run = -CUDART_INF_F;
+      float l_run = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        const int tile = w.tile_lo + j;
+        const bool is_pool = tile < n_pool_tiles;
+        const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBN;
+        mbar_wait(&bar.s_full[k], j & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, rescale && alpha != 1.f)) {
+        float sv[kBN];
+        {
+          uint32_t ra[32], rb[32], rc[32], rd[32];
+          tmem_ld32(s_col + 0, ra);
+          tmem_ld32(s_col + 32, rb);
+          tmem_ld32(s_col + 64, rc);
+          tmem_ld32(s_col + 96, rd);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            sv[i] = __uint_as_float(ra[i]);
+            sv[32 + i] = __uint_as_float(rb[i]);
+            sv[64 + i] = __uint_as_float(rc[i]);
+            sv[96 + i] = __uint_as_float(rd[i]);
+          }
+        }
+        bool need_mask;
+        int lim, hlo = 0, hhi = 0;
+        if (is_pool) {
+          lim = sg.n_slots - key0;
+          hlo = sg.hole_lo - key0;
+          hhi = sg.hole_hi - key0;
+          need_mask = lim < kBN || (hhi > 0 && hlo < kBN && hhi > hlo);
+        } else {
+          lim = last_key - key0 + 1;
+          need_mask = lim < kBN;
+        }
+        if (__any_sync(0xffffffffu, need_mask)) {
+#pragma unroll
+          for (int i = 0; i < kBN; ++i) {
+            const bool ok = i < lim && !(i >= hlo && i < hhi);
+            sv[i] = ok ? sv[i] : -CUDART_INF_F;
+          }
+        }
+        float mt = sv[0];
+#pragma unroll
+        for (int i = 1; i < kBN; ++i) mt = fmaxf(mt, sv[i]);
+        float alpha = 1.f;
+        if (mt > m_run + kRescaleLog2 / c || m_run == -CUDART_INF_F) {
+          const float m_new = fmaxf(m_run, mt);
+          alpha = (m_run == -CUDART_INF_F) ? 0.f : ex2((m_run - m_new) * c);
+          m_run = m_new;
+        }
+        const float mc = (m_run == -CUDART_INF_F) ? 0.f : m_run * c;
+        uint32_t pk[kBN / 2];
+        float2 sum2 = make_float2(0.f, 0.f);
+        const float2 c2 = make_float2(c, c), nmc2 = make_float2(-mc, -mc);
+#pragma unroll
+        for (int i = 0; i < kBN / 2; ++i) {
+          const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), c2, nmc2);
+          const float2 e = make_float2(ex2(x.x), ex2(x.y));
+          sum2 = __fadd2_rn(sum2, e);
+          pk[i] = pack_bf16(e.x, e.y);
+        }
+        l_run = l_run * alpha + (sum2.x + sum2.y);
+        // O rescale (PV(j-1) completed: s_full(j) committed after it)
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t regs[32];
-            const uint32_t a = tmem + lane_base + 256 + q4 * 32;
-            tmem_ld32(a, regs);
+            uint32_t ro[32];
+            tmem_ld32(o_col + q4 * 32, ro);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) regs[i] = __float_as_uint(__uint_as_float(regs[i]) * alpha);
-            tmem_st32(a, regs);
-          }
-          tmem_wait_st();
-        }
-      }
-      l_run = l_run * alpha + sum;
-      // P row -> smem, bf16, 128B-swizzled K-major (two 64-key chunks)
-#pragma unroll
-      for (int g = 0; g < 16; ++g) {
-        const int chunk = g >> 3, gi = g & 7;
-        uint4 v;
-        v.x = pack_bf16(sv[g * 8 + 0], sv[g * 8 + 1]);
-        v.y = pack_bf16(sv[g * 8 + 2], sv[g * 8 + 3]);
-        v.z = pack_bf16(sv[g * 8 + 4], sv[g * 8 + 5]);
-        v.w = pack_bf16(sv[g * 8 + 6], sv[g * 8 + 7]);
-        *reinterpret_cast<uint4*>(prow + chunk * kChunkBytes + ((gi ^ sw) << 4)) = v;
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.p_full);
-    }
-    // ------------------------------------------------------------- epilogue
-    const int rows = wu.q_ntok * G;
-    if (nt > 0) {
-      mbar_wait(&sm.o_done, (nt - 1) & 1);
-      tc_fence_after();
-    }
-    const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
-    const int h = wu.kv_head * G + r % G;
-    const int64_t orow = in_row0 + tok;
-#pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
-      uint32_t regs[32];
-      tmem_ld32(tmem + lane_base + 256 + q4 * 32, regs);
-      tmem_wait_ld();
-      if (r < rows) {
-        if (wu.group < 0) {
-          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(regs[i + 0]) * inv_l, __uint_as_float(regs[i + 1]) * inv_l);
-            v.y = pack_bf16(__uint_as_float(regs[i + 2]) * inv_l, __uint_as_float(regs[i + 3]) * inv_l);
-            v.z = pack_bf16(__uint_as_float(regs[i + 4]) * inv_l, __uint_as_float(regs[i + 5]) * inv_l);
-            v.w = pack_bf16(__uint_as_float(regs[i + 6]) * inv_l, __uint_as_float(regs[i + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(out + i) = v;
-          }
-        } else {
-          const int64_t slot = (int64_t)ly * p.n_units + u;
-          float* out = p.part_o + (slot * kM + r) * kD + q4 * 32;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 v = make_float4(__uint_as_float(regs[i]) * inv_l, __uint_as_float(regs[i + 1]) * inv_l,
-                                   __uint_as_float(regs[i + 2]) * inv_l, __uint_as_float(regs[i + 3]) * inv_l);
-            *reinterpret_cast<float4*>(out + i) = v;
+            for (int i = 0; i < 32; i += 2) {
+              const float2 v = __fmul2_rn(make_float2(__uint_as_float(ro[i]), __uint_as_float(ro[i + 1])),
+                                          make_float2(alpha, alpha));
+              ro[i] = __float_as_uint(v.x);
+              ro[i + 1] = __float_as_uint(v.y);
+            }
+            tmem_st32(o_col + q4 * 32, ro);
           }
         }
+        // P (bf16 pairs) into the first 64 columns of this slot's S region
+        {
+          uint32_t lo[32], hi[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) { lo[i] = pk[i]; hi[i] = pk[32 + i]; }
+          tmem_st32(s_col + 0, lo);
+          tmem_st32(s_col + 32, hi);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.p_full[k]);
       }
-    }
-    if (wu.group >= 0 && r < rows) {
-      const int64_t slot = (int64_t)ly * p.n_units + u;
-      p.part_lse[slot * kM + r] = l_run > 0.f ? m_run * c + log2f(l_run) : -CUDART_INF_F;
+      // ----------------------------------------------------------- epilogue
+      if (nt > 0) {
+        mbar_wait(&bar.o_final[k], 0);
+        tc_fence_after();
+      }
+      const int rows = w.q_ntok * G;
+      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+      const int h = w.kv_head * G + r % G;
+      const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+      const int64_t orow = in_l + sg.row0 + tok;
+      const int unit = k ? pr.ub : pr.ua;
+      const int64_t pslot = (int64_t)ly * p.n_units + unit;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t ro[32];
+        tmem_ld32(o_col + q4 * 32, ro);
+        tmem_wait_ld();
+        if (r < rows) {
+          if (w.group < 0) {
+            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(ro[i + 0]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l);
+              v.y = pack_bf16(__uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l);
+              v.z = pack_bf16(__uint_as_float(ro[i + 4]) * inv_l, __uint_as_float(ro[i + 5]) * inv_l);
+              v.w = pack_bf16(__uint_as_float(ro[i + 6]) * inv_l, __uint_as_float(ro[i + 7]) * inv_l);
+              *reinterpret_cast<uint4*>(out + i) = v;
+            }
+          } else {
+            float* out = p.part_o + (pslot * kM + r) * kD + q4 * 32;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              *reinterpret_cast<float4*>(out + i) =
+                  make_float4(__uint_as_float(ro[i]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l,
+                              __uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l);
+            }
+          }
+        }
+      }
+      if (w.group >= 0 && r < rows)
+        p.part_lse[pslot * kM + r] = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
     }
   }
   tc_fence_before();
@@ -391,7 +461,7 @@ bool tc_supported_shape(int D, int G, bool bf16) {
 
 cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, cudaStream_t s) {
   (void)q_tiles_opt;
-  if (p.n_units == 0 || n_layers == 0) return cudaSuccess;
+  if (p.n_pairs == 0 || n_layers == 0) return cudaSuccess;
   if (!tc_supported_shape(p.D, p.G, true)) return cudaErrorNotSupported;
   TcMaps maps;
   const int G = p.G;
@@ -411,7 +481,6 @@ cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, c
   }
   const int box_rows = p.P < kBN ? p.P : kBN;
   {
-    // pool rows: all layers (the map is re-encoded per launch; cheap host call)
     const cuuint64_t prow = (cuuint64_t)(p.layer0 + n_layers) * p.num_pages * p.Hkv * p.P;
     cuuint64_t dims[2] = {(cuuint64_t)kD, prow};
     cuuint64_t str[1] = {(cuuint64_t)kD * 2};
@@ -419,14 +488,14 @@ cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, c
     if (!encode(&maps.pk, p.poolK, 2, dims, str, box)) return cudaErrorInvalidValue;
     if (!encode(&maps.pv, p.poolV, 2, dims, str, box)) return cudaErrorInvalidValue;
   }
-  const size_t smem = sizeof(TcSmem) + 1024;
+  const size_t smem = (size_t)kNumSlots * kSlotBytes + sizeof(Bars) + 1024;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(p.n_units, n_layers);
+  dim3 grid(p.n_pairs, n_layers);
   attn_tc_kernel<<<grid, kThreads, smem, s>>>(p, maps, box_rows);
   return cudaGetLastError();
 }

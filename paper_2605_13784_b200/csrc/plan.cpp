@@ -7,6 +7,7 @@
 // launch fills the GPU (148 SMs on B200).  Units of one (segment, q tile, kv
 // head) form a Group merged by the combine kernel (log-sum-exp, reading R-11).
 #include <algorithm>
+#include <tuple>
 #include <cstdint>
 #include <vector>
 
@@ -98,6 +99,73 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
     }
     if (group >= 0) out->groups.push_back({it.seg, it.kvh, it.tok0, it.ntok, unit0, (int)n});
   }
+}
+
+// Two units can share K/V tile loads (SHARED) when every tile index of the
+// shorter one maps to the same keys in both: same segment and same tile_lo, or
+// same cached pool (pages, slots, hole) with both ranges inside the pool tiles.
+static bool same_keys(const std::vector<SegDesc>& segs, const WorkUnit& a, const WorkUnit& b, int key_tile) {
+  if (a.kv_head != b.kv_head || a.tile_lo != b.tile_lo) return false;
+  if (a.seg == b.seg) return true;
+  const SegDesc& x = segs[a.seg];
+  const SegDesc& y = segs[b.seg];
+  if (x.pages != y.pages || x.n_slots != y.n_slots || x.hole_lo != y.hole_lo || x.hole_hi != y.hole_hi) return false;
+  const int pool_tiles = (x.n_slots + key_tile - 1) / key_tile;
+  return std::max(a.tile_hi, b.tile_hi) <= pool_tiles;
+}
+
+void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out) {
+  out->clear();
+  const int n = (int)plan.units.size();
+  std::vector<char> used(n, 0);
+  // SHARED: bucket by (kv_head, tile_lo, pool identity or seg); pair neighbours.
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  auto key_of = [&](int i) {
+    const WorkUnit& u = plan.units[i];
+    const SegDesc& s = segs[u.seg];
+    return std::make_tuple(u.kv_head, u.tile_lo, (uintptr_t)s.pages, s.n_slots, u.seg, u.tile_hi);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key_of(a) < key_of(b); });
+  for (int ii = 0; ii < n; ++ii) {
+    const int a = order[ii];
+    if (used[a]) continue;
+    for (int jj = ii + 1; jj < n && jj < ii + 64; ++jj) {
+      const int b = order[jj];
+      if (used[b]) continue;
+      if (plan.units[a].q_tok0 == plan.units[b].q_tok0 && plan.units[a].seg == plan.units[b].seg) continue;
+      if (same_keys(segs, plan.units[a], plan.units[b], key_tile)) {
+        used[a] = used[b] = 1;
+        out->push_back({a, b, TC_SHARED, 0});
+        break;
+      }
+    }
+  }
+  // SPLIT: remaining units of one group, consecutive splits.
+  for (int i = 0; i < n; ++i) {
+    if (used[i]) continue;
+    const WorkUnit& u = plan.units[i];
+    int partner = -1;
+    if (u.group >= 0) {
+      for (int j = i + 1; j < n; ++j) {
+        if (!used[j] && plan.units[j].group == u.group) { partner = j; break; }
+      }
+    }
+    used[i] = 1;
+    if (partner >= 0) {
+      used[partner] = 1;
+      out->push_back({i, partner, TC_SPLIT, 0});
+    } else {
+      out->push_back({i, -1, TC_SINGLE, 0});
+    }
+  }
+  // Largest CTA first.
+  auto work = [&](const TcPair& p) {
+    const int wa = plan.units[p.ua].tile_hi - plan.units[p.ua].tile_lo;
+    const int wb = p.ub >= 0 ? plan.units[p.ub].tile_hi - plan.units[p.ub].tile_lo : 0;
+    return p.mode == TC_SHARED ? std::max(wa, wb) : wa + wb;
+  };
+  std::stable_sort(out->begin(), out->end(), [&](const TcPair& a, const TcPair& b) { return work(a) > work(b); });
 }
 
 }  // namespace ssa

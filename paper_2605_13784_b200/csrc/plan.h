@@ -26,4 +26,8 @@ struct Plan {
 
 void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out);
 
+// Pair units into two-slot tcgen05 CTAs (SHARED first, then SPLIT, then SINGLE),
+// largest work first.
+void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out);
+
 }  // namespace ssa

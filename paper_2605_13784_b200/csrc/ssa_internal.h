@@ -51,6 +51,19 @@ struct Group {
   int32_t n_splits;
 };
 
+// tcgen05 CTA = up to two work units ("slots") run by two softmax warpgroups.
+//   SHARED: both slots read the same key tiles (one TMA load feeds both) with
+//           different q tiles — the K/V tile is reused by 256 rows.
+//   SPLIT:  both slots use the same q tile over different key ranges (two
+//           splits of one group), each with its own K/V stream.
+//   SINGLE: one slot.
+enum TcMode : int32_t { TC_SINGLE = 0, TC_SHARED = 1, TC_SPLIT = 2 };
+struct TcPair {
+  int32_t ua, ub;   // unit indices (ub = -1 for SINGLE)
+  int32_t mode;
+  int32_t pad;
+};
+
 struct AttnParams {
   const void* Q;         // [n_layers_in][rows_per_layer][Hq][D]
   const void* Kt;        // [n_layers_in][rows_per_layer][Hkv][D]  (segment "tail" keys)
@@ -74,6 +87,8 @@ struct AttnParams {
   int32_t rows_tile;     // rows per unit (q tile tokens * G)
   int32_t key_tile;      // keys per tile (SIMT 64, tcgen05 128)
   int32_t fault;         // SSA_OPT_FAULT_INJECT
+  const TcPair* pairs;   // tcgen05 CTAs (per layer)
+  int32_t n_pairs;
 };
 
 // Append scatter (KA): copy new K/V rows into pages, bit-exact.
@@ -126,7 +141,7 @@ struct CombineParams {
 
 // Kernel launchers (kernels_*.cu).  Return cudaGetLastError() after launch.
 cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s);
-cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s);
+cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits);
 cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
 cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
 int simt_rows_tile(int G, int D);     // rows per SIMT unit

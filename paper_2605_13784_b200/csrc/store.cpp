@@ -320,13 +320,15 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     pc.q_tile_tokens = std::max(1, (use_tc ? tc_rows_tile() : simt_rows_tile(G, D)) / G);
     pc.n_layers = n_layers;
     pc.num_sms = num_sms;
-    pc.ctas_per_sm = use_tc ? 1 : 2;
+    pc.ctas_per_sm = 2;   // SIMT: 2 CTAs/SM; tcgen05: 2 slots per CTA
     pc.max_splits = (int)opt_max_splits;
     pc.min_tiles_per_unit = use_tc ? 2 : 2;
     pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
     pc.fault = (int)opt_fault;
     plan_units(segs, pc, &plan);
   }
+  std::vector<TcPair> pairs;
+  if (use_tc) pair_units(segs, plan, pc.key_tile, &pairs);
   // ---- append segments for the scatter
   std::vector<int32_t> app_idx;
   for (int i = 0; i < (int)segs.size(); ++i)
@@ -343,8 +345,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   const size_t b_groups = plan.groups.size() * sizeof(Group);
   const size_t b_app = app_segs.size() * sizeof(SegDesc);
   const size_t b_pre = prefix.size() * sizeof(int32_t);
+  const size_t b_pairs = pairs.size() * sizeof(TcPair);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre);
+  const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre) + al(b_pairs);
   const size_t off = ring.alloc(total);
   if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
   size_t o = off;
@@ -359,6 +362,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   auto d_groups = reinterpret_cast<const Group*>(put(plan.groups.data(), b_groups));
   auto d_app = reinterpret_cast<const SegDesc*>(put(app_segs.data(), b_app));
   auto d_pre = reinterpret_cast<const int32_t*>(put(prefix.data(), b_pre));
+  auto d_pairs = reinterpret_cast<const TcPair*>(put(pairs.data(), b_pairs));
   SSA_CUDA(this, ring.to_device(off, total, st));
 
   // ---- KA: scatter new K/V into pages
@@ -421,6 +425,8 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.rows_tile = rows_tile;
     ap.key_tile = pc.key_tile;
     ap.fault = (int32_t)opt_fault;
+    ap.pairs = d_pairs;
+    ap.n_pairs = (int32_t)pairs.size();
     cudaEvent_t t0 = tick(st);
     if (use_tc) {
       SSA_CUDA(this, launch_attn_tc(ap, n_layers, (int)opt_tc_qtiles, st));
@@ -448,7 +454,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       cp.D = D;
       cp.write_o = 1;
       cudaEvent_t t1 = tick(st);
-      SSA_CUDA(this, launch_combine(cp, n_layers, cfg.dtype == SSA_BF16, st));
+      int max_split = 1;
+      for (auto& g : plan.groups) max_split = std::max(max_split, g.n_splits);
+      SSA_CUDA(this, launch_combine(cp, n_layers, cfg.dtype == SSA_BF16, st, max_split));
       if (t1) timed_push(query_plane ? 3 : 2, t1, tick(st));
       stats.kernel_launches++;
     }
