@@ -393,7 +393,7 @@ class OracleStore:
     def truncate(self, sid, p):
         """SeqRemove(s, p, inf) (Alg. 3 L540/L547): drop tokens >= p, free pages."""
         s = self._check(sid)
-        if p < 0 or p > s.n_tokens:
+        if p < s.n_prefix or p > s.n_tokens:      # Region 0 is frozen (reading R-17)
             raise OracleError("INVALID_ARG")
         if p == s.n_tokens:
             return s.version

@@ -1,11 +1,11 @@
 // kernels_tc.cu — tensor-core (tcgen05 / TMEM / TMA) attention for sm_100a.
 //
 // A CTA runs up to two work units ("slots", plan.cpp pair_units) with two
-// softmax warpgroups that ping-pong against one MMA issuer:
-//   SHARED  two q tiles over the same key tiles: each TMA-loaded K/V tile feeds
-//           256 query rows (halves L2->SM traffic for prefill / flash batches);
-//   SPLIT   one q tile over two key ranges (two split-KV partials; query plane);
-//   SINGLE  one slot.
+// softmax warpgroups that ping-pong against one MMA issuer.  The first
+// n_shared key tiles are common to both slots and loaded once (each K/V tile
+// then feeds 256 query rows: the q tiles of an append, or Flash Queries over
+// one cached pool); later tiles are private to a slot (own-token tails, or the
+// two key ranges of a split pair that shares one q tile).
 // Per slot and key tile of 128 keys (Eq. attention P:145 on the rows of Eq.
 // query-attention P:150-155; causal tail, reading R-2):
 //     S = Q K^T         tcgen05.mma M=128 N=128 K=128 -> TMEM (fp32)
@@ -83,16 +83,13 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
-struct SlotInfo {
-  int tile_lo, nt;
-};
-
-// Load-event index of (slot k, tile j): SHARED loads tile j once for both slots;
-// SPLIT/SINGLE interleave the two slots' streams.
-__device__ __forceinline__ int event_of(int mode, int k, int j, int nt0, int nt1) {
-  if (mode == TC_SHARED) return j;
-  const int m = min(nt0, nt1);
-  return j < m ? 2 * j + k : 2 * m + (j - m);
+// Load-event index of (slot k, tile j): shared tiles are one event each; after
+// them the two slots' private tiles interleave.
+__device__ __forceinline__ int event_of(int k, int j, int nsh, int nt0, int nt1) {
+  if (j < nsh) return j;
+  const int jj = j - nsh;
+  const int m = min(nt0, nt1) - nsh;
+  return nsh + (jj < m ? 2 * jj + k : 2 * m + (jj - m));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -105,7 +102,6 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   const int lane = threadIdx.x & 31;
   const int ly = blockIdx.y;
   const TcPair pr = p.pairs[blockIdx.x];
-  const int mode = pr.mode;
   const WorkUnit w0 = p.units[pr.ua];
   WorkUnit w1 = w0;
   int nt1 = 0;
@@ -114,10 +110,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     nt1 = w1.tile_hi - w1.tile_lo;
   }
   const int nt0 = w0.tile_hi - w0.tile_lo;
-  const int NS = mode == TC_SHARED ? 2 : 3;
-  // smem tile slots
-  uint8_t* q_buf[2] = {tiles, mode == TC_SHARED ? tiles + kSlotBytes : tiles};
-  uint8_t* stage_base = tiles + (mode == TC_SHARED ? 2 : 1) * kSlotBytes;   // K(s) = base + 2s slots, V(s) = +1
+  const int nsh = pr.ub >= 0 ? pr.n_shared : 0;
+  const bool two_q = pr.ub >= 0 && !pr.same_q;
+  const int NS = two_q ? 2 : 3;
+  // smem tile slots: Q (1 or 2), then NS stages of (K, V)
+  uint8_t* q_buf[2] = {tiles, two_q ? tiles + kSlotBytes : tiles};
+  uint8_t* stage_base = tiles + (two_q ? 2 : 1) * kSlotBytes;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.q);
@@ -151,7 +149,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       if (elect_one()) {
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
-        const int nq = mode == TC_SHARED ? 2 : 1;
+        const int nq = two_q ? 2 : 1;
         mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
         for (int k = 0; k < nq; ++k) {
           const WorkUnit& w = k ? w1 : w0;
@@ -159,13 +157,13 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           for (int c = 0; c < 2; ++c)
             tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
         }
-        const int E = mode == TC_SHARED ? max(nt0, nt1) : nt0 + nt1;
-        const int m01 = min(nt0, nt1);
+        const int E = nt0 + nt1 - nsh;
+        const int m01 = min(nt0, nt1) - nsh;
         for (int e = 0; e < E; ++e) {
           int k, j;
-          if (mode == TC_SHARED) { k = 0; j = e; }
-          else if (e < 2 * m01) { k = e & 1; j = e >> 1; }
-          else { k = nt0 > nt1 ? 0 : 1; j = m01 + (e - 2 * m01); }
+          if (e < nsh) { k = 0; j = e; }
+          else if (e - nsh < 2 * m01) { k = (e - nsh) & 1; j = nsh + ((e - nsh) >> 1); }
+          else { k = nt0 > nt1 ? 0 : 1; j = nsh + m01 + (e - nsh - 2 * m01); }
           const WorkUnit& w = k ? w1 : w0;
           const SegDesc sg = p.segs[w.seg];
           const int s = e % NS;
@@ -214,7 +212,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         mbar_wait(&bar.q_full, 0);
         tc_fence_after();
         auto issue_s = [&](int k, int j) {
-          const int e = event_of(mode, k, j, nt0, nt1);
+          const int e = event_of(k, j, nsh, nt0, nt1);
           const int s = e % NS;
           mbar_wait(&bar.k_full[s], (e / NS) & 1);
           tc_fence_after();
@@ -230,7 +228,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           mma_commit(&bar.s_full[k]);
         };
         auto issue_pv = [&](int k, int j) {
-          const int e = event_of(mode, k, j, nt0, nt1);
+          const int e = event_of(k, j, nsh, nt0, nt1);
           const int s = e % NS;
           mbar_wait(&bar.p_full[k], j & 1);
           mbar_wait(&bar.v_full[s], (e / NS) & 1);
@@ -244,9 +242,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
             mma_bf16_ts(o, pa + 8 * kk, sdesc_sw128(v_addr + kk * 2048, kChunkBytes, 1024), idesc_o,
                         (j > 0 || kk > 0) ? 1u : 0u);
           }
-          // the stage is free after the last consumer's PV
-          const bool last = mode != TC_SHARED || k == 1 || j >= nt[1];
-          if (last) mma_commit(&bar.kv_empty[s]);
+          // a shared stage is free after slot 1's PV, a private one after its own
+          if (j >= nsh || k == 1) mma_commit(&bar.kv_empty[s]);
           if (j == nt[k] - 1) mma_commit(&bar.o_final[k]);
         };
         for (int k = 0; k < 2; ++k)

@@ -101,69 +101,71 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
   }
 }
 
-// Two units can share K/V tile loads (SHARED) when every tile index of the
-// shorter one maps to the same keys in both: same segment and same tile_lo, or
-// same cached pool (pages, slots, hole) with both ranges inside the pool tiles.
-static bool same_keys(const std::vector<SegDesc>& segs, const WorkUnit& a, const WorkUnit& b, int key_tile) {
-  if (a.kv_head != b.kv_head || a.tile_lo != b.tile_lo) return false;
-  if (a.seg == b.seg) return true;
+// Leading key tiles two units can share: same KV head and start tile, and the
+// same keys behind those tile indices (same segment, or the same cached pool for
+// the pool part of the tile list).
+static int shared_tiles(const std::vector<SegDesc>& segs, const WorkUnit& a, const WorkUnit& b, int key_tile) {
+  if (a.kv_head != b.kv_head || a.tile_lo != b.tile_lo) return -1;
+  const int na = a.tile_hi - a.tile_lo, nb = b.tile_hi - b.tile_lo;
+  if (a.seg == b.seg) return std::min(na, nb);
   const SegDesc& x = segs[a.seg];
   const SegDesc& y = segs[b.seg];
-  if (x.pages != y.pages || x.n_slots != y.n_slots || x.hole_lo != y.hole_lo || x.hole_hi != y.hole_hi) return false;
+  if (x.pages != y.pages || x.n_slots != y.n_slots || x.hole_lo != y.hole_lo || x.hole_hi != y.hole_hi) return -1;
   const int pool_tiles = (x.n_slots + key_tile - 1) / key_tile;
-  return std::max(a.tile_hi, b.tile_hi) <= pool_tiles;
+  return std::max(0, std::min(std::min(na, nb), pool_tiles - a.tile_lo));
 }
 
 void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out) {
   out->clear();
   const int n = (int)plan.units.size();
   std::vector<char> used(n, 0);
-  // SHARED: bucket by (kv_head, tile_lo, pool identity or seg); pair neighbours.
+  // 1. shared-key pairs: bucket by (kv_head, tile_lo, pool), pair neighbours
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;
   auto key_of = [&](int i) {
     const WorkUnit& u = plan.units[i];
     const SegDesc& s = segs[u.seg];
-    return std::make_tuple(u.kv_head, u.tile_lo, (uintptr_t)s.pages, s.n_slots, u.seg, u.tile_hi);
+    return std::make_tuple(u.kv_head, u.tile_lo, (uintptr_t)s.pages, s.n_slots, u.seg, -(u.tile_hi - u.tile_lo));
   };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key_of(a) < key_of(b); });
   for (int ii = 0; ii < n; ++ii) {
     const int a = order[ii];
     if (used[a]) continue;
-    for (int jj = ii + 1; jj < n && jj < ii + 64; ++jj) {
+    for (int jj = ii + 1; jj < n && jj < ii + 8; ++jj) {
       const int b = order[jj];
       if (used[b]) continue;
-      if (plan.units[a].q_tok0 == plan.units[b].q_tok0 && plan.units[a].seg == plan.units[b].seg) continue;
-      if (same_keys(segs, plan.units[a], plan.units[b], key_tile)) {
+      const WorkUnit& ua = plan.units[a];
+      const WorkUnit& ub = plan.units[b];
+      if (ua.seg == ub.seg && ua.q_tok0 == ub.q_tok0) continue;   // same q tile: split pair below
+      const int sh = shared_tiles(segs, ua, ub, key_tile);
+      if (sh > 0) {
         used[a] = used[b] = 1;
-        out->push_back({a, b, TC_SHARED, 0});
+        out->push_back({a, b, sh, 0});
         break;
       }
     }
   }
-  // SPLIT: remaining units of one group, consecutive splits.
+  // 2. split pairs: two key ranges of one q tile (same group)
   for (int i = 0; i < n; ++i) {
     if (used[i]) continue;
     const WorkUnit& u = plan.units[i];
     int partner = -1;
-    if (u.group >= 0) {
-      for (int j = i + 1; j < n; ++j) {
+    if (u.group >= 0)
+      for (int j = i + 1; j < n; ++j)
         if (!used[j] && plan.units[j].group == u.group) { partner = j; break; }
-      }
-    }
     used[i] = 1;
     if (partner >= 0) {
       used[partner] = 1;
-      out->push_back({i, partner, TC_SPLIT, 0});
+      out->push_back({i, partner, 0, 1});
     } else {
-      out->push_back({i, -1, TC_SINGLE, 0});
+      out->push_back({i, -1, 0, 1});
     }
   }
-  // Largest CTA first.
+  // Largest CTA first (tiles loaded + tiles computed).
   auto work = [&](const TcPair& p) {
     const int wa = plan.units[p.ua].tile_hi - plan.units[p.ua].tile_lo;
     const int wb = p.ub >= 0 ? plan.units[p.ub].tile_hi - plan.units[p.ub].tile_lo : 0;
-    return p.mode == TC_SHARED ? std::max(wa, wb) : wa + wb;
+    return 2 * (wa + wb) + (wa + wb - p.n_shared);
   };
   std::stable_sort(out->begin(), out->end(), [&](const TcPair& a, const TcPair& b) { return work(a) > work(b); });
 }

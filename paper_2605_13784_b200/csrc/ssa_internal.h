@@ -52,16 +52,15 @@ struct Group {
 };
 
 // tcgen05 CTA = up to two work units ("slots") run by two softmax warpgroups.
-//   SHARED: both slots read the same key tiles (one TMA load feeds both) with
-//           different q tiles — the K/V tile is reused by 256 rows.
-//   SPLIT:  both slots use the same q tile over different key ranges (two
-//           splits of one group), each with its own K/V stream.
-//   SINGLE: one slot.
-enum TcMode : int32_t { TC_SINGLE = 0, TC_SHARED = 1, TC_SPLIT = 2 };
+// The first n_shared key tiles of both slots are the same keys: each TMA load
+// feeds both slots (256 query rows per K/V tile: the q tiles of one append, or
+// Flash Queries over one cached pool).  Later tiles are private to a slot and
+// loaded separately (own-token tails; the two halves of a split).  same_q: both
+// slots use one q tile (a split pair), so only one Q buffer is needed.
 struct TcPair {
-  int32_t ua, ub;   // unit indices (ub = -1 for SINGLE)
-  int32_t mode;
-  int32_t pad;
+  int32_t ua, ub;     // unit indices (ub = -1: single slot)
+  int32_t n_shared;   // leading tiles shared by both slots
+  int32_t same_q;
 };
 
 struct AttnParams {

@@ -367,3 +367,27 @@ def test_streams_torch_matches_numpy_on_gpu(cuda):
         a = streams.gen_tensor_np(spec, 2, 0, 1, streams.TENSOR_K, 50, 40, 8, 128, hkv=8)
         b = streams.gen_tensor_torch(spec, 2, 0, 1, streams.TENSOR_K, 50, 40, 8, 128, hkv=8, device=cuda)
         assert np.array_equal(a, from_dev(b))
+
+
+def test_flash_query_batch_64x32(cuda):
+    """BJ.configs[3] shape at small context: 64 registered 32-token questions in one launch
+    (pairs share the cached K/V tiles, private own-token tails)."""
+    import torch
+    spec = streams.StreamSpec("market", seed=14)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=1000, appends=(200,), num_pages=128)
+    k, m = 64, 32
+    layer = 1
+    qs = [gen_qkv(spec, 1, LL["hq"], LL["hkv"], LL["d"], streams.FLASH_DOMAIN + i, 0, m, layers=[layer])
+          for i in range(k)]
+    Q = np.concatenate([q[0] for q in qs], axis=1)
+    K = np.concatenate([q[1] for q in qs], axis=1)
+    V = np.concatenate([q[2] for q in qs], axis=1)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    st.stats(reset=True)
+    st.flash_query_batch(sid, [m] * k, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O, layer=layer)
+    assert st.stats()["tc_launches"] == 1
+    got = from_dev(O)[0]
+    for i in (0, 1, 17, 62, 63):
+        want = ref.flash_query_batch(rsid, [(qs[i][0][0], qs[i][1][0], qs[i][2][0])], layer)[0]
+        ok, e = within(got[i * m:(i + 1) * m], want, "bf16")
+        assert ok, (i, e)
