@@ -306,6 +306,21 @@ ssa_status ssa_sharded_query(ssa_store_t store, ssa_session_t session, int32_t l
 
 ssa_status ssa_comm_destroy(ssa_store_t store);
 
+/* Building blocks of ssa_sharded_query, usable without NCCL.
+ * ssa_sharded_partial: the rank partial of the n_q query rows over this
+ * store's shard of the session (include_tail != 0: this rank also covers the
+ * query's own tokens, i.e. it is the tail owner).  Writes one packed chunk of
+ * rows*Hq*(d+1) floats to device memory `part`: O fp32 [L'][n_q][Hq][d] (each
+ * row normalized over the shard) followed by lse [L'][n_q][Hq] in log2 units
+ * (-inf for a row with no visible key on this shard).
+ * ssa_merge_rank_partials: merges `world` consecutive chunks (device) into O
+ * (log-sum-exp, R-11); rows = L' * n_q. */
+ssa_status ssa_sharded_partial(ssa_store_t store, ssa_session_t session, int32_t layer, int32_t n_q,
+                               const void *Q, const void *K, const void *V, int32_t include_tail,
+                               float *part, void *stream);
+ssa_status ssa_merge_rank_partials(ssa_store_t store, int32_t world, int64_t rows, const float *parts,
+                                   void *O, void *stream);
+
 /* ----------------------------------------------------------------------------
  * Diagnostics
  * -------------------------------------------------------------------------- */

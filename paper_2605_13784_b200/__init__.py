@@ -96,6 +96,8 @@ def _load():
         "ssa_comm_init": (i32, [vp, i32, i32, P(ctypes.c_uint8)]),
         "ssa_sharded_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "ssa_comm_destroy": (i32, [vp]),
+        "ssa_sharded_partial": (i32, [vp, i32, i32, i32, vp, vp, vp, i32, vp, vp]),
+        "ssa_merge_rank_partials": (i32, [vp, i32, i64, vp, vp, vp]),
         "ssa_status_str": (ctypes.c_char_p, [i32]),
         "ssa_last_error": (ctypes.c_char_p, []),
         "ssa_abi_version": (i32, []),
@@ -305,6 +307,19 @@ class Store:
     def comm_init(self, rank, world, uid: bytes):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib.ssa_comm_init(self._h, rank, world, buf), "comm_init")
+
+    def sharded_partial(self, sid, Q, K, V, part, include_tail, layer=-1, stream=None, n_q=None):
+        """Rank partial over this store's shard -> packed fp32 chunk [O | lse] (device `part`)."""
+        n = n_q if n_q is not None else _ntok(K)
+        _check(lib.ssa_sharded_partial(self._h, sid, layer, n, _ptr(Q), _ptr(K), _ptr(V), int(include_tail),
+                                       _ptr(part), _stream(stream)), "sharded_partial")
+
+    def merge_rank_partials(self, world, rows, parts, O, stream=None):
+        _check(lib.ssa_merge_rank_partials(self._h, world, rows, _ptr(parts), _ptr(O), _stream(stream)),
+               "merge_rank_partials")
+
+    def comm_destroy(self):
+        _check(lib.ssa_comm_destroy(self._h), "comm_destroy")
 
     def sharded_query(self, sid, Q, K, V, O, layer=-1, stream=None, n_q=None):
         n = n_q if n_q is not None else _ntok(K)

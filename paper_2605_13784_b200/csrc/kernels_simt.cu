@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
           kv = ld_f(PK, off);
           vv = ld_f(PV, off);
         }
-      } else if (key < sg.m) {
+      } else if (key < sg.tail_m) {
         const int64_t off = ((in_row0 + key) * p.Hkv + wu.kv_head) * D + e;
         kv = ld_f(Kt, off);
         vv = ld_f(Vt, off);
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
         valid = valid && key < sg.n_slots && !(key >= sg.hole_lo && key < sg.hole_hi);
       } else {
         const int tok = wu.q_tok0 + r / G;
-        valid = valid && key < sg.m && (p.fault == 2 ? key < tok : key <= tok);
+        valid = valid && key < sg.tail_m && (p.fault == 2 ? key < tok : key <= tok);
       }
       float s = -CUDART_INF_F;
       if (valid) {
@@ -205,8 +205,10 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
     for (int s = 0; s < gr.n_splits; ++s) wsm[s * RT + r] *= inv;
-    if (p.lse_out)
-      p.lse_out[((int64_t)ly * p.n_groups + g) * RT + r] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+    if (p.lse_out) {
+      const int64_t row = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0 + gr.q_tok0 + r / p.G;
+      p.lse_out[row * p.Hq + gr.kv_head * p.G + r % p.G] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+    }
   }
   __syncthreads();
   if (!p.write_o) return;
@@ -225,11 +227,43 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
     }
     const int64_t row = in_row0 + gr.q_tok0 + r / p.G;
     const int h = gr.kv_head * p.G + r % p.G;
-    T* out = static_cast<T*>(p.O) + (row * p.Hq + h) * p.D + e;
-    st_f(out, 0, acc.x);
-    st_f(out, 1, acc.y);
-    st_f(out, 2, acc.z);
-    st_f(out, 3, acc.w);
+    if (p.o_f32) {
+      *reinterpret_cast<float4*>(p.o_f32 + (row * p.Hq + h) * p.D + e) = acc;
+    } else {
+      T* out = static_cast<T*>(p.O) + (row * p.Hq + h) * p.D + e;
+      st_f(out, 0, acc.x);
+      st_f(out, 1, acc.y);
+      st_f(out, 2, acc.z);
+      st_f(out, 3, acc.w);
+    }
+  }
+}
+
+// Cross-rank merge (A9): one warp per (row, head); world packed chunks of
+// [O fp32 rows*Hq*D | lse rows*Hq] (log2 units), reading R-11.
+template <typename T>
+__global__ void __launch_bounds__(256) merge_ranks_kernel(const float* parts, int world, int64_t rows, int Hq, int D,
+                                                          T* O) {
+  const int64_t rh = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (rh >= rows * Hq) return;
+  const int64_t chunk = rows * Hq * (int64_t)(D + 1);
+  const float* lse = parts + rows * Hq * (int64_t)D;
+  float L = -CUDART_INF_F;
+  for (int r = 0; r < world; ++r) L = fmaxf(L, lse[r * chunk + rh]);
+  float wsum = 0.f;
+  for (int r = 0; r < world; ++r) {
+    const float l = lse[r * chunk + rh];
+    if (l != -CUDART_INF_F) wsum += exp2f(l - L);
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  for (int e = lane; e < D; e += 32) {
+    float acc = 0.f;
+    for (int r = 0; r < world; ++r) {
+      const float l = lse[r * chunk + rh];
+      if (l != -CUDART_INF_F) acc = fmaf(exp2f(l - L), parts[r * chunk + rh * D + e], acc);
+    }
+    st_f(O, rh * D + e, acc * inv);
   }
 }
 
@@ -298,6 +332,16 @@ cudaError_t launch_simt_t(const AttnParams& p, int n_layers, cudaStream_t s) {
 }  // namespace
 
 int simt_rows_tile(int G, int D) { (void)G; (void)D; return kRT; }
+
+cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
+                               cudaStream_t s) {
+  const int64_t warps = rows * Hq;
+  if (warps == 0) return cudaSuccess;
+  const int blocks = (int)((warps + 7) / 8);
+  if (bf16) merge_ranks_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<__nv_bfloat16*>(O));
+  else merge_ranks_kernel<float><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<float*>(O));
+  return cudaGetLastError();
+}
 int simt_key_tile() { return kBK; }
 
 cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s) {

@@ -275,7 +275,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       const float c = p.scale_log2;
       const int G = p.G;
       const int tok = w.q_tok0 + r / G;
-      const int last_key = min(sg.m - 1, p.fault == 2 ? tok - 1 : tok);   // own keys 0..tok (R-2)
+      const int last_key = min(sg.tail_m - 1, p.fault == 2 ? tok - 1 : tok);   // own keys 0..tok (R-2)
       const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
       float m_run = -CUDART_INF_F;
       float l_run = 0.f;

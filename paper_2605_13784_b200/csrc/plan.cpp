@@ -28,7 +28,7 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
     const int64_t pool_tiles = ceil_div(sg.n_slots, c.key_tile);
     for (int tok0 = 0; tok0 < sg.m; tok0 += c.q_tile_tokens) {
       const int ntok = std::min(c.q_tile_tokens, sg.m - tok0);
-      const int64_t tail_tiles = ceil_div(tok0 + ntok, c.key_tile);
+      const int64_t tail_tiles = ceil_div(std::min(tok0 + ntok, sg.tail_m), c.key_tile);
       for (int h = 0; h < c.Hkv; ++h) {
         items.push_back({s, h, tok0, ntok, pool_tiles + tail_tiles, pool_tiles});
         total_tiles += pool_tiles + tail_tiles;
@@ -83,7 +83,7 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
     const Item& it = items[idx];
     const int64_t n = n_splits_of(it);
     const int unit0 = (int)out->units.size();
-    const int group = n > 1 ? (int)out->groups.size() : -1;
+    const int group = (n > 1 || c.force_groups) ? (int)out->groups.size() : -1;
     for (int64_t s = 0; s < n; ++s) {
       WorkUnit u;
       u.seg = it.seg;

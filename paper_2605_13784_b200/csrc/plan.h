@@ -17,6 +17,7 @@ struct PlanConfig {
   int min_tiles_per_unit = 1;
   double unit_overhead_tiles = 1.0;
   int fault = 0;
+  bool force_groups = false;  // every item writes partials (sharded query)
 };
 
 struct Plan {

@@ -18,7 +18,8 @@ namespace ssa {
 // keys, causally (Eq. query-attention; reading R-2).
 struct SegDesc {
   int64_t row0;          // first token row of the segment in the packed inputs
-  int32_t m;             // tokens in the segment (length of the "tail" key source)
+  int32_t m;             // tokens (query rows) in the segment
+  int32_t tail_m;        // own keys visible to the rows (m, or 0 on a non-tail rank of a sharded query)
   int32_t n_slots;       // slot extent of the visible cached keys (0: none)
   int32_t hole_lo;       // slots [hole_lo, hole_hi) hold no token (R0 page pad, R-9)
   int32_t hole_hi;
@@ -126,7 +127,8 @@ struct CombineParams {
   const float* part_o;
   const float* part_lse;
   void* O;
-  float* lse_out;        // optional [layers][groups][rows_tile]
+  float* lse_out;        // optional lse (log2 units) in O layout [rows][Hq]
+  float* o_f32;          // optional: write fp32 O here (O layout) instead of O
   const SegDesc* segs;
   const Group* groups;
   int32_t n_groups;
@@ -143,6 +145,9 @@ cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaS
 cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits);
 cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
 cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
+// Merge `world` rank partials (packed chunks [O fp32 rows*Hq*D | lse rows*Hq]) into O.
+cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
+                               cudaStream_t s);
 int simt_rows_tile(int G, int D);     // rows per SIMT unit
 int simt_key_tile();                  // keys per SIMT tile
 

@@ -307,7 +307,7 @@ ssa_status ssa_store::unstage_output(IoSet* io, cudaStream_t st) {
 // over input layers [0, n_layers) mapped to pool layers layer0 + y.
 ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t rows_per_layer,
                           int32_t layer0, int32_t n_layers, int32_t in_layer_stride, bool compute_o,
-                          bool query_plane, cudaStream_t st) {
+                          bool query_plane, cudaStream_t st, const RunOpts& opts) {
   const int G = cfg.num_q_heads / cfg.num_kv_heads;
   const int D = cfg.head_dim;
   // ---- plan attention
@@ -325,6 +325,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     pc.min_tiles_per_unit = use_tc ? 2 : 2;
     pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
     pc.fault = (int)opt_fault;
+    pc.force_groups = opts.force_groups;
     plan_units(segs, pc, &plan);
   }
   std::vector<TcPair> pairs;
@@ -441,7 +442,8 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       cp.part_o = part_o;
       cp.part_lse = part_lse;
       cp.O = io.o.dev;
-      cp.lse_out = nullptr;
+      cp.lse_out = opts.lse_out;
+      cp.o_f32 = opts.o_f32;
       cp.segs = d_segs;
       cp.groups = d_groups;
       cp.n_groups = (int32_t)plan.groups.size();
@@ -648,6 +650,7 @@ static ssa_status do_append(ssa_store* st, Session& s, int32_t n_new, const void
   SegDesc sg{};
   sg.row0 = 0;
   sg.m = n_new;
+  sg.tail_m = sg.m;
   st->fill_cached(s, &sg);
   sg.append_slot0 = (int32_t)st->slot_of(s, s.n_tokens);
   std::vector<SegDesc> segs{sg};
@@ -763,6 +766,7 @@ ssa_status ssa_append_layer(ssa_store_t st, ssa_session_t id, int32_t ticket, in
   if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
   SegDesc sg{};
   sg.m = n_new;
+  sg.tail_m = sg.m;
   st->fill_cached(*s, &sg);
   sg.append_slot0 = (int32_t)st->slot_of(*s, s->n_tokens);
   std::vector<SegDesc> segs{sg};
@@ -874,6 +878,7 @@ ssa_status ssa_flash_query_batch(ssa_store_t st, ssa_session_t id, int32_t layer
     SegDesc sg{};
     sg.row0 = row;
     sg.m = q_lens[i];
+    sg.tail_m = sg.m;
     st->fill_cached(*s, &sg);
     sg.append_slot0 = -1;
     segs.push_back(sg);
@@ -960,6 +965,7 @@ ssa_status ssa_batch_run(ssa_store_t st, int32_t layer, int32_t n_items, const s
     SegDesc sg{};
     sg.row0 = it.row_offset;
     sg.m = it.n_tokens;
+    sg.tail_m = sg.m;
     sg.append_slot0 = -1;
     if (it.kind == SSA_WORK_STATELESS) {
       sg.n_slots = 0;
@@ -1115,6 +1121,7 @@ int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_
   for (int i = 0; i < n_segs; ++i) {
     segs[i] = SegDesc{};
     segs[i].m = seg_m[i];
+    segs[i].tail_m = seg_m[i];
     segs[i].n_slots = seg_slots[i];
   }
   PlanConfig pc;

@@ -47,6 +47,12 @@ struct IoSet {
   IoBuf q, k, v, o;
 };
 
+struct RunOpts {
+  bool force_groups = false;   // all outputs as partials through the combine
+  float* o_f32 = nullptr;      // combine writes fp32 O here (O layout)
+  float* lse_out = nullptr;    // combine writes lse (log2) here, [rows][Hq]
+};
+
 // tcgen05 path (kernels_tc.cu)
 int tc_key_tile();
 int tc_rows_tile();
@@ -107,9 +113,12 @@ struct ssa_store {
   void fill_cached(const ssa::Session& s, ssa::SegDesc* sg) const;
   ssa_status ensure_scratch(size_t part_o_floats, size_t part_lse_floats, cudaStream_t st);
   ssa_status stage_inputs(ssa::IoSet* io, cudaStream_t st);
+  ssa_status query_segments(ssa::Session& s, int32_t layer, int32_t k, const int32_t* q_lens, bool include_tail,
+                            std::vector<ssa::SegDesc>* segs, int64_t* total);
   ssa_status unstage_output(ssa::IoSet* io, cudaStream_t st);
   ssa_status run(std::vector<ssa::SegDesc>& segs, const ssa::IoSet& io, int64_t rows_per_layer, int32_t layer0,
-                 int32_t n_layers, int32_t in_layer_stride, bool compute_o, bool query_plane, cudaStream_t st);
+                 int32_t n_layers, int32_t in_layer_stride, bool compute_o, bool query_plane, cudaStream_t st,
+                 const ssa::RunOpts& opts = ssa::RunOpts());
   bool tc_eligible(const std::vector<ssa::SegDesc>& segs) const;
   void destroy_comm();
 };

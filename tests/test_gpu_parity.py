@@ -391,3 +391,49 @@ def test_flash_query_batch_64x32(cuda):
         want = ref.flash_query_batch(rsid, [(qs[i][0][0], qs[i][1][0], qs[i][2][0])], layer)[0]
         ok, e = within(got[i * m:(i + 1) * m], want, "bf16")
         assert ok, (i, e)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("nq", [1, 32])
+def test_sharded_partials_merge(cuda, world, nq):
+    """A9 on one GPU: `world` stores hold contiguous shards (R-12); rank partials + merge == unsharded."""
+    import torch
+    from paper_2605_13784_b200.sharding import shard_range
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    n = 3001
+    spec = streams.StreamSpec("market", seed=15)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, nq)
+    rows = L * nq
+    chunk = rows * hq * (d + 1)
+    parts = torch.empty((world, chunk), dtype=torch.float32, device=cuda)
+    stores = []
+    for r in range(world):
+        lo, hi = shard_range(n, r, world)
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+        sid = st.session_create(None, to_dev(K[:, lo:hi], cuda), to_dev(V[:, lo:hi], cuda))
+        st.sharded_partial(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), parts[r],
+                           include_tail=(r == world - 1))
+        stores.append(st)
+    O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    stores[0].merge_rank_partials(world, rows, parts, O)
+    ok, e = within(from_dev(O), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, e
+
+
+def test_sharded_query_nccl_world1(cuda):
+    """The NCCL path end to end (world = 1 on a single GPU): partial -> ncclAllGather -> merge."""
+    import torch
+    ssa = _ssa()
+    spec = streams.StreamSpec("peaked", seed=16)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=900, appends=(100,))
+    st.comm_init(0, 1, ssa.Store.comm_unique_id())
+    Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
+    O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.sharded_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), O)
+    ok, e = within(from_dev(O), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, e
+    st.comm_destroy()
