@@ -161,16 +161,20 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- our arm
 def build_session(st, torch, dev, spec, n, chunk=4096):
+    return build_session_n(st, torch, dev, spec, n, chunk=chunk)
+
+
+def build_session_n(st, torch, dev, spec, n, chunk=4096, session=0):
     """Bulk-import an n-token market-feed session (K/V generated on the GPU)."""
     import streams
     sid = None
     tok = 0
     while tok < n:
         m = min(chunk, n - tok)
-        K = torch.stack([streams.gen_tensor_torch(spec, 0, 0, l, streams.TENSOR_K, tok, m, CFG["hkv"], CFG["d"],
-                                                  device=dev) for l in range(CFG["L"])])
-        V = torch.stack([streams.gen_tensor_torch(spec, 0, 0, l, streams.TENSOR_V, tok, m, CFG["hkv"], CFG["d"],
-                                                  device=dev) for l in range(CFG["L"])])
+        K = torch.stack([streams.gen_tensor_torch(spec, session, 0, l, streams.TENSOR_K, tok, m, CFG["hkv"],
+                                                  CFG["d"], device=dev) for l in range(CFG["L"])])
+        V = torch.stack([streams.gen_tensor_torch(spec, session, 0, l, streams.TENSOR_V, tok, m, CFG["hkv"],
+                                                  CFG["d"], device=dev) for l in range(CFG["L"])])
         if sid is None:
             sid = st.session_create(None, K, V, n_prefix=m)   # R0 = first chunk (S, P:186)
         else:
@@ -179,15 +183,129 @@ def build_session(st, torch, dev, spec, n, chunk=4096):
     return sid
 
 
-def gen_new(torch, dev, spec, domain, tok0, m):
+def gen_new(torch, dev, spec, domain, tok0, m, session=0):
     import streams
     out = []
     for t in (streams.TENSOR_Q, streams.TENSOR_K, streams.TENSOR_V):
         h = CFG["hq"] if t == streams.TENSOR_Q else CFG["hkv"]
-        out.append(torch.stack([streams.gen_tensor_torch(spec, 0, domain, l, t, tok0, m, h, CFG["d"], hkv=CFG["hkv"],
-                                                         device=dev) for l in range(CFG["L"])]).contiguous())
+        out.append(torch.stack([streams.gen_tensor_torch(spec, session, domain, l, t, tok0, m, h, CFG["d"],
+                                                         hkv=CFG["hkv"], device=dev)
+                                for l in range(CFG["L"])]).contiguous())
     return out
 
+
+
+# ----------------------------------------------------------------------------- extra legs (configs 3-5)
+def _timed(torch, stream, fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def leg_flash(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_ctx):
+    """BJ.configs[3]: 64 registered 32-token questions in ONE batched launch (all 32 layers) on the
+    32k session, vs 64 separate query calls.  Tensor-core bound."""
+    import streams
+    k, m = 64, 32
+    Qs, Ks, Vs = [], [], []
+    for i in range(k):
+        q, kk, v = gen_new(torch, dev, spec, streams.FLASH_DOMAIN + i, 0, m)
+        Qs.append(q); Ks.append(kk); Vs.append(v)
+    Q, K, V = (torch.cat(x, dim=1).contiguous() for x in (Qs, Ks, Vs))
+    O = torch.empty_like(Q)
+    ms = _timed(torch, stream, lambda: st.flash_query_batch(sid, [m] * k, Q, K, V, O, stream=stream), steps, warmup)
+    flops = k * append_flops_per_layer(n_ctx, m, CFG["hq"], CFG["d"]) * CFG["L"]
+    Os = [torch.empty_like(Qs[i]) for i in range(k)]
+    sep = _timed(torch, stream, lambda: [st.session_query(sid, Qs[i], Ks[i], Vs[i], Os[i], stream=stream)
+                                         for i in range(k)], 1, 1)
+    return {"workload": "BJ.configs[3]: 64 x 32-token Flash Queries, one launch over 32 layers, n=%d" % n_ctx,
+            "ms_per_batch_32_layers": ms, "tflops": flops / (ms * 1e-3) / 1e12,
+            "tc_frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+            "ms_64_separate_queries": sep, "speedup_vs_separate": sep / ms,
+            "paper_context": "paper T_f ~30-35 ms per Flash Query on L40S, full 8B forward (P:484)"}
+
+
+def leg_multitenant(torch, dev, stream, peaks, steps, warmup):
+    """BJ.configs[2]: 48 sessions of 4k-16k context; one launch (all 32 layers) packs 24 appends of 256,
+    24 queries of 32 and 4 stateless 1024-token prompts (snapshot semantics, R-7)."""
+    import streams
+    import paper_2605_13784_b200 as ssa
+    L, hq, hkv, d, P = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"], CFG["P"]
+    ns = [4096 + 256 * s for s in range(48)]
+    num_pages = sum(-(-(n + 256) // P) for n in ns) + 64
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=num_pages, max_sessions=64, dtype="bf16")
+    spec = streams.StreamSpec("market", seed=3)
+    sids = []
+    for s, n in enumerate(ns):
+        sids.append(build_session_n(st, torch, dev, spec, n, session=s))
+    items, Qs, Ks, Vs, row = [], [], [], [], 0
+    bytes_l, flops_l = 0, 0
+    for s, n in enumerate(ns):
+        if s % 2 == 0:
+            q, k, v = gen_new(torch, dev, spec, 0, n, 256, session=s)
+            items.append((ssa.WORK_APPEND, sids[s], 256, row))
+            m = 256
+        else:
+            q, k, v = gen_new(torch, dev, spec, 1, 0, 32, session=s)
+            items.append((ssa.WORK_QUERY, sids[s], 32, row))
+            m = 32
+        Qs.append(q); Ks.append(k); Vs.append(v)
+        row += m
+        bytes_l += query_bytes_per_layer(n, m, hq, hkv, d)
+        flops_l += append_flops_per_layer(n, m, hq, d)
+    for j in range(4):
+        q, k, v = gen_new(torch, dev, spec, 100 + j, 0, 1024, session=60 + j)
+        items.append((ssa.WORK_STATELESS, -1, 1024, row))
+        Qs.append(q); Ks.append(k); Vs.append(v)
+        row += 1024
+        bytes_l += query_bytes_per_layer(0, 1024, hq, hkv, d)
+        flops_l += append_flops_per_layer(0, 1024, hq, d)
+    Q, K, V = (torch.cat(x, dim=1).contiguous() for x in (Qs, Ks, Vs))
+    del Qs, Ks, Vs
+    O = torch.empty_like(Q)
+
+    def step():
+        st.batch_run(items, Q, K, V, O, stream=stream)
+        for s in range(0, 48, 2):
+            st.session_truncate(sids[s], ns[s])
+
+    ms = _timed(torch, stream, step, steps, warmup)
+    bound_ms = max(bytes_l * L / (peaks["hbm_gbs"] * 1e9), flops_l * L / (peaks["bf16_tflops"] * 1e12)) * 1e3
+    st.close()
+    return {"workload": "BJ.configs[2]: 48 sessions n=4096+256s, one launch/32 layers: 24 appends x256, "
+                        "24 queries x32, 4 stateless x1024",
+            "ms_per_launch_32_layers": ms, "us_per_layer": ms * 1e3 / L,
+            "roofline_bound_ms": bound_ms, "frac_of_mixed_roofline": bound_ms / ms,
+            "bytes_per_layer": bytes_l, "flops_per_layer": flops_l,
+            "tokens_per_s": (24 * 256 + 24 * 32 + 4 * 1024) / (ms * 1e-3)}
+
+
+def leg_split128k(torch, dev, stream, peaks, steps, warmup):
+    """BJ.configs[4] at N=1: one 131,072-token session, 1-token and 32-token queries over 32 layers."""
+    import streams
+    import paper_2605_13784_b200 as ssa
+    L, hq, hkv, d, P = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"], CFG["P"]
+    n = 131072
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=n // P + 8, max_sessions=2, dtype="bf16")
+    spec = streams.StreamSpec("market", seed=5)
+    sid = build_session_n(st, torch, dev, spec, n)
+    out = {"workload": "BJ.configs[4] at N=1: n=131,072, queries over 32 layers"}
+    for qn in (1, 32):
+        q, k, v = gen_new(torch, dev, spec, 1, 0, qn)
+        o = torch.empty_like(q)
+        ms = _timed(torch, stream, lambda: st.session_query(sid, q, k, v, o, stream=stream), steps, warmup)
+        nb = query_bytes_per_layer(n, qn, hq, hkv, d) * L
+        out[f"q{qn}"] = {"ms_32_layers": ms, "us_per_layer": ms * 1e3 / L, "gbs": nb / (ms * 1e-3) / 1e9,
+                         "hbm_frac": nb / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+    st.close()
+    return out
 
 def run_ours(args):
     import torch
@@ -287,6 +405,24 @@ def run_ours(args):
     h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV))
     d2h = hO.numel() * hO.element_size()
 
+    legs = {}
+    if rank == 0 and args.legs:
+        peaks_l, _ = load_peaks()
+        want = args.legs.split(",")
+        if "flash" in want:
+            st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # the 256-token update, n -> 32,768
+            legs["flash_queries"] = leg_flash(st, sid, torch, dev, spec, stream, peaks_l, 3, 1, n_ctx)
+            st.session_truncate(sid, n0)
+        st.close()
+        del Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq
+        torch.cuda.empty_cache()
+        if "tenant" in want:
+            legs["multi_tenant"] = leg_multitenant(torch, dev, stream, peaks_l, 3, 1)
+            torch.cuda.empty_cache()
+        if "split" in want:
+            legs["split_kv_128k"] = leg_split128k(torch, dev, stream, peaks_l, 3, 1)
+            torch.cuda.empty_cache()
+
     line = None
     if rank == 0:
         clocks = clk.summary()
@@ -334,6 +470,7 @@ def run_ours(args):
             "paper_context": "paper: ~43 ms end-to-end standard query (full Llama-3.1-8B forward) on 1x L40S "
                              "(P:645, Table 1 P:672); not comparable to this attention-only path",
         }
+        line.update(legs)
         if not args.no_cpu_baseline:
             import oracle
             oracle.build()
@@ -342,7 +479,8 @@ def run_ours(args):
                                     "sample": "fp64 C oracle, single thread: one layer, one KV head (4 q heads), "
                                               f"32-token query over 32,768 cached tokens ({dt:.1f} s)"}
         print(json.dumps(line), flush=True)
-    st.close()
+    if not (rank == 0 and args.legs):
+        st.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -354,6 +492,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--legs", default="flash,tenant,split",
+                    help="extra single-GPU legs (configs 3-5) reported in the same JSON line; '' to skip")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

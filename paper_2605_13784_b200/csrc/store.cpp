@@ -475,15 +475,14 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
 }
 
 bool ssa_store::tc_eligible(const std::vector<SegDesc>& segs) const {
+  (void)segs;
   if (opt_backend == 1 || !sm100) return false;
   const int G = cfg.num_q_heads / cfg.num_kv_heads;
-  if (!tc_supported_shape(cfg.head_dim, G, cfg.dtype == SSA_BF16)) return false;
-  if (opt_backend == 2) return true;
-  // auto: tensor cores once a q tile packs >= 16 rows per KV head (SURVEY §0
-  // finding 1); 1-token GQA decode (4 rows) stays on the SIMT split-KV kernel.
-  int max_m = 0;
-  for (auto& s : segs) max_m = std::max(max_m, s.m);
-  return (int64_t)std::min(max_m, tc_rows_tile() / G) * G >= 16;
+  // bf16 with head_dim 128 always runs on tcgen05: even a 1-token GQA query
+  // (4 of 128 rows used) is HBM-bound there — per 128-key tile the two MMAs
+  // (~1k clk) and the softmax fit under the ~2.9k clk it takes an SM to stream
+  // the 64 KB of K/V at its share of HBM bandwidth.
+  return tc_supported_shape(cfg.head_dim, G, cfg.dtype == SSA_BF16);
 }
 
 // ============================================================================

@@ -143,7 +143,7 @@ def test_llama_append_and_query_bf16(cuda, stream_name, backend):
 @pytest.mark.parametrize("backend", [0, 2])
 @pytest.mark.parametrize("nq", [1, 4, 32, 33, 100])
 def test_query_lengths_bf16(cuda, nq, backend):
-    """|q| = 1 (SIMT decode path under auto) .. 100 (several q tiles, ragged tail)."""
+    """|q| = 1 .. 100 (several q tiles, ragged tail); auto (0) and forced tcgen05 (2)."""
     import torch
     spec = streams.StreamSpec("peaked", seed=3)
     st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=700, appends=(300,), backend=backend)
