@@ -269,8 +269,11 @@ typedef enum {
     SSA_OPT_FAULT_INJECT = 3,   /* negative controls: 0 none, 1 drop last key tile,
                                    2 causal off-by-one (row t misses its own key) */
     SSA_OPT_TC_Q_TILES = 4,     /* tcgen05 Q tiles per CTA (1 or 2; 0 = auto) */
-    SSA_OPT_TIMING = 5          /* 1: record CUDA events around every kernel launch
+    SSA_OPT_TIMING = 5,         /* 1: record CUDA events around every kernel launch
                                    (on the call's stream) for ssa_store_timing */
+    SSA_OPT_FUSED_MERGE = 6     /* 1: the last tcgen05 CTA of a split group merges the
+                                   group in-kernel (no combine launch); 0 (default):
+                                   separate combine kernel */
 } ssa_option;
 ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
 

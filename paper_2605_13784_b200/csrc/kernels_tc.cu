@@ -43,6 +43,14 @@ constexpr int kSlotBytes = 2 * kChunkBytes;     // one 128 x 128 bf16 tile = 32 
 constexpr int kNumSlots = 7;                    // 224 KB of tiles
 constexpr int kMaxStages = 3;
 constexpr float kRescaleLog2 = 8.0f;
+// setmaxnreg budget: the CTA's pool is fixed at launch (168 regs x 384 threads
+// from __launch_bounds__(384, 1)); setmaxnreg.inc blocks until registers are
+// free, so the rebalanced total must fit the pool or the kernel deadlocks.
+constexpr int kLaunchRegs = 168;
+constexpr int kRegsWG0 = 56;       // TMA producer / MMA issuer / allocator warpgroup
+constexpr int kRegsSoftmax = 224;  // two softmax warpgroups
+static_assert(128 * kRegsWG0 + 256 * kRegsSoftmax <= kLaunchRegs * kThreads, "setmaxnreg over the CTA pool");
+static_assert(kRegsWG0 % 8 == 0 && kRegsSoftmax % 8 == 0, "setmaxnreg needs multiples of 8");
 
 struct Bars {
   uint64_t q_full;
@@ -53,6 +61,7 @@ struct Bars {
   uint64_t p_full[2];
   uint64_t o_final[2];
   uint32_t tmem_base;
+  uint32_t merge_flag[2];
 };
 
 struct TcMaps {
@@ -143,7 +152,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   const uint32_t tmem = bar.tmem_base;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsWG0));
     if (warp == 0) {
       // ----------------------------------------------------------- TMA producer
       if (elect_one()) {
@@ -208,59 +217,60 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       if (elect_one()) {
         constexpr uint32_t idesc_s = idesc_bf16(kM, kBN, 0, 0);   // Q, K both K-major
         constexpr uint32_t idesc_o = idesc_bf16(kM, kD, 0, 1);    // P K-major (TMEM), V MN-major
-        const int nt[2] = {nt0, nt1};
+        // descriptor bases; per-step offsets are compile-time adds on the 16-byte address field
+        const uint64_t qd0 = sdesc_sw128(smem_u32(q_buf[0]), 16, 1024);
+        const uint64_t qd1 = sdesc_sw128(smem_u32(q_buf[1]), 16, 1024);
+        const uint64_t kd0 = sdesc_sw128(smem_u32(stage_base), 16, 1024);
+        const uint64_t vd0 = sdesc_sw128(smem_u32(stage_base + kSlotBytes), kChunkBytes, 1024);
+        constexpr uint64_t kStageStep = (2 * kSlotBytes) >> 4;
         mbar_wait(&bar.q_full, 0);
         tc_fence_after();
-        auto issue_s = [&](int k, int j) {
-          const int e = event_of(k, j, nsh, nt0, nt1);
-          const int s = e % NS;
-          mbar_wait(&bar.k_full[s], (e / NS) & 1);
-          tc_fence_after();
-          const uint32_t q_addr = smem_u32(q_buf[k]);
-          const uint32_t k_addr = smem_u32(stage_base + (2 * s) * kSlotBytes);
-          const uint32_t d = tmem + 256u * k;
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
-            mma_bf16_ss(d, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024), idesc_s,
-                        kk > 0 ? 1u : 0u);
-          }
-          mma_commit(&bar.s_full[k]);
-        };
-        auto issue_pv = [&](int k, int j) {
-          const int e = event_of(k, j, nsh, nt0, nt1);
-          const int s = e % NS;
-          mbar_wait(&bar.p_full[k], j & 1);
-          mbar_wait(&bar.v_full[s], (e / NS) & 1);
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(stage_base + (2 * s + 1) * kSlotBytes);
-          const uint32_t o = tmem + 256u * k + 128u;
-          const uint32_t pa = tmem + 256u * k;
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            // B = V[16 keys][128 d], MN-major: 16 keys = 2048 B down each 64-column chunk
-            mma_bf16_ts(o, pa + 8 * kk, sdesc_sw128(v_addr + kk * 2048, kChunkBytes, 1024), idesc_o,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          // a shared stage is free after slot 1's PV, a private one after its own
-          if (j >= nsh || k == 1) mma_commit(&bar.kv_empty[s]);
-          if (j == nt[k] - 1) mma_commit(&bar.o_final[k]);
-        };
-        for (int k = 0; k < 2; ++k)
-          if (nt[k] > 0) issue_s(k, 0);
         const int jmax = max(nt0, nt1);
-        for (int j = 0; j < jmax; ++j) {
+        // prologue: S(k, 0); then per j: PV(k, j) and S(k, j+1) for k = 0, 1
+        for (int it = -1; it < jmax; ++it) {
+#pragma unroll 1
           for (int k = 0; k < 2; ++k) {
-            if (j < nt[k]) {
-              issue_pv(k, j);
-              if (j + 1 < nt[k]) issue_s(k, j + 1);
+            const int ntk = k ? nt1 : nt0;
+            if (it >= 0 && it < ntk) {
+              // ---- PV(k, it): O_k += P_k (TMEM) * V
+              const int e = event_of(k, it, nsh, nt0, nt1);
+              const int s = e % NS;
+              mbar_wait(&bar.p_full[k], it & 1);
+              mbar_wait(&bar.v_full[s], (e / NS) & 1);
+              tc_fence_after();
+              const uint64_t vd = vd0 + (uint64_t)s * kStageStep;
+              const uint32_t o = tmem + 256u * k + 128u;
+              const uint32_t pa = tmem + 256u * k;
+#pragma unroll
+              for (int kk = 0; kk < kBN / 16; ++kk)   // 16 keys = 2048 B down each 64-column V chunk
+                mma_bf16_ts(o, pa + 8 * kk, vd + (uint64_t)((kk * 2048) >> 4), idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+              // a shared stage is free after slot 1's PV, a private one after its own
+              if (it >= nsh || k == 1) mma_commit(&bar.kv_empty[s]);
+              if (it == ntk - 1) mma_commit(&bar.o_final[k]);
+            }
+            const int jn = it + 1;
+            if (jn < ntk) {
+              // ---- S(k, jn) = Q_k K^T
+              const int e = event_of(k, jn, nsh, nt0, nt1);
+              const int s = e % NS;
+              mbar_wait(&bar.k_full[s], (e / NS) & 1);
+              tc_fence_after();
+              const uint64_t qd = k ? qd1 : qd0;
+              const uint64_t kd = kd0 + (uint64_t)s * kStageStep;
+              const uint32_t d = tmem + 256u * k;
+#pragma unroll
+              for (int kk = 0; kk < kD / 16; ++kk) {
+                const uint64_t off = (uint64_t)(((kk >> 2) * kChunkBytes + (kk & 3) * 32) >> 4);
+                mma_bf16_ss(d, qd + off, kd + off, idesc_s, kk > 0 ? 1u : 0u);
+              }
+              mma_commit(&bar.s_full[k]);
             }
           }
         }
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
     // ------------------------------------------------------------- softmax + epilogue
     const int k = (warp - 4) >> 2;                 // slot
     const bool active = (k == 0) || pr.ub >= 0;
@@ -412,6 +422,71 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       }
       if (w.group >= 0 && r < rows)
         p.part_lse[pslot * kM + r] = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
+      // ------------------------------------------------- fused split-KV merge (R-11)
+      if (w.group >= 0 && p.group_counters) {
+        const Group gr = p.groups[w.group];
+        int* cnt = p.group_counters + (int64_t)ly * p.n_groups + w.group;
+        __threadfence();   // release this thread's partial row
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
+        if (r == 0) {
+          __threadfence();
+          const int old = atomicAdd(cnt, 1);
+          bar.merge_flag[k] = (old == gr.n_splits - 1) ? 1u : 0u;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
+        if (bar.merge_flag[k]) {
+          __threadfence();
+          if (r < rows) {
+            const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
+            float L = -CUDART_INF_F;
+            for (int s = 0; s < gr.n_splits; ++s) L = fmaxf(L, __ldcg(p.part_lse + (s0 + s) * kM + r));
+            float wsum = 0.f;
+            for (int s = 0; s < gr.n_splits; ++s) {
+              const float ls = __ldcg(p.part_lse + (s0 + s) * kM + r);
+              if (ls != -CUDART_INF_F) wsum += exp2f(ls - L);
+            }
+            const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+#pragma unroll 1
+            for (int q4 = 0; q4 < kD / 32; ++q4) {       // 32 columns at a time
+              float4 acc[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int s = 0; s < gr.n_splits; ++s) {
+                const float ls = __ldcg(p.part_lse + (s0 + s) * kM + r);
+                if (ls == -CUDART_INF_F) continue;
+                const float wt = exp2f(ls - L) * inv;
+                const float4* src = reinterpret_cast<const float4*>(p.part_o + ((s0 + s) * kM + r) * kD + q4 * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 v = __ldcg(src + i);
+                  acc[i].x = fmaf(wt, v.x, acc[i].x);
+                  acc[i].y = fmaf(wt, v.y, acc[i].y);
+                  acc[i].z = fmaf(wt, v.z, acc[i].z);
+                  acc[i].w = fmaf(wt, v.w, acc[i].w);
+                }
+              }
+              if (p.o_f32) {
+                float4* out = reinterpret_cast<float4*>(p.o_f32 + (orow * p.Hq + h) * kD + q4 * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) out[i] = acc[i];
+              } else {
+                uint4* out = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  uint4 v;
+                  v.x = pack_bf16(acc[2 * i].x, acc[2 * i].y);
+                  v.y = pack_bf16(acc[2 * i].z, acc[2 * i].w);
+                  v.z = pack_bf16(acc[2 * i + 1].x, acc[2 * i + 1].y);
+                  v.w = pack_bf16(acc[2 * i + 1].z, acc[2 * i + 1].w);
+                  out[i] = v;
+                }
+              }
+            }
+            if (p.lse_out) p.lse_out[orow * p.Hq + h] = wsum > 0.f ? L + __log2f(wsum) : -CUDART_INF_F;
+          }
+          if (r == 0) *cnt = 0;   // ready for the next launch
+        }
+      }
     }
   }
   tc_fence_before();

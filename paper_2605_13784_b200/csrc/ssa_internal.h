@@ -89,6 +89,11 @@ struct AttnParams {
   int32_t fault;         // SSA_OPT_FAULT_INJECT
   const TcPair* pairs;   // tcgen05 CTAs (per layer)
   int32_t n_pairs;
+  // fused split-KV merge (tcgen05 path): the last unit of a group to finish
+  // merges the group's partials; counters are zero between launches.
+  int32_t* group_counters;   // [layers][n_groups], or null: separate combine kernel
+  float* o_f32;              // optional fp32 O output (O layout) instead of O
+  float* lse_out;            // optional lse output (log2, [rows][Hq])
 };
 
 // Append scatter (KA): copy new K/V rows into pages, bit-exact.

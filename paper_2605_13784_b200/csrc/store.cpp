@@ -428,6 +428,21 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.fault = (int32_t)opt_fault;
     ap.pairs = d_pairs;
     ap.n_pairs = (int32_t)pairs.size();
+    const bool fused = use_tc && !plan.groups.empty() && opt_fused_merge;
+    if (fused) {
+      const size_t need = (size_t)n_layers * plan.groups.size();
+      if (need > counters_cap) {
+        SSA_CUDA(this, cudaDeviceSynchronize());
+        if (counters) cudaFree(counters);
+        counters = nullptr;
+        counters_cap = std::max(need, counters_cap * 2);
+        SSA_CUDA(this, cudaMalloc(&counters, counters_cap * sizeof(int32_t)));
+        SSA_CUDA(this, cudaMemset(counters, 0, counters_cap * sizeof(int32_t)));
+      }
+      ap.group_counters = counters;
+      ap.o_f32 = opts.o_f32;
+      ap.lse_out = opts.lse_out;
+    }
     cudaEvent_t t0 = tick(st);
     if (use_tc) {
       SSA_CUDA(this, launch_attn_tc(ap, n_layers, (int)opt_tc_qtiles, st));
@@ -437,7 +452,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     if (t0) timed_push(query_plane ? 1 : 0, t0, tick(st));
     stats.kernel_launches++;
     if (use_tc) stats.tc_launches++;
-    if (!plan.groups.empty()) {
+    if (!plan.groups.empty() && !fused) {
       CombineParams cp{};
       cp.part_o = part_o;
       cp.part_lse = part_lse;
@@ -577,6 +592,7 @@ ssa_store::~ssa_store() {
   if (part_o) cudaFree(part_o);
   if (part_lse) cudaFree(part_lse);
   if (stage) cudaFree(stage);
+  if (counters) cudaFree(counters);
   destroy_comm();
 }
 
@@ -609,6 +625,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
     case SSA_OPT_FAULT_INJECT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_fault = value; break;
     case SSA_OPT_TC_Q_TILES: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_tc_qtiles = value; break;
     case SSA_OPT_TIMING: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_timing = value; break;
+    case SSA_OPT_FUSED_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_fused_merge = value; break;
     default: return SSA_ERR_INVALID_ARG;
   }
   return SSA_OK;

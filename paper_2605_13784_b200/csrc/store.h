@@ -83,7 +83,9 @@ struct ssa_store {
   size_t part_lse_cap = 0;
   void* stage = nullptr;
   size_t stage_cap = 0;
-  int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0;
+  int32_t* counters = nullptr;   // fused-merge group counters (zero between launches)
+  size_t counters_cap = 0;
+  int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0, opt_fused_merge = 0;
   ssa_stats stats{};
   int32_t ticket_seq = 0;
   int64_t last_plan_units = 0, last_plan_groups = 0;

@@ -1,5 +1,5 @@
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 2>&1 | tail -25
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python -m pytest tests -m gpu -q -x --timeout 240 --timeout-method=thread 2>&1 | tail -25
+timeout 400 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 tail -c 3000 gpurun_out/bench.json; tail -5 gpurun_out/bench.err

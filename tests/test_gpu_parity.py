@@ -437,3 +437,19 @@ def test_sharded_query_nccl_world1(cuda):
     ok, e = within(from_dev(O), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
     assert ok, e
     st.comm_destroy()
+
+
+@pytest.mark.parametrize("nq", [1, 32, 100])
+def test_fused_merge_option(cuda, nq):
+    """SSA_OPT_FUSED_MERGE: the last CTA of each split group merges in-kernel; same parity."""
+    import torch
+    ssa = _ssa()
+    spec = streams.StreamSpec("peaked", seed=17)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=1800, appends=(200,))
+    st.set_option(ssa.OPT_FUSED_MERGE, 1)
+    Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, nq)
+    for rep in range(2):     # counters must be back at zero for the second launch
+        Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+        ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+        assert ok, (rep, e)
