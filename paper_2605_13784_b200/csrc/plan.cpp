@@ -7,6 +7,8 @@
 // launch fills the GPU (148 SMs on B200).  Units of one (segment, q tile, kv
 // head) form a Group merged by the combine kernel (log-sum-exp, reading R-11).
 #include <algorithm>
+#include <functional>
+#include <queue>
 #include <tuple>
 #include <cstdint>
 #include <vector>
@@ -36,36 +38,60 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
     }
   }
   if (items.empty()) return;
-  // Makespan model: waves * (tiles per unit + fixed per-unit overhead).  Pick
-  // the tiles-per-unit that minimises it (ties -> fewer splits).
-  const int64_t slots = std::max<int64_t>(1, (int64_t)c.num_sms * c.ctas_per_sm);
+  // Choose the tiles-per-unit cap by an LPT makespan estimate over the CTAs
+  // the units will form.  A CTA runs two units (two softmax slots) and costs
+  // about the sum of their tiles plus a fixed overhead per unit (launch, Q
+  // load, TMEM setup) and per split unit (partial write + merge).  With a
+  // moderate job count the greedy LPT assignment onto the SMs is simulated;
+  // with many jobs the bound sum/m + max is used (quantization is then small).
+  const int64_t m_slots = std::max<int64_t>(1, (int64_t)c.num_sms * std::max(1, c.ctas_per_sm / 2));
   int64_t max_tiles = 0;
   for (auto& it : items) max_tiles = std::max(max_tiles, it.tiles);
-  int64_t best_tpu = max_tiles;
-  double best_cost = 1e300;
   const int max_splits = c.max_splits > 0 ? c.max_splits : 1 << 20;
   std::vector<int64_t> cands;
-  for (int64_t t = std::max<int64_t>(1, c.min_tiles_per_unit); t <= max_tiles;
-       t = t < 32 ? t + 1 : std::max<int64_t>(t + 1, (int64_t)(t * 1.06))) cands.push_back(t);
-  if (cands.empty() || cands.back() != max_tiles) cands.push_back(std::max<int64_t>(1, max_tiles));
+  for (int64_t div = 1; div <= 64; div = div < 8 ? div + 1 : div * 3 / 2) {
+    const int64_t t = std::max<int64_t>(std::max<int64_t>(1, c.min_tiles_per_unit), (max_tiles + div - 1) / div);
+    if (cands.empty() || cands.back() != t) cands.push_back(t);
+  }
+  int64_t best_tpu = 0;
+  double best_cost = 1e300;
+  std::vector<double> unit_cost, jobs;
   for (int64_t tpu : cands) {
-    int64_t units = 0;
+    unit_cost.clear();
     bool ok = true;
     for (auto& it : items) {
       const int64_t n = ceil_div(it.tiles, tpu);
       if (n > max_splits) { ok = false; break; }
-      units += n;
+      for (int64_t s = 0; s < n; ++s) {
+        const int64_t t = it.tiles * (s + 1) / n - it.tiles * s / n;
+        unit_cost.push_back((double)t + c.unit_overhead_tiles + (n > 1 ? 1.0 : 0.0));
+      }
     }
     if (!ok) continue;
-    units *= c.n_layers;
-    const double waves = (double)ceil_div(units, slots);
-    const double per_unit = (double)std::min<int64_t>(tpu, max_tiles) + c.unit_overhead_tiles;
-    const double cost = waves * per_unit + 1e-3 * (double)units / (double)slots;
-    if (cost < best_cost - 1e-9) { best_cost = cost; best_tpu = tpu; }
-    if (units <= c.n_layers * (int64_t)items.size()) break;  // no more splitting possible
-  }
-  if (best_cost > 1e299) {  // max_splits binds: split each item into max_splits
-    best_tpu = 0;
+    std::sort(unit_cost.begin(), unit_cost.end(), std::greater<double>());
+    jobs.clear();
+    for (size_t i = 0; i < unit_cost.size(); i += 2)
+      jobs.push_back(unit_cost[i] + (i + 1 < unit_cost.size() ? unit_cost[i + 1] : 0.0));
+    const int64_t n_jobs = (int64_t)jobs.size() * c.n_layers;
+    double makespan;
+    if (n_jobs <= 24 * m_slots) {
+      std::priority_queue<double, std::vector<double>, std::greater<double>> load;
+      for (int64_t i = 0; i < m_slots; ++i) load.push(0.0);
+      for (double jc : jobs)
+        for (int l = 0; l < c.n_layers; ++l) {
+          const double x = load.top();
+          load.pop();
+          load.push(x + jc);
+        }
+      makespan = 0.0;
+      while (!load.empty()) { makespan = std::max(makespan, load.top()); load.pop(); }
+    } else {
+      double sum = 0.0;
+      for (double jc : jobs) sum += jc;
+      makespan = sum * c.n_layers / (double)m_slots + jobs.front();
+    }
+    const double cost = makespan * (1.0 + 1e-6 * (double)unit_cost.size());
+    if (cost < best_cost) { best_cost = cost; best_tpu = tpu; }
   }
   // Order groups by per-unit work, largest first (LPT over the CTA rasterizer).
   std::vector<int> order(items.size());

@@ -101,7 +101,16 @@ def test_planner_covers_every_key_tile_once(case):
 
 def test_planner_fills_the_gpu_for_the_query():
     import paper_2605_13784_b200 as ssa
-    units = ssa.debug_plan([32], [32768], 8, 32, 128, n_layers=1, num_sms=148)
-    assert 120 <= len(units) <= 148          # one wave of 148 SMs
-    units = ssa.debug_plan([32], [32768], 8, 32, 128, n_layers=1, num_sms=148, max_splits=4)
+    units = ssa.debug_plan([32], [32768], 8, 32, 128, n_layers=1, num_sms=148, ctas_per_sm=2)
+    assert 240 <= len(units) <= 296          # one wave of two-slot CTAs on 148 SMs
+    units = ssa.debug_plan([32], [32768], 8, 32, 128, n_layers=1, num_sms=148, ctas_per_sm=2, max_splits=4)
     assert len(units) == 32
+
+
+def test_planner_does_not_shred_heterogeneous_batches():
+    """Config 3 (48 sessions + stateless prompts, 32 layers): enough CTAs already, so no splits."""
+    import paper_2605_13784_b200 as ssa
+    ns = [4096 + 256 * s for s in range(48)]
+    seg_m = [256 if s % 2 == 0 else 32 for s in range(48)] + [1024] * 4
+    units = ssa.debug_plan(seg_m, ns + [0] * 4, 8, 32, 128, n_layers=32, num_sms=148, ctas_per_sm=2)
+    assert all(u[6] == -1 for u in units)
