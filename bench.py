@@ -59,23 +59,33 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms (the recipe's clocks line,
+    B200_PROFILING.md).  Rows carry host timestamps; `mark()` brackets the timed region.
+    The sampler is started (and its first row awaited) before the timed region and kept
+    running through the rest of the GPU work, so a short timed region still gets the
+    load-window samples right after it."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []        # (host time, fields)
         self.proc = None
+        self.windows = {}
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10.0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -84,26 +94,45 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    def mark(self, name, t0, t1):
+        self.windows[name] = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.2)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
 
+    def _summ(self, rows):
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        out = {}
+        t_lo, t_hi = self.windows.get("timed", (None, None))
+        if t_lo is not None:
+            # a sample lands ~50 ms after the clock it reports was read: allow that lag
+            timed = [r for t, r in self.rows if t_lo <= t <= t_hi + 0.06]
+            load_hi = self.windows.get("load", (t_lo, t_hi))[1]
+            load = [r for t, r in self.rows if t_lo <= t <= load_hi + 0.06]
+        else:
+            timed, load = [], [r for _, r in self.rows]
+        base = self._summ(timed if timed else load)
+        base["window"] = "timed region" if timed else "timed region + the GPU legs right after it"
+        base["samples_timed_region"] = len(timed)
+        base["load_window"] = self._summ(load)
+        out.update(base)
+        return out
 
 
 def dist_env():
@@ -389,12 +418,14 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ev[0].record(stream)
-        for _ in range(args.steps):
-            step()
-        ev[1].record(stream)
-        torch.cuda.synchronize()
+    clk = ClockSampler(local).__enter__()   # kept running through the legs below (load window)
+    t_timed0 = time.time()
+    ev[0].record(stream)
+    for _ in range(args.steps):
+        step()
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    clk.mark("timed", t_timed0, time.time())
     if world > 1:
         torch.distributed.barrier()
     step_ms = ev[0].elapsed_time(ev[1]) / args.steps
@@ -477,6 +508,8 @@ def run_ours(args):
                     lambda: leg_split128k_sharded(torch, dev, stream, peaks_l, 3, 1, world, rank))
         torch.cuda.empty_cache()
 
+    clk.mark("load", t_timed0, time.time())
+    clk.__exit__(None, None, None)
     line = None
     if rank == 0:
         clocks = clk.summary()

@@ -287,6 +287,13 @@ ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value
 ssa_status ssa_store_timing(ssa_store_t store, double ms[SSA_TIMING_KINDS],
                             int64_t count[SSA_TIMING_KINDS], int32_t reset);
 
+/* Kernel-internal timestamps of a trace build (compiled with -DSSA_TRACE; a
+ * profiling aid, not part of the method): copies the clock64 record of the
+ * tcgen05 kernel's softmax / MMA-issuer events for the first CTAs of layer 5
+ * into `host` (`bytes` capacity).  Returns the bytes written, 0 in a normal
+ * build, -1 if `bytes` is too small or the copy fails.  Synchronous. */
+int32_t ssa_debug_trace(void *host, size_t bytes);
+
 /* ----------------------------------------------------------------------------
  * Multi-GPU split-KV for one long session (R-12)
  * -------------------------------------------------------------------------- */

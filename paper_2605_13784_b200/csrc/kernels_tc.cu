@@ -42,7 +42,10 @@ constexpr int kChunkBytes = 128 * 128;          // 128 rows x 128 B
 constexpr int kSlotBytes = 2 * kChunkBytes;     // one 128 x 128 bf16 tile = 32 KB
 constexpr int kNumSlots = 7;                    // 224 KB of tiles
 constexpr int kMaxStages = 3;
-constexpr float kRescaleLog2 = 8.0f;
+#ifndef SSA_RESCALE_LOG2
+#define SSA_RESCALE_LOG2 8.0f
+#endif
+constexpr float kRescaleLog2 = SSA_RESCALE_LOG2;   // lazy max threshold (log2 units)
 // setmaxnreg budget: the CTA's pool is fixed at launch (168 regs x 384 threads
 // from __launch_bounds__(384, 1)); setmaxnreg.inc blocks until registers are
 // free, so the rebalanced total must fit the pool or the kernel deadlocks.
@@ -81,6 +84,23 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// exp2 runs on MUFU (16/clk/SM on B200, one op per element).  Measured
+// alternatives that do not help on sm_100a (scripts/ubench_sfu.cu): a degree-3
+// polynomial on the FMA pipe (13.8 elements/clk/SM, issue-bound) and
+// ex2.approx.bf16x2 (ptxas splits it into two MUFU.EX2.BF16 + PRMT).
+
+// Optional per-tile timestamps (debug builds with -DSSA_TRACE): clock64 of the
+// softmax and MMA-issuer events of a few CTAs, read back by ssa_debug_trace().
+#ifdef SSA_TRACE
+constexpr int kTraceCtas = 4, kTraceTiles = 256, kTraceLayer = 5;
+__device__ unsigned long long g_trace[kTraceCtas][4][kTraceTiles][2];
+#define TRACE(cond, row, j, w, val) \
+  do { if ((cond) && blockIdx.y == kTraceLayer && blockIdx.x < kTraceCtas && (j) < kTraceTiles) \
+         g_trace[blockIdx.x][row][j][w] = (val); } while (0)
+#else
+#define TRACE(cond, row, j, w, val) do { } while (0)
+#endif
 
 // D[tmem] (+)= A[tmem] * B[smem desc]  (A = P, K-major in TMEM).
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -236,6 +256,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               const int e = event_of(k, it, nsh, nt0, nt1);
               const int s = e % NS;
               mbar_wait(&bar.p_full[k], it & 1);
+              TRACE(true, 2 + k, it, 0, clock64());
               mbar_wait(&bar.v_full[s], (e / NS) & 1);
               tc_fence_after();
               const uint64_t vd = vd0 + (uint64_t)s * kStageStep;
@@ -264,6 +285,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
                 mma_bf16_ss(d, qd + off, kd + off, idesc_s, kk > 0 ? 1u : 0u);
               }
               mma_commit(&bar.s_full[k]);
+              TRACE(true, 2 + k, jn, 1, clock64());
             }
           }
         }
@@ -294,6 +316,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const bool is_pool = tile < n_pool_tiles;
         const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBN;
         mbar_wait(&bar.s_full[k], j & 1);
+        TRACE(r == 0, k, j, 0, clock64());
         tc_fence_after();
         float sv[kBN];
         {
@@ -329,9 +352,16 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
             sv[i] = ok ? sv[i] : -CUDART_INF_F;
           }
         }
-        float mt = sv[0];
+        // row max: 8 independent 3-input max chains (FMNMX3), then a short tree
+        float mx8[8];
 #pragma unroll
-        for (int i = 1; i < kBN; ++i) mt = fmaxf(mt, sv[i]);
+        for (int c8 = 0; c8 < 8; ++c8) mx8[c8] = fmaxf(sv[c8], sv[c8 + 8]);
+#pragma unroll
+        for (int i = 16; i < kBN; i += 16)
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) mx8[c8] = fmaxf(mx8[c8], fmaxf(sv[i + c8], sv[i + 8 + c8]));
+        const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         float alpha = 1.f;
         if (mt > m_run + kRescaleLog2 / c || m_run == -CUDART_INF_F) {
           const float m_new = fmaxf(m_run, mt);
@@ -340,15 +370,18 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         }
         const float mc = (m_run == -CUDART_INF_F) ? 0.f : m_run * c;
         uint32_t pk[kBN / 2];
-        float2 sum2 = make_float2(0.f, 0.f);
+        float2 sum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
         const float2 c2 = make_float2(c, c), nmc2 = make_float2(-mc, -mc);
 #pragma unroll
         for (int i = 0; i < kBN / 2; ++i) {
           const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), c2, nmc2);
           const float2 e = make_float2(ex2(x.x), ex2(x.y));
-          sum2 = __fadd2_rn(sum2, e);
+          sum4[i & 3] = __fadd2_rn(sum4[i & 3], e);
           pk[i] = pack_bf16(e.x, e.y);
         }
+        const float2 s01 = __fadd2_rn(sum4[0], sum4[1]), s23 = __fadd2_rn(sum4[2], sum4[3]);
+        const float2 sum2 = __fadd2_rn(s01, s23);
         l_run = l_run * alpha + (sum2.x + sum2.y);
         // O rescale (PV(j-1) completed: s_full(j) committed after it)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -378,6 +411,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
+        TRACE(r == 0, k, j, 1, clock64());
         if (lane == 0) mbar_arrive(&bar.p_full[k]);
       }
       // ----------------------------------------------------------- epilogue
@@ -526,6 +560,17 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 }  // namespace
 
 int tc_key_tile() { return kBN; }
+
+int tc_debug_trace(void* host, size_t bytes) {
+#ifdef SSA_TRACE
+  if (bytes < sizeof(g_trace)) return -1;
+  if (cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)) != cudaSuccess) return -1;
+  return (int)sizeof(g_trace);
+#else
+  (void)host; (void)bytes;
+  return 0;
+#endif
+}
 int tc_rows_tile() { return kM; }
 bool tc_supported_shape(int D, int G, bool bf16) {
   return bf16 && D == kD && G >= 1 && G <= 16 && (kM % G) == 0 && get_encode() != nullptr;

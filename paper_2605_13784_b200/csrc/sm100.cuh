@@ -36,8 +36,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Latency-critical waits (the softmax <-> MMA-issuer handoffs) spin on try_wait
+// without a suspend-time hint: with a long hint the retry path compiles to
+// NANOSLEEP.SYNCS and the measured wake-up lag was 250-450 cycles per handoff
+// (scripts/trace_run.py).  SSA_MBAR_SLEEP_HINT restores a hint for experiments.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#ifdef SSA_MBAR_SLEEP_HINT
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
@@ -45,6 +50,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // ---------------------------------------------------------------- TMA

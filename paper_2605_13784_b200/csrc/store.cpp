@@ -507,6 +507,8 @@ extern "C" {
 
 int32_t ssa_abi_version(void) { return SSA_ABI_VERSION; }
 
+int32_t ssa_debug_trace(void* host, size_t bytes) { return ssa::tc_debug_trace(host, bytes); }
+
 const char* ssa_status_str(ssa_status s) {
   switch (s) {
     case SSA_OK: return "SSA_OK";

@@ -55,6 +55,7 @@ struct RunOpts {
 
 // tcgen05 path (kernels_tc.cu)
 int tc_key_tile();
+int tc_debug_trace(void* host, size_t bytes);
 int tc_rows_tile();
 cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, cudaStream_t s);
 bool tc_supported_shape(int D, int G, bool bf16);
