@@ -94,13 +94,34 @@ __device__ __forceinline__ float ex2(float x) {
 // softmax and MMA-issuer events of a few CTAs, read back by ssa_debug_trace().
 #ifdef SSA_TRACE
 constexpr int kTraceCtas = 4, kTraceTiles = 256, kTraceLayer = 5;
-__device__ unsigned long long g_trace[kTraceCtas][4][kTraceTiles][2];
+__device__ unsigned long long g_trace[kTraceCtas][12][kTraceTiles][2];
 #define TRACE(cond, row, j, w, val) \
   do { if ((cond) && blockIdx.y == kTraceLayer && blockIdx.x < kTraceCtas && (j) < kTraceTiles) \
          g_trace[blockIdx.x][row][j][w] = (val); } while (0)
 #else
 #define TRACE(cond, row, j, w, val) do { } while (0)
 #endif
+
+// Optional exp2 offload (SSA_POLY_PAIRS_OF_8 = n > 0): n of every 8 element
+// pairs use 2^x = 2^j * p(f) on the FMA pipe (j = rint(x) by the 1.5*2^23 magic
+// add, f in [-0.5, 0.5], degree-3 minimax p with relative error 7.5e-5, far
+// below bf16's 2^-8 unit roundoff of P; x clamped at -126).
+#ifndef SSA_POLY_PAIRS_OF_8
+#define SSA_POLY_PAIRS_OF_8 0
+#endif
+constexpr int kPolyPairsOf8 = SSA_POLY_PAIRS_OF_8;
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(make_float2(0.0551716685f, 0.0551716685f), f, make_float2(0.2426111549f, 0.2426111549f));
+  q = __ffma2_rn(q, f, make_float2(0.6932609677f, 0.6932609677f));
+  q = __ffma2_rn(q, f, make_float2(0.9999280572f, 0.9999280572f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
 
 // D[tmem] (+)= A[tmem] * B[smem desc]  (A = P, K-major in TMEM).
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -326,6 +347,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           tmem_ld32(s_col + 64, rc);
           tmem_ld32(s_col + 96, rd);
           tmem_wait_ld();
+          TRACE(r == 0, 4 + k, j, 0, clock64());
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             sv[i] = __uint_as_float(ra[i]);
@@ -369,6 +391,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           m_run = m_new;
         }
         const float mc = (m_run == -CUDART_INF_F) ? 0.f : m_run * c;
+        TRACE(r == 0, 6 + k, j, 0, clock64());
         uint32_t pk[kBN / 2];
         float2 sum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
@@ -376,12 +399,13 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
 #pragma unroll
         for (int i = 0; i < kBN / 2; ++i) {
           const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), c2, nmc2);
-          const float2 e = make_float2(ex2(x.x), ex2(x.y));
+          const float2 e = ((i & 7) >= 8 - kPolyPairsOf8) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           sum4[i & 3] = __fadd2_rn(sum4[i & 3], e);
           pk[i] = pack_bf16(e.x, e.y);
         }
         const float2 s01 = __fadd2_rn(sum4[0], sum4[1]), s23 = __fadd2_rn(sum4[2], sum4[3]);
         const float2 sum2 = __fadd2_rn(s01, s23);
+        TRACE(r == 0, 4 + k, j, 1, clock64());
         l_run = l_run * alpha + (sum2.x + sum2.y);
         // O rescale (PV(j-1) completed: s_full(j) committed after it)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -409,9 +433,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           tmem_st32(s_col + 32, hi);
         }
         tmem_wait_st();
+        TRACE(r == 0, 6 + k, j, 1, clock64());
         tc_fence_before();
         __syncwarp();
         TRACE(r == 0, k, j, 1, clock64());
+        TRACE(lane == 0 && k == 0, 8 + (warp & 3), j, 0, clock64());
+        TRACE(lane == 0 && k == 1, 8 + (warp & 3), j, 1, clock64());
         if (lane == 0) mbar_arrive(&bar.p_full[k]);
       }
       // ----------------------------------------------------------- epilogue
