@@ -342,7 +342,9 @@ int32_t ssa_abi_version(void);
  * work units for n_segs segments of seg_m[i] new tokens over seg_slots[i]
  * cached slots and writes up to cap_units units as 8 int32 each
  * (seg, kv_head, q_tok0, q_ntok, tile_lo, tile_hi, group, split) into
- * units_out (may be NULL).  Returns the number of units. */
+ * units_out (may be NULL).  key_tile == 128 (the tcgen05 key tile) plans for
+ * two-slot tcgen05 CTAs, where a lone one-q-tile unit is split in two so
+ * that its halves share a CTA.  Returns the number of units. */
 int32_t ssa_debug_plan(int32_t n_segs, const int32_t *seg_m, const int32_t *seg_slots,
                        int32_t Hkv, int32_t q_tile_tokens, int32_t key_tile, int32_t n_layers,
                        int32_t num_sms, int32_t ctas_per_sm, int32_t max_splits,

@@ -96,9 +96,23 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
   // Order groups by per-unit work, largest first (LPT over the CTA rasterizer).
   std::vector<int> order(items.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  // A unit that cannot share a CTA with another q tile over the same keys (a
+  // one-tile segment whose cached pool no other segment of the call reads, e.g.
+  // a 32-token query of one session in a multi-tenant batch) would run alone in
+  // a two-slot tcgen05 CTA with one softmax warpgroup idle.  Split it (into an
+  // two key ranges) so the halves pair up as one SPLIT CTA instead.
+  std::vector<int> seg_qtiles(segs.size(), 0), pool_users(segs.size(), 0);
+  for (size_t s = 0; s < segs.size(); ++s) {
+    seg_qtiles[s] = (int)ceil_div(segs[s].m, c.q_tile_tokens);
+    for (size_t t = 0; t < segs.size(); ++t)
+      if (segs[t].n_slots > 0 && segs[t].pages == segs[s].pages && segs[t].n_slots == segs[s].n_slots) ++pool_users[s];
+  }
   auto n_splits_of = [&](const Item& it) -> int64_t {
     int64_t n = best_tpu > 0 ? ceil_div(it.tiles, best_tpu) : std::min<int64_t>(max_splits, it.tiles);
-    return std::max<int64_t>(1, std::min<int64_t>(n, std::max<int64_t>(1, it.tiles)));
+    n = std::max<int64_t>(1, std::min<int64_t>(n, std::max<int64_t>(1, it.tiles)));
+    const bool alone = seg_qtiles[it.seg] == 1 && pool_users[it.seg] <= 1;
+    if (c.pair_slots && alone && it.tiles >= 2 && n == 1 && max_splits >= 2) n = 2;
+    return std::min<int64_t>(n, it.tiles);
   };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     const double wa = (double)items[a].tiles / (double)n_splits_of(items[a]);

@@ -18,6 +18,7 @@ struct PlanConfig {
   double unit_overhead_tiles = 1.0;
   int fault = 0;
   bool force_groups = false;  // every item writes partials (sharded query)
+  bool pair_slots = false;    // units run in two-slot (tcgen05) CTAs: avoid lone units
 };
 
 struct Plan {

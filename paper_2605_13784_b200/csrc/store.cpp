@@ -326,6 +326,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
     pc.fault = (int)opt_fault;
     pc.force_groups = opts.force_groups;
+    pc.pair_slots = use_tc;
     plan_units(segs, pc, &plan);
   }
   std::vector<TcPair> pairs;
@@ -1150,6 +1151,7 @@ int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_
   pc.num_sms = num_sms;
   pc.ctas_per_sm = ctas_per_sm;
   pc.max_splits = max_splits;
+  pc.pair_slots = key_tile == tc_key_tile();   // the tcgen05 key tile selects two-slot CTAs
   Plan plan;
   plan_units(segs, pc, &plan);
   const int32_t n = (int32_t)plan.units.size();

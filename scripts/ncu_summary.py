@@ -2,7 +2,7 @@
 """Summarise ncu captures for profiles/ (run here, on the files gpurun brought back).
 
     python scripts/ncu_summary.py raw  <raw.csv>  [--traffic profiles/traffic.json]
-    python scripts/ncu_summary.py launches <launches.csv>
+    python scripts/ncu_summary.py launches <launches.csv> [--slice a:b]
 
 `raw` reads an `ncu -i rep --page raw --csv` export (one row per profiled launch) and
 prints duration, DRAM bytes, tensor-pipe / XU / issue utilisation per launch.  With
@@ -82,7 +82,7 @@ def cmd_raw(path, traffic_path=None):
         print("wrote", traffic_path)
 
 
-def cmd_launches(path):
+def cmd_launches(path, sl=None):
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
@@ -92,6 +92,11 @@ def cmd_launches(path):
         if hdr and len(r) == len(hdr):
             data.append(dict(zip(hdr, r)))
     agg = collections.defaultdict(list)
+    if sl:
+        a, b = (int(x) for x in sl.split(":"))
+        data = data[a:b]      # the launches of the timed steps
+        for d in data:
+            print("  ", d["Kernel Name"].split("(")[0].split("::")[-1], d["Metric Value"], d["Metric Unit"])
     for d in data:
         name = d["Kernel Name"].split("(")[0].split("::")[-1]
         agg[name].append(float(d["Metric Value"].replace(",", "")) * UNITS.get(d["Metric Unit"], 1.0))
@@ -105,4 +110,4 @@ if __name__ == "__main__":
         tp = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
         cmd_raw(sys.argv[2], tp)
     else:
-        cmd_launches(sys.argv[2])
+        cmd_launches(sys.argv[2], sys.argv[sys.argv.index("--slice") + 1] if "--slice" in sys.argv else None)

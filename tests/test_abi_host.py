@@ -113,4 +113,11 @@ def test_planner_does_not_shred_heterogeneous_batches():
     ns = [4096 + 256 * s for s in range(48)]
     seg_m = [256 if s % 2 == 0 else 32 for s in range(48)] + [1024] * 4
     units = ssa.debug_plan(seg_m, ns + [0] * 4, 8, 32, 128, n_layers=32, num_sms=148, ctas_per_sm=2)
-    assert all(u[6] == -1 for u in units)
+    for u in units:
+        if seg_m[u[0]] == 32:
+            # a lone 32-token query (one q tile, private pool) is halved so its two key
+            # ranges fill both softmax slots of one tcgen05 CTA
+            assert u[6] >= 0 and u[7] in (0, 1)
+        else:
+            assert u[6] == -1          # appends and stateless prompts pair their own q tiles
+    assert sum(1 for u in units if seg_m[u[0]] == 32) == 24 * 8 * 2
