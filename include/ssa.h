@@ -257,7 +257,8 @@ typedef struct {
     int64_t pages_reserved;
     int64_t h2d_bytes;           /* host staging copies */
     int64_t d2h_bytes;
-    int64_t tc_launches;         /* attention launches on the tcgen05 kernel */
+    int64_t tc_launches;         /* attention launches on the tcgen05 kernels */
+    int64_t tc_pair_launches;    /* of which on the cta_group::2 CTA-pair kernel */
 } ssa_stats;
 
 ssa_status ssa_store_stats(ssa_store_t store, ssa_stats *out, int32_t reset);
@@ -271,9 +272,12 @@ typedef enum {
     SSA_OPT_TC_Q_TILES = 4,     /* tcgen05 Q tiles per CTA (1 or 2; 0 = auto) */
     SSA_OPT_TIMING = 5,         /* 1: record CUDA events around every kernel launch
                                    (on the call's stream) for ssa_store_timing */
-    SSA_OPT_FUSED_MERGE = 6     /* 1: the last tcgen05 CTA of a split group merges the
+    SSA_OPT_FUSED_MERGE = 6,    /* 1: the last tcgen05 CTA of a split group merges the
                                    group in-kernel (no combine launch); 0 (default):
                                    separate combine kernel */
+    SSA_OPT_CTA_PAIR = 7        /* 1: work units whose key tiles are the same keys (q tiles
+                                   of one append / prompt) run on cta_group::2 CTA pairs
+                                   with double-buffered S; 0: two-slot CTAs only */
 } ssa_option;
 ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
 
@@ -289,8 +293,9 @@ ssa_status ssa_store_timing(ssa_store_t store, double ms[SSA_TIMING_KINDS],
 
 /* Kernel-internal timestamps of a trace build (compiled with -DSSA_TRACE; a
  * profiling aid, not part of the method): copies the clock64 record of the
- * tcgen05 kernel's softmax / MMA-issuer events for the first CTAs of layer 5
- * into `host` (`bytes` capacity).  Returns the bytes written, 0 in a normal
+ * tcgen05 kernels' softmax / MMA-issuer events for the first CTAs of layer 5
+ * into `host` (`bytes` capacity): the two-slot kernel's record, followed by the
+ * CTA-pair kernel's if it fits.  Returns the bytes written, 0 in a normal
  * build, -1 if `bytes` is too small or the copy fails.  Synchronous. */
 int32_t ssa_debug_trace(void *host, size_t bytes);
 

@@ -16,6 +16,7 @@ import os
 
 __all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", "WORK_STATELESS",
            "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING", "OPT_FUSED_MERGE",
+           "OPT_CTA_PAIR",
            "debug_plan", "TIMING_KINDS"]
 TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter")
 
@@ -24,6 +25,7 @@ LIB_PATH = os.path.join(_HERE, "libssa.so")
 
 WORK_APPEND, WORK_QUERY, WORK_STATELESS = 0, 1, 2
 OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES, OPT_TIMING, OPT_FUSED_MERGE = 1, 2, 3, 4, 5, 6
+OPT_CTA_PAIR = 7
 BF16, FP32 = 0, 1
 
 _STATUS = {0: "SSA_OK", -1: "SSA_ERR_INVALID_ARG", -2: "SSA_ERR_UNKNOWN_SESSION", -3: "SSA_ERR_POOL_EXHAUSTED",
@@ -59,7 +61,7 @@ class WorkItem(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("kernel_launches", "rows_computed", "query_rows",
                                               "tokens_appended", "pages_reserved", "h2d_bytes", "d2h_bytes",
-                                              "tc_launches")]
+                                              "tc_launches", "tc_pair_launches")]
 
 
 def _load():

@@ -59,7 +59,8 @@ struct Bars {
   uint64_t q_full;
   uint64_t k_full[kMaxStages];
   uint64_t v_full[kMaxStages];
-  uint64_t kv_empty[kMaxStages];
+  uint64_t k_empty[kMaxStages];   // K stage consumed by the S MMA(s) of its event
+  uint64_t v_empty[kMaxStages];   // V stage consumed by the PV MMA(s) of its event
   uint64_t s_full[2];
   uint64_t p_full[2];
   uint64_t o_final[2];
@@ -110,18 +111,6 @@ __device__ unsigned long long g_trace[kTraceCtas][12][kTraceTiles][2];
 #define SSA_POLY_PAIRS_OF_8 0
 #endif
 constexpr int kPolyPairsOf8 = SSA_POLY_PAIRS_OF_8;
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
-  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
-  float2 q = __ffma2_rn(make_float2(0.0551716685f, 0.0551716685f), f, make_float2(0.2426111549f, 0.2426111549f));
-  q = __ffma2_rn(q, f, make_float2(0.6932609677f, 0.6932609677f));
-  q = __ffma2_rn(q, f, make_float2(0.9999280572f, 0.9999280572f));
-  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
-}
 
 // D[tmem] (+)= A[tmem] * B[smem desc]  (A = P, K-major in TMEM).
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -162,10 +151,15 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   const int nt0 = w0.tile_hi - w0.tile_lo;
   const int nsh = pr.ub >= 0 ? pr.n_shared : 0;
   const bool two_q = pr.ub >= 0 && !pr.same_q;
-  const int NS = two_q ? 2 : 3;
-  // smem tile slots: Q (1 or 2), then NS stages of (K, V)
+  // smem tile slots (7 x 32 KB): Q (1 or 2), a K ring of NK and a V ring of NV
+  // stages.  K(e) is released by its S MMA, V(e) by its PV MMA, which run
+  // about a tile later, so the rings and their producer warps progress
+  // independently (K loads run further ahead).
+  const int NK = 3;
+  const int NV = two_q ? 2 : 3;
   uint8_t* q_buf[2] = {tiles, two_q ? tiles + kSlotBytes : tiles};
-  uint8_t* stage_base = tiles + (two_q ? 2 : 1) * kSlotBytes;
+  uint8_t* k_base = tiles + (two_q ? 2 : 1) * kSlotBytes;
+  uint8_t* v_base = k_base + NK * kSlotBytes;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.q);
@@ -177,7 +171,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&bar.k_full[s], 1);
       mbar_init(&bar.v_full[s], 1);
-      mbar_init(&bar.kv_empty[s], 1);
+      mbar_init(&bar.k_empty[s], 1);
+      mbar_init(&bar.v_empty[s], 1);
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&bar.s_full[k], 1);
@@ -194,19 +189,29 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsWG0));
-    if (warp == 0) {
-      // ----------------------------------------------------------- TMA producer
+    if (warp == 0 || warp == 3) {
+      // ----------------------------------------------------------- TMA producers
+      // warp 0: Q and the K ring; warp 3: the V ring
       if (elect_one()) {
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
-        const int nq = two_q ? 2 : 1;
-        mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
-        for (int k = 0; k < nq; ++k) {
-          const WorkUnit& w = k ? w1 : w0;
-          const int32_t qrow = (int32_t)(in_l + p.segs[w.seg].row0 + w.q_tok0);
-          for (int c = 0; c < 2; ++c)
-            tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
+        const bool is_k = warp == 0;
+        if (is_k) {
+          const int nq = two_q ? 2 : 1;
+          mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
+          for (int k = 0; k < nq; ++k) {
+            const WorkUnit& w = k ? w1 : w0;
+            const int32_t qrow = (int32_t)(in_l + p.segs[w.seg].row0 + w.q_tok0);
+            for (int c = 0; c < 2; ++c)
+              tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
+          }
         }
+        const int NR = is_k ? NK : NV;
+        uint8_t* ring = is_k ? k_base : v_base;
+        uint64_t* full = is_k ? bar.k_full : bar.v_full;
+        uint64_t* empty = is_k ? bar.k_empty : bar.v_empty;
+        const CUtensorMap* pool_map = is_k ? &maps.pk : &maps.pv;
+        const CUtensorMap* tail_map = is_k ? &maps.kt : &maps.vt;
         const int E = nt0 + nt1 - nsh;
         const int m01 = min(nt0, nt1) - nsh;
         for (int e = 0; e < E; ++e) {
@@ -216,40 +221,29 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           else { k = nt0 > nt1 ? 0 : 1; j = nsh + m01 + (e - nsh - 2 * m01); }
           const WorkUnit& w = k ? w1 : w0;
           const SegDesc sg = p.segs[w.seg];
-          const int s = e % NS;
-          if (e >= NS) mbar_wait(&bar.kv_empty[s], ((e / NS) - 1) & 1);
-          uint8_t* kb = stage_base + (2 * s) * kSlotBytes;
-          uint8_t* vb = kb + kSlotBytes;
+          const int s = e % NR;
+          if (e >= NR) mbar_wait(&empty[s], ((e / NR) - 1) & 1);
+          uint8_t* dst = ring + s * kSlotBytes;
           const int tile = w.tile_lo + j;
           const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
-          mbar_arrive_expect_tx(&bar.k_full[s], kSlotBytes);
+          mbar_arrive_expect_tx(&full[s], kSlotBytes);
           if (tile < n_pool_tiles) {
             const int key0 = tile * kBN;
             const int nb = kBN / box_rows;
-            auto row_of = [&](int b) -> int32_t {
+            for (int b = 0; b < nb; ++b) {
               const int slot = key0 + b * box_rows;
-              if (slot >= sg.n_slots) return 0x7FFFFFF0;   // past the tensor -> TMA zero fill
-              const int64_t page = __ldg(sg.pages + slot / p.P);
-              return (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
-            };
-            for (int b = 0; b < nb; ++b) {
-              const int32_t row = row_of(b);
+              int32_t row = 0x7FFFFFF0;   // past the tensor -> TMA zero fill
+              if (slot < sg.n_slots) {
+                const int64_t page = __ldg(sg.pages + slot / p.P);
+                row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
+              }
               for (int c = 0; c < 2; ++c)
-                tma_load_2d(kb + c * kChunkBytes + b * box_rows * 128, &maps.pk, &bar.k_full[s], c * 64, row);
-            }
-            mbar_arrive_expect_tx(&bar.v_full[s], kSlotBytes);
-            for (int b = 0; b < nb; ++b) {
-              const int32_t row = row_of(b);
-              for (int c = 0; c < 2; ++c)
-                tma_load_2d(vb + c * kChunkBytes + b * box_rows * 128, &maps.pv, &bar.v_full[s], c * 64, row);
+                tma_load_2d(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row);
             }
           } else {
             const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
             for (int c = 0; c < 2; ++c)
-              tma_load_3d(kb + c * kChunkBytes, &maps.kt, &bar.k_full[s], c * 64, w.kv_head, krow);
-            mbar_arrive_expect_tx(&bar.v_full[s], kSlotBytes);
-            for (int c = 0; c < 2; ++c)
-              tma_load_3d(vb + c * kChunkBytes, &maps.vt, &bar.v_full[s], c * 64, w.kv_head, krow);
+              tma_load_3d(dst + c * kChunkBytes, tail_map, &full[s], c * 64, w.kv_head, krow);
           }
         }
       }
@@ -261,9 +255,9 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         // descriptor bases; per-step offsets are compile-time adds on the 16-byte address field
         const uint64_t qd0 = sdesc_sw128(smem_u32(q_buf[0]), 16, 1024);
         const uint64_t qd1 = sdesc_sw128(smem_u32(q_buf[1]), 16, 1024);
-        const uint64_t kd0 = sdesc_sw128(smem_u32(stage_base), 16, 1024);
-        const uint64_t vd0 = sdesc_sw128(smem_u32(stage_base + kSlotBytes), kChunkBytes, 1024);
-        constexpr uint64_t kStageStep = (2 * kSlotBytes) >> 4;
+        const uint64_t kd0 = sdesc_sw128(smem_u32(k_base), 16, 1024);
+        const uint64_t vd0 = sdesc_sw128(smem_u32(v_base), kChunkBytes, 1024);
+        constexpr uint64_t kStageStep = kSlotBytes >> 4;
         mbar_wait(&bar.q_full, 0);
         tc_fence_after();
         const int jmax = max(nt0, nt1);
@@ -275,10 +269,11 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
             if (it >= 0 && it < ntk) {
               // ---- PV(k, it): O_k += P_k (TMEM) * V
               const int e = event_of(k, it, nsh, nt0, nt1);
-              const int s = e % NS;
+              const int s = e % NV;
               mbar_wait(&bar.p_full[k], it & 1);
               TRACE(true, 2 + k, it, 0, clock64());
-              mbar_wait(&bar.v_full[s], (e / NS) & 1);
+              mbar_wait(&bar.v_full[s], (e / NV) & 1);
+              TRACE(true, 11, it, k, clock64());
               tc_fence_after();
               const uint64_t vd = vd0 + (uint64_t)s * kStageStep;
               const uint32_t o = tmem + 256u * k + 128u;
@@ -287,15 +282,16 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               for (int kk = 0; kk < kBN / 16; ++kk)   // 16 keys = 2048 B down each 64-column V chunk
                 mma_bf16_ts(o, pa + 8 * kk, vd + (uint64_t)((kk * 2048) >> 4), idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
               // a shared stage is free after slot 1's PV, a private one after its own
-              if (it >= nsh || k == 1) mma_commit(&bar.kv_empty[s]);
+              if (it >= nsh || k == 1) mma_commit(&bar.v_empty[s]);
               if (it == ntk - 1) mma_commit(&bar.o_final[k]);
             }
             const int jn = it + 1;
             if (jn < ntk) {
               // ---- S(k, jn) = Q_k K^T
               const int e = event_of(k, jn, nsh, nt0, nt1);
-              const int s = e % NS;
-              mbar_wait(&bar.k_full[s], (e / NS) & 1);
+              const int s = e % NK;
+              mbar_wait(&bar.k_full[s], (e / NK) & 1);
+              TRACE(true, 10, jn, k, clock64());
               tc_fence_after();
               const uint64_t qd = k ? qd1 : qd0;
               const uint64_t kd = kd0 + (uint64_t)s * kStageStep;
@@ -306,6 +302,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
                 mma_bf16_ss(d, qd + off, kd + off, idesc_s, kk > 0 ? 1u : 0u);
               }
               mma_commit(&bar.s_full[k]);
+              if (jn >= nsh || k == 1) mma_commit(&bar.k_empty[s]);
               TRACE(true, 2 + k, jn, 1, clock64());
             }
           }
@@ -437,8 +434,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         tc_fence_before();
         __syncwarp();
         TRACE(r == 0, k, j, 1, clock64());
-        TRACE(lane == 0 && k == 0, 8 + (warp & 3), j, 0, clock64());
-        TRACE(lane == 0 && k == 1, 8 + (warp & 3), j, 1, clock64());
+        TRACE(lane == 0 && k == 0 && (warp & 3) < 2, 8 + (warp & 3), j, 0, clock64());
+        TRACE(lane == 0 && k == 1 && (warp & 3) < 2, 8 + (warp & 3), j, 1, clock64());
         if (lane == 0) mbar_arrive(&bar.p_full[k]);
       }
       // ----------------------------------------------------------- epilogue
@@ -573,8 +570,10 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-            const cuuint32_t* box) {
+}  // namespace
+
+bool encode_bf16_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+                     const cuuint64_t* strides_bytes, const cuuint32_t* box) {
   EncodeTiledFn fn = get_encode();
   if (!fn) return false;
   cuuint32_t es[3] = {1, 1, 1};
@@ -584,6 +583,11 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
   return r == CUDA_SUCCESS;
 }
 
+namespace {
+bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+            const cuuint32_t* box) {
+  return encode_bf16_map(m, base, rank, dims, strides_bytes, box);
+}
 }  // namespace
 
 int tc_key_tile() { return kBN; }

@@ -155,10 +155,51 @@ static int shared_tiles(const std::vector<SegDesc>& segs, const WorkUnit& a, con
   return std::max(0, std::min(std::min(na, nb), pool_tiles - a.tile_lo));
 }
 
-void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out) {
+void pair_units_cta2(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
+                     std::vector<char>* used) {
+  out->clear();
+  const int n = (int)plan.units.size();
+  used->assign(n, 0);
+  // Two units can share every tcgen05.mma of a CTA pair when all their key
+  // tiles are the same keys: same KV head and tile range, and the same segment
+  // (q tiles of one append / prompt) or the same cached pool with no private
+  // own-token tiles in the range.
+  auto pool_tiles = [&](const WorkUnit& u) { return (segs[u.seg].n_slots + key_tile - 1) / key_tile; };
+  auto same_keys = [&](const WorkUnit& a, const WorkUnit& b) {
+    if (a.kv_head != b.kv_head || a.tile_lo != b.tile_lo || a.tile_hi != b.tile_hi) return false;
+    if (a.seg == b.seg) return a.q_tok0 != b.q_tok0;
+    const SegDesc& x = segs[a.seg];
+    const SegDesc& y = segs[b.seg];
+    return x.pages == y.pages && x.n_slots == y.n_slots && x.hole_lo == y.hole_lo && x.hole_hi == y.hole_hi &&
+           a.tile_hi <= pool_tiles(a);
+  };
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  auto key_of = [&](int i) {
+    const WorkUnit& u = plan.units[i];
+    const SegDesc& s = segs[u.seg];
+    return std::make_tuple(u.kv_head, u.tile_lo, u.tile_hi, (uintptr_t)s.pages, s.n_slots, u.seg, u.q_tok0);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key_of(a) < key_of(b); });
+  for (int ii = 0; ii + 1 < n; ++ii) {
+    const int a = order[ii], b = order[ii + 1];
+    if ((*used)[a] || (*used)[b]) continue;
+    if (plan.units[a].tile_hi == plan.units[a].tile_lo) continue;
+    if (same_keys(plan.units[a], plan.units[b])) {
+      (*used)[a] = (*used)[b] = 1;
+      out->push_back({a, b, plan.units[a].tile_hi - plan.units[a].tile_lo, 0});
+    }
+  }
+  std::stable_sort(out->begin(), out->end(), [](const TcPair& x, const TcPair& y) { return x.n_shared > y.n_shared; });
+}
+
+void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
+                const std::vector<char>* skip) {
   out->clear();
   const int n = (int)plan.units.size();
   std::vector<char> used(n, 0);
+  if (skip)
+    for (int i = 0; i < n; ++i) used[i] = (*skip)[i];
   // 1. shared-key pairs: bucket by (kv_head, tile_lo, pool), pair neighbours
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;

@@ -30,6 +30,13 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
 
 // Pair units into two-slot tcgen05 CTAs (SHARED first, then SPLIT, then SINGLE),
 // largest work first.
-void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out);
+void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
+                const std::vector<char>* skip = nullptr);
+
+// Pair units whose key tiles are the same keys into cta_group::2 CTA pairs
+// (kernels_tc2.cu): ua runs on CTA rank 0, ub on rank 1; n_shared = tiles.
+// `used` marks the paired units (the rest go to pair_units).
+void pair_units_cta2(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
+                     std::vector<char>* used);
 
 }  // namespace ssa

@@ -329,8 +329,15 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     pc.pair_slots = use_tc;
     plan_units(segs, pc, &plan);
   }
-  std::vector<TcPair> pairs;
-  if (use_tc) pair_units(segs, plan, pc.key_tile, &pairs);
+  // tcgen05: units with identical key tiles run as cta_group::2 CTA pairs
+  // (kernels_tc2.cu), the rest as two-slot CTAs (kernels_tc.cu).
+  std::vector<TcPair> pairs, pairs2;
+  const bool fused_req = use_tc && opt_fused_merge;
+  if (use_tc) {
+    std::vector<char> in_pair2;
+    if (opt_cta_pair && !fused_req) pair_units_cta2(segs, plan, pc.key_tile, &pairs2, &in_pair2);
+    pair_units(segs, plan, pc.key_tile, &pairs, pairs2.empty() ? nullptr : &in_pair2);
+  }
   // ---- append segments for the scatter
   std::vector<int32_t> app_idx;
   for (int i = 0; i < (int)segs.size(); ++i)
@@ -348,8 +355,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   const size_t b_app = app_segs.size() * sizeof(SegDesc);
   const size_t b_pre = prefix.size() * sizeof(int32_t);
   const size_t b_pairs = pairs.size() * sizeof(TcPair);
+  const size_t b_pairs2 = pairs2.size() * sizeof(TcPair);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre) + al(b_pairs);
+  const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre) + al(b_pairs) + al(b_pairs2);
   const size_t off = ring.alloc(total);
   if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
   size_t o = off;
@@ -365,6 +373,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   auto d_app = reinterpret_cast<const SegDesc*>(put(app_segs.data(), b_app));
   auto d_pre = reinterpret_cast<const int32_t*>(put(prefix.data(), b_pre));
   auto d_pairs = reinterpret_cast<const TcPair*>(put(pairs.data(), b_pairs));
+  auto d_pairs2 = reinterpret_cast<const TcPair*>(put(pairs2.data(), b_pairs2));
   SSA_CUDA(this, ring.to_device(off, total, st));
 
   // ---- KA: scatter new K/V into pages
@@ -446,6 +455,14 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     }
     cudaEvent_t t0 = tick(st);
     if (use_tc) {
+      if (!pairs2.empty()) {
+        SSA_CUDA(this, launch_attn_tc2(ap, d_pairs2, (int)pairs2.size(), n_layers, st));
+        stats.tc_pair_launches++;
+        if (!pairs.empty()) {   // the two-slot launch below is counted there
+          stats.kernel_launches++;
+          stats.tc_launches++;
+        }
+      }
       SSA_CUDA(this, launch_attn_tc(ap, n_layers, (int)opt_tc_qtiles, st));
     } else {
       SSA_CUDA(this, launch_attn_simt(ap, n_layers, cfg.dtype == SSA_BF16, st));
@@ -508,7 +525,12 @@ extern "C" {
 
 int32_t ssa_abi_version(void) { return SSA_ABI_VERSION; }
 
-int32_t ssa_debug_trace(void* host, size_t bytes) { return ssa::tc_debug_trace(host, bytes); }
+int32_t ssa_debug_trace(void* host, size_t bytes) {
+  const int a = ssa::tc_debug_trace(host, bytes);
+  if (a <= 0) return a;
+  const int b = ssa::tc2_debug_trace(static_cast<char*>(host) + a, bytes - (size_t)a);
+  return b < 0 ? a : a + b;
+}
 
 const char* ssa_status_str(ssa_status s) {
   switch (s) {
@@ -629,6 +651,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
     case SSA_OPT_TC_Q_TILES: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_tc_qtiles = value; break;
     case SSA_OPT_TIMING: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_timing = value; break;
     case SSA_OPT_FUSED_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_fused_merge = value; break;
+    case SSA_OPT_CTA_PAIR: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_cta_pair = value; break;
     default: return SSA_ERR_INVALID_ARG;
   }
   return SSA_OK;

@@ -1,6 +1,7 @@
 // store.h — the store and session objects behind the opaque ssa_store_t.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <functional>
@@ -56,9 +57,15 @@ struct RunOpts {
 // tcgen05 path (kernels_tc.cu)
 int tc_key_tile();
 int tc_debug_trace(void* host, size_t bytes);
+int tc2_debug_trace(void* host, size_t bytes);
 int tc_rows_tile();
 cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, cudaStream_t s);
 bool tc_supported_shape(int D, int G, bool bf16);
+// bf16 tensor map, 128-byte swizzle (kernels_tc.cu); false if the driver entry point is missing.
+bool encode_bf16_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+                     const cuuint64_t* strides_bytes, const cuuint32_t* box);
+// cta_group::2 path (kernels_tc2.cu): CTA pairs sharing each K/V tile, S double-buffered.
+cudaError_t launch_attn_tc2(const AttnParams& p, const TcPair* d_pairs2, int n_pairs2, int n_layers, cudaStream_t s);
 
 }  // namespace ssa
 
@@ -87,6 +94,10 @@ struct ssa_store {
   int32_t* counters = nullptr;   // fused-merge group counters (zero between launches)
   size_t counters_cap = 0;
   int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0, opt_fused_merge = 0;
+#ifndef SSA_CTA_PAIR_DEFAULT
+#define SSA_CTA_PAIR_DEFAULT 0
+#endif
+  int64_t opt_cta_pair = SSA_CTA_PAIR_DEFAULT;   // SSA_OPT_CTA_PAIR
   ssa_stats stats{};
   int32_t ticket_seq = 0;
   int64_t last_plan_units = 0, last_plan_groups = 0;

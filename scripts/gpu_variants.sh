@@ -8,7 +8,7 @@ for f in variants/*.so; do
   b=$(basename $f .so)
   echo "== $b"
   case $b in
-    trace*) timeout 300 python scripts/trace_run.py && for k in append query; do mv gpurun_out/trace_$k.npy gpurun_out/${b}_$k.npy; done ;;
+    trace*) timeout 300 python scripts/trace_run.py && for k in append query; do mv gpurun_out/trace_$k.npy gpurun_out/${b}_$k.npy; mv gpurun_out/trace2_$k.npy gpurun_out/${b}_t2_$k.npy; done ;;
     *) timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --legs "${LEGS:-}" 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:

@@ -23,7 +23,8 @@ Qa, Ka, Va = bench.gen_new(torch, dev, spec, 0, n0, CFG["m_append"])
 Oa = torch.empty_like(Qa)
 Qq, Kq, Vq = bench.gen_new(torch, dev, spec, 1, 0, CFG["q_len"])
 Oq = torch.empty_like(Qq)
-buf = np.zeros(4 * 12 * 256 * 2, dtype=np.uint64)
+buf = np.zeros(4 * 12 * 256 * 2 + 4 * 2 * 4 * 256 * 2, dtype=np.uint64)
+n1 = 4 * 12 * 256 * 2
 lib = ssa.lib
 for kind in ("append", "query"):
     for _ in range(3):
@@ -36,5 +37,6 @@ for kind in ("append", "query"):
     n = lib.ssa_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
     print(kind, "trace bytes", n)
     os.makedirs("gpurun_out", exist_ok=True)
-    np.save(f"gpurun_out/trace_{kind}.npy", buf.reshape(4, 12, 256, 2).copy())
+    np.save(f"gpurun_out/trace_{kind}.npy", buf[:n1].reshape(4, 12, 256, 2).copy())
+    np.save(f"gpurun_out/trace2_{kind}.npy", buf[n1:].reshape(4, 2, 4, 256, 2).copy())
     buf[:] = 0

@@ -453,3 +453,79 @@ def test_fused_merge_option(cuda, nq):
         st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
         ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
         assert ok, (rep, e)
+
+
+@pytest.mark.parametrize("page_size", [16, 64, 128])
+def test_cta_pair_append_parity(cuda, page_size):
+    """SSA_OPT_CTA_PAIR: q tiles of an append pair up on cta_group::2 CTA pairs (double-buffered S,
+    K/V halves per SM); ragged R0 and appends, several page sizes, vs the oracle."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d = 2, 32, 8, 128
+    spec = streams.StreamSpec("peaked", seed=21)
+    st = ssa.Store(L, hq, hkv, d, page_size=page_size, num_pages=4096 // page_size * 4, dtype="bf16")
+    st.set_option(ssa.OPT_CTA_PAIR, 1)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=page_size, num_pages=4096 // page_size * 4)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 700)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    rsid, Oref = ref.session_create(700, Q, K, V)
+    ok, e = within(from_dev(O), Oref, "bf16")
+    assert ok, ("create", e)
+    tok = 700
+    for m in (256, 300, 37):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, tok, m)
+        O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        Oref, _ = ref.session_append(rsid, Q, K, V)
+        ok, e = within(from_dev(O), Oref, "bf16")
+        assert ok, (m, e)
+        tok += m
+    assert st.page_table(sid) == ref.page_table(rsid)
+    assert st.digest(sid) == ref.digest(rsid)
+    assert st.stats()["tc_pair_launches"] >= 3      # create + the 256/300-token appends used CTA pairs
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 32)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, ("query", e)
+
+
+def test_cta_pair_batch_and_needles(cuda):
+    """CTA pairs inside a varlen batch (appends + a stateless prompt + a query) and on the needle
+    stream (boundary keys must be retrieved exactly)."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 1, 32, 8, 128, 64
+    for stream_name in ("market", "needle"):
+        spec = streams.StreamSpec(stream_name, seed=22)
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=256, dtype="bf16")
+        st.set_option(ssa.OPT_CTA_PAIR, 1)
+        ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=256)
+        sids, rsids = [], []
+        for s, n in enumerate((1000, 2500)):
+            Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n, session=s)
+            sids.append(st.session_create(None, to_dev(K, cuda), to_dev(V, cuda)))
+            rsids.append(ref.session_create(n, Q, K, V, compute=False)[0])
+        parts, items, ritems, row = [], [], [], 0
+        for s, (kind, m, dom, tok0) in enumerate(((ssa.WORK_APPEND, 256, 0, 1000), (ssa.WORK_QUERY, 32, 1, 0))):
+            Q, K, V = gen_qkv(spec, L, hq, hkv, d, dom, tok0, m, session=s)
+            parts.append((Q, K, V))
+            items.append((kind, sids[s], m, row))
+            ritems.append({"kind": "append" if kind == ssa.WORK_APPEND else "query", "session": rsids[s],
+                           "Q": Q, "K": K, "V": V})
+            row += m
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 9, 0, 300, session=7)
+        parts.append((Q, K, V))
+        items.append((ssa.WORK_STATELESS, -1, 300, row))
+        ritems.append({"kind": "stateless", "session": -1, "Q": Q, "K": K, "V": V})
+        Qa, Ka, Va = (np.concatenate([p[i] for p in parts], axis=1) for i in range(3))
+        O = torch.empty(Qa.shape, dtype=torch.bfloat16, device=cuda)
+        st.stats(reset=True)
+        st.batch_run(items, to_dev(Qa, cuda), to_dev(Ka, cuda), to_dev(Va, cuda), O)
+        assert st.stats()["tc_pair_launches"] == 1
+        got = from_dev(O)
+        want = ref.batch_run(ritems)
+        for (kind, sid, m, row), w in zip(items, want):
+            ok, e = within(got[:, row:row + m], w, "bf16")
+            assert ok, (stream_name, kind, e)
