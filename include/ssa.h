@@ -160,6 +160,41 @@ ssa_status ssa_append_abort(ssa_store_t store, ssa_session_t session, int32_t ti
 ssa_status ssa_session_truncate(ssa_store_t store, ssa_session_t session, int64_t p,
                                 uint64_t *new_version);
 
+/* Region-1 FIFO eviction, K.evict_oldest(|tokens|) of Alg. 1: drop
+ * the n_tokens oldest retained Region-1 tokens (Region 0 is frozen, P:186;
+ * SPEC kv-store evict_oldest).  Positions of the remaining tokens are not
+ * re-based (R-8); they keep their order and the digest records their original
+ * positions.  Pages whose slots are all evicted leave the page table and
+ * return to the pool once no alias references them; the device page table is
+ * updated on `stream`.  version += 1 when n_tokens > 0.  Errors (no state
+ * change): SSA_ERR_INVALID_ARG if n_tokens < 0 or exceeds the retained
+ * Region-1 tokens; SSA_ERR_STATE with an append ticket open. */
+ssa_status ssa_session_evict_oldest(ssa_store_t store, ssa_session_t session, int64_t n_tokens,
+                                    void *stream, uint64_t *new_version);
+
+/* Retention window of Region 1 ("configurable retention"): with
+ * max_tokens > 0 every later append of m tokens (session_append, append_begin,
+ * batch APPEND items, load_kv) first evicts m oldest Region-1 tokens when
+ * n_tokens + m > max_tokens -- the guard of Alg. 1 L279-281.  The append
+ * fails with SSA_ERR_INVALID_ARG and no state change when fewer than m
+ * Region-1 tokens are retained.  0 disables the guard. */
+ssa_status ssa_session_set_retention(ssa_store_t store, ssa_session_t session, int64_t max_tokens);
+
+/* Metadata-only prefix aliasing (Eq. T_restore; SPEC
+ * kv-store alias_prefix): create a new session whose first len_tokens tokens
+ * are the donor's first len_tokens tokens, by reference.  Whole pages are
+ * shared (reference counted; a page returns to the pool when its last referer
+ * releases it); the one page that holds tokens past len_tokens, if any, is
+ * copied (one page per layer: constant in len_tokens), so appends to either
+ * session never disturb the other.  The new session's Region 0 is
+ * min(len_tokens, donor Region 0); version 0.  Requires 0 <= len_tokens <=
+ * donor n_tokens and, when len_tokens reaches into Region 1, a donor with no
+ * evictions (the prefix must be contiguous from the start).  Errors:
+ * SSA_ERR_UNKNOWN_SESSION, SSA_ERR_INVALID_ARG, SSA_ERR_SESSION_LIMIT,
+ * SSA_ERR_POOL_EXHAUSTED (no state change); copies are enqueued on `stream`. */
+ssa_status ssa_session_alias_prefix(ssa_store_t store, ssa_session_t donor, int64_t len_tokens,
+                                    void *stream, ssa_session_t *out);
+
 /* Destroy a session, returning its pages to the pool. */
 ssa_status ssa_session_destroy(ssa_store_t store, ssa_session_t session);
 
@@ -223,6 +258,8 @@ typedef struct {
     int64_t n_prefix;   /* Region 0 length */
     int64_t n_pages;    /* pages held (per layer) */
     uint64_t version;   /* data version t */
+    int64_t n_evicted;  /* Region-1 tokens evicted so far (positions are not re-based) */
+    int64_t retention;  /* Region-1 retention window (0 = unlimited) */
 } ssa_session_info;
 
 ssa_status ssa_session_get_info(ssa_store_t store, ssa_session_t session, ssa_session_info *out);

@@ -27,6 +27,7 @@ invariants, golden fixtures under ``tests/golden/``).
 from __future__ import annotations
 
 import ctypes
+import copy
 import heapq
 import math
 import os
@@ -215,6 +216,10 @@ class _Session:
     n_tokens: int = 0
     version: int = 0
     pages: list = field(default_factory=list)
+    pos: list = field(default_factory=list)   # original position of each retained token (never re-based)
+    r1_skip: int = 0        # evicted Region-1 slots at the head of the first retained R1 page
+    n_evicted: int = 0
+    retention: int = 0      # Region-1 retention window, 0 = unlimited
 
 
 class OracleStore:
@@ -227,6 +232,12 @@ class OracleStore:
     * flash_query_batch(f_1..f_k) — Eq. flash-eval P:406 for each f_i against K_t, each
                     seeing only the cache and its own tokens (reading R-4); no state change.
     * truncate(p) — SeqRemove(s, p, inf), P:438 / Alg. 3 L540.
+    * evict_oldest(n) — Alg. 1 L279-281 FIFO eviction of the n oldest Region-1 tokens
+                    (R0 frozen; SPEC kv-store evict_oldest); positions never re-based.
+    * set_retention(w) — the Alg. 1 guard: an append of m tokens that would exceed w first
+                    evicts m tokens.
+    * alias_prefix(donor, m) — metadata-only prefix sharing (SPEC alias_prefix):
+                    whole pages shared by reference count, the page holding token m-1 copied.
     * pages       — P-token pages, lowest free id first, R0 padded to a page boundary
                     (reading R-9); the page table is compared bit-exactly with the GPU store.
     """
@@ -239,25 +250,44 @@ class OracleStore:
         self.max_sessions = max_sessions
         self.free = list(range(num_pages))
         heapq.heapify(self.free)
+        self.ref = [0] * num_pages      # referers per page (aliases share pages)
         self.sessions: dict[int, _Session] = {}
         self.next_id = 0
 
     # -- page model (reading R-9) --------------------------------------------
-    def slots_for(self, n_prefix: int, n_tokens: int) -> int:
-        """Slots occupied by n_tokens tokens: R0 is padded to a page boundary."""
+    def slots_for(self, n_prefix: int, n_tokens: int, r1_skip: int = 0) -> int:
+        """Slots occupied by n_tokens retained tokens: R0 is padded to a page boundary,
+        and r1_skip evicted slots precede the first retained Region-1 token."""
         if n_tokens <= n_prefix:
             return n_tokens
         pad = -(-n_prefix // self.P) * self.P
-        return pad + (n_tokens - n_prefix)
+        return pad + r1_skip + (n_tokens - n_prefix)
 
-    def pages_for(self, n_prefix: int, n_tokens: int) -> int:
-        return -(-self.slots_for(n_prefix, n_tokens) // self.P)
+    def pages_for(self, n_prefix: int, n_tokens: int, r1_skip: int = 0) -> int:
+        return -(-self.slots_for(n_prefix, n_tokens, r1_skip) // self.P)
+
+    def _take_page(self) -> int:
+        pg = heapq.heappop(self.free)        # lowest free id first (reading R-9)
+        self.ref[pg] = 1
+        return pg
+
+    def _release(self, pages) -> None:
+        for pg in pages:
+            self.ref[pg] -= 1
+            if self.ref[pg] == 0:            # last referer gone (SPEC: deferred free)
+                heapq.heappush(self.free, pg)
 
     def _reserve(self, s: _Session, n_new: int) -> list:
-        need = self.pages_for(s.n_prefix, s.n_tokens + n_new) - len(s.pages)
+        need = self.pages_for(s.n_prefix, s.n_tokens + n_new, s.r1_skip) - len(s.pages)
         if need > len(self.free):
             raise OracleError("POOL_EXHAUSTED")
-        return [heapq.heappop(self.free) for _ in range(need)]
+        return [self._take_page() for _ in range(need)]
+
+    def _snapshot(self):
+        return copy.deepcopy((self.sessions, self.free, self.ref, self.next_id))
+
+    def _restore(self, snap):
+        self.sessions, self.free, self.ref, self.next_id = snap
 
     def occupancy(self):
         return self.num_pages - len(self.free), self.num_pages
@@ -288,6 +318,7 @@ class OracleStore:
         s = _Session(n_prefix=n_prefix)
         s.pages = []
         s.pages = self._reserve(s, n_prefix)
+        s.pos = list(range(n_prefix))
         sid = self.next_id
         self.next_id += 1
         O = self._compute(s, Q, K, V, -1) if compute else None
@@ -306,20 +337,103 @@ class OracleStore:
             outs.append(o)
         return np.stack(outs)
 
+    def _retention_evict(self, s: _Session, m: int) -> None:
+        """Alg. 1: if K.size() + |tokens| > K.capacity(): K.evict_oldest(|tokens|)."""
+        if s.retention > 0 and s.n_tokens + m > s.retention:
+            self._evict(s, m)
+
+    def _next_position(self, s: _Session) -> int:
+        return (s.pos[-1] + 1) if s.pos else 0
+
+    def _commit_append(self, s: _Session, new_pages, K, V) -> None:
+        m = K.shape[1]
+        p0 = self._next_position(s)
+        s.pages.extend(new_pages)
+        for l in range(self.L):
+            li = l if K.shape[0] == self.L else 0
+            s.k[l] = np.concatenate([s.k[l][:s.n_tokens], K[li]], axis=0)
+            s.v[l] = np.concatenate([s.v[l][:s.n_tokens], V[li]], axis=0)
+        s.pos = s.pos[:s.n_tokens] + list(range(p0, p0 + m))
+        s.n_tokens += m
+        s.version += 1
+
     def session_append(self, sid, Q, K, V, compute=True):
         s = self._check(sid)
         m = K.shape[1]
         if m <= 0:
             raise OracleError("INVALID_ARG")
-        new_pages = self._reserve(s, m)
+        snap = self._snapshot()
+        try:
+            self._retention_evict(s, m)
+            new_pages = self._reserve(s, m)
+        except OracleError:
+            self._restore(snap)                  # all-or-none
+            raise
         O = self._compute(s, Q, K, V, -1) if compute else None
-        s.pages.extend(new_pages)
-        for l in range(self.L):
-            s.k[l] = np.concatenate([s.k[l][:s.n_tokens], K[l]], axis=0)
-            s.v[l] = np.concatenate([s.v[l][:s.n_tokens], V[l]], axis=0)
-        s.n_tokens += m
-        s.version += 1
+        self._commit_append(s, new_pages, K, V)
         return O, s.version
+
+    # -- Region-1 retention (Alg. 1 L279-281) and prefix aliasing (P:565-571) --
+    def _evict(self, s: _Session, n: int) -> None:
+        if n < 0 or n > s.n_tokens - s.n_prefix:
+            raise OracleError("INVALID_ARG")     # SPEC: insufficient SLIDING tokens
+        if n == 0:
+            return
+        for l in range(self.L):                  # the n lowest-position Region-1 tokens leave
+            s.k[l] = np.concatenate([s.k[l][:s.n_prefix], s.k[l][s.n_prefix + n:s.n_tokens]], axis=0)
+            s.v[l] = np.concatenate([s.v[l][:s.n_prefix], s.v[l][s.n_prefix + n:s.n_tokens]], axis=0)
+        s.pos = s.pos[:s.n_prefix] + s.pos[s.n_prefix + n:s.n_tokens]
+        s.n_tokens -= n
+        s.n_evicted += n
+        s.r1_skip += n
+        r0_pages = -(-s.n_prefix // self.P)
+        if s.n_tokens == s.n_prefix:             # Region 1 empty: all its pages go
+            drop = len(s.pages) - r0_pages
+            s.r1_skip = 0
+        else:                                    # whole pages of evicted slots go
+            drop = s.r1_skip // self.P
+            s.r1_skip -= drop * self.P
+        gone = s.pages[r0_pages:r0_pages + drop]
+        s.pages = s.pages[:r0_pages] + s.pages[r0_pages + drop:]
+        self._release(gone)
+        s.version += 1
+
+    def evict_oldest(self, sid, n):
+        s = self._check(sid)
+        self._evict(s, n)
+        return s.version
+
+    def set_retention(self, sid, max_tokens):
+        if max_tokens < 0:
+            raise OracleError("INVALID_ARG")
+        self._check(sid).retention = max_tokens
+
+    def alias_prefix(self, donor, m):
+        """New session whose first m tokens are the donor's first m, shared by reference."""
+        d = self._check(donor)
+        if m < 0 or m > d.n_tokens or (m > d.n_prefix and d.n_evicted > 0):
+            raise OracleError("INVALID_ARG")
+        if len(self.sessions) >= self.max_sessions:
+            raise OracleError("SESSION_LIMIT")
+        end_slot = self.slots_for(d.n_prefix, m, d.r1_skip)
+        full = end_slot // self.P
+        if end_slot % self.P and not self.free:
+            raise OracleError("POOL_EXHAUSTED")
+        t = _Session(n_prefix=min(m, d.n_prefix))
+        t.pages = list(d.pages[:full])
+        for pg in t.pages:
+            self.ref[pg] += 1
+        if end_slot % self.P:
+            t.pages.append(self._take_page())   # the page holding token m-1 is a private copy
+        t.k = [np.array(d.k[l][:m]) for l in range(self.L)]
+        t.v = [np.array(d.v[l][:m]) for l in range(self.L)]
+        t.pos = list(d.pos[:m])
+        t.n_tokens = m
+        t.version = 1
+        sid = self.next_id
+        self.next_id += 1
+        self.sessions[sid] = t
+        return sid
 
     def session_query(self, sid, Q, K, V, layer=-1, tokens=None, heads=None):
         """Query plane: Q/K/V [L'][m][H][d] (L' = L, or 1 when layer >= 0). No state change."""
@@ -355,16 +469,18 @@ class OracleStore:
                 seen.add(it["session"])
                 self._check(it["session"])
         reserved = {}
-        for it in items:
-            if it["kind"] == "append":
-                s = self.sessions[it["session"]]
-                try:
+        snap = self._snapshot()
+        try:
+            for it in items:                     # retention evictions apply before any item runs
+                if it["kind"] == "append":
+                    self._retention_evict(self.sessions[it["session"]], it["K"].shape[1])
+            for it in items:
+                if it["kind"] == "append":
+                    s = self.sessions[it["session"]]
                     reserved[it["session"]] = self._reserve(s, it["K"].shape[1])
-                except OracleError:
-                    for pages in reserved.values():
-                        for p in pages:
-                            heapq.heappush(self.free, p)
-                    raise
+        except OracleError:
+            self._restore(snap)
+            raise
         outs = []
         for it in items:
             Q, K, V = it["Q"], it["K"], it["V"]
@@ -380,14 +496,7 @@ class OracleStore:
             for it in items:
                 if it["kind"] == "append":
                     s = self.sessions[it["session"]]
-                    s.pages.extend(reserved[it["session"]])
-                    K, V = it["K"], it["V"]
-                    for l in range(self.L):
-                        li = l if K.shape[0] == self.L else 0
-                        s.k[l] = np.concatenate([s.k[l][:s.n_tokens], K[li]], axis=0)
-                        s.v[l] = np.concatenate([s.v[l][:s.n_tokens], V[li]], axis=0)
-                    s.n_tokens += K.shape[1]
-                    s.version += 1
+                    self._commit_append(s, reserved[it["session"]], it["K"], it["V"])
         return outs
 
     def truncate(self, sid, p):
@@ -398,17 +507,18 @@ class OracleStore:
         if p == s.n_tokens:
             return s.version
         s.n_tokens = p
-        keep = self.pages_for(s.n_prefix, p)
-        for pg in s.pages[keep:]:
-            heapq.heappush(self.free, pg)
+        s.pos = s.pos[:p]
+        keep = self.pages_for(s.n_prefix, p, s.r1_skip)
+        self._release(s.pages[keep:])
         s.pages = s.pages[:keep]
+        if p == s.n_prefix:
+            s.r1_skip = 0
         s.version += 1
         return s.version
 
     def session_destroy(self, sid):
         s = self._check(sid)
-        for pg in s.pages:
-            heapq.heappush(self.free, pg)
+        self._release(s.pages)
         del self.sessions[sid]
 
     def page_table(self, sid):
@@ -416,16 +526,18 @@ class OracleStore:
 
     def info(self, sid):
         s = self._check(sid)
-        return dict(n_tokens=s.n_tokens, n_prefix=s.n_prefix, n_pages=len(s.pages), version=s.version)
+        return dict(n_tokens=s.n_tokens, n_prefix=s.n_prefix, n_pages=len(s.pages), version=s.version,
+                    n_evicted=s.n_evicted, retention=s.retention)
 
     def digest(self, sid) -> int:
         """FNV-1a-64 over, layer-major then token order, the records
-        int32 LE layer || int64 LE token || K bytes || V bytes."""
+        int32 LE layer || int64 LE position || K bytes || V bytes (SPEC S:158-166, S:177);
+        positions are the tokens' original ones (never re-based after eviction)."""
         s = self._check(sid)
-        return session_digest(s.k, s.v, s.n_tokens)
+        return session_digest(s.k, s.v, s.n_tokens, s.pos)
 
 
-def session_digest(k_layers, v_layers, n_tokens) -> int:
+def session_digest(k_layers, v_layers, n_tokens, positions=None) -> int:
     h = None
     for l, (K, V) in enumerate(zip(k_layers, v_layers)):
         K = np.ascontiguousarray(K[:n_tokens])
@@ -434,7 +546,8 @@ def session_digest(k_layers, v_layers, n_tokens) -> int:
         vb = V.reshape(n_tokens, -1).view(np.uint8)
         rec = np.empty((n_tokens, 12 + kb.shape[1] + vb.shape[1]), dtype=np.uint8)
         rec[:, 0:4] = np.frombuffer(np.int32(l).astype("<i4").tobytes(), dtype=np.uint8)
-        rec[:, 4:12] = np.arange(n_tokens, dtype="<i8").view(np.uint8).reshape(n_tokens, 8)
+        pos = np.arange(n_tokens, dtype="<i8") if positions is None else np.asarray(positions[:n_tokens], dtype="<i8")
+        rec[:, 4:12] = pos.view(np.uint8).reshape(n_tokens, 8)
         rec[:, 12:12 + kb.shape[1]] = kb
         rec[:, 12 + kb.shape[1]:] = vb
         h = fnv1a64(rec.tobytes(), h)

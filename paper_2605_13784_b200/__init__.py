@@ -50,7 +50,8 @@ class StoreConfig(ctypes.Structure):
 
 class SessionInfo(ctypes.Structure):
     _fields_ = [("n_tokens", ctypes.c_int64), ("n_prefix", ctypes.c_int64),
-                ("n_pages", ctypes.c_int64), ("version", ctypes.c_uint64)]
+                ("n_pages", ctypes.c_int64), ("version", ctypes.c_uint64),
+                ("n_evicted", ctypes.c_int64), ("retention", ctypes.c_int64)]
 
 
 class WorkItem(ctypes.Structure):
@@ -83,6 +84,10 @@ def _load():
         "ssa_append_abort": (i32, [vp, i32, i32]),
         "ssa_session_truncate": (i32, [vp, i32, i64, P(u64)]),
         "ssa_session_destroy": (i32, [vp, i32]),
+        "ssa_session_evict_oldest": (i32, [vp, i32, i64, vp, P(u64)]),
+        "ssa_session_set_retention": (i32, [vp, i32, i64]),
+        "ssa_session_alias_prefix": (i32, [vp, i32, i64, vp, P(i32)]),
+        "ssa_debug_trace": (i32, [vp, ctypes.c_size_t]),
         "ssa_session_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "ssa_flash_query_batch": (i32, [vp, i32, i32, i32, P(i32), vp, vp, vp, vp, vp]),
         "ssa_batch_run": (i32, [vp, i32, i32, P(WorkItem), vp, vp, vp, vp, vp]),
@@ -229,6 +234,23 @@ class Store:
         _check(lib.ssa_session_truncate(self._h, sid, p, ctypes.byref(ver)), "session_truncate")
         return ver.value
 
+    def evict_oldest(self, sid, n_tokens, stream=None):
+        """Region-1 FIFO eviction (Alg. 1); returns the new version."""
+        ver = ctypes.c_uint64()
+        _check(lib.ssa_session_evict_oldest(self._h, sid, n_tokens, _stream(stream), ctypes.byref(ver)),
+               "session_evict_oldest")
+        return ver.value
+
+    def set_retention(self, sid, max_tokens):
+        _check(lib.ssa_session_set_retention(self._h, sid, max_tokens), "session_set_retention")
+
+    def alias_prefix(self, donor, len_tokens, stream=None):
+        """Metadata-only prefix aliasing; returns the new session id."""
+        out = ctypes.c_int32()
+        _check(lib.ssa_session_alias_prefix(self._h, donor, len_tokens, _stream(stream), ctypes.byref(out)),
+               "session_alias_prefix")
+        return out.value
+
     def session_destroy(self, sid):
         _check(lib.ssa_session_destroy(self._h, sid), "session_destroy")
 
@@ -253,7 +275,8 @@ class Store:
     def info(self, sid):
         i = SessionInfo()
         _check(lib.ssa_session_get_info(self._h, sid, ctypes.byref(i)), "session_get_info")
-        return dict(n_tokens=i.n_tokens, n_prefix=i.n_prefix, n_pages=i.n_pages, version=i.version)
+        return dict(n_tokens=i.n_tokens, n_prefix=i.n_prefix, n_pages=i.n_pages, version=i.version,
+                    n_evicted=i.n_evicted, retention=i.retention)
 
     def page_table(self, sid):
         n = ctypes.c_int64()

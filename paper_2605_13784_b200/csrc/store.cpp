@@ -157,12 +157,14 @@ ssa_status ssa_store::drain_timing() {
 
 int64_t ssa_store::pad_prefix(int64_t n_prefix) const { return ceil_div64(n_prefix, cfg.page_size) * cfg.page_size; }
 
-// Slot of token t of a session (reading R-9: R0 padded to a page boundary).
+// Slot of retained token t of a session (reading R-9: R0 padded to a page
+// boundary; R-8: R1 tokens evicted from the front leave r1_skip empty slots
+// at the start of the first retained R1 page).
 int64_t ssa_store::slot_of(const Session& s, int64_t t) const {
-  return t < s.n_prefix ? t : pad_prefix(s.n_prefix) + (t - s.n_prefix);
+  return t < s.n_prefix ? t : pad_prefix(s.n_prefix) + s.r1_skip + (t - s.n_prefix);
 }
 int64_t ssa_store::slots_for(const Session& s, int64_t n) const {
-  return n <= s.n_prefix ? n : pad_prefix(s.n_prefix) + (n - s.n_prefix);
+  return n <= s.n_prefix ? n : pad_prefix(s.n_prefix) + s.r1_skip + (n - s.n_prefix);
 }
 int64_t ssa_store::pages_for(const Session& s, int64_t n) const {
   return ceil_div64(slots_for(s, n), cfg.page_size);
@@ -184,19 +186,112 @@ ssa_status ssa_store::reserve(Session& s, int64_t n_total, std::vector<int32_t>*
   }
   for (int64_t i = 0; i < need; ++i) {
     got->push_back(free_pages.top());
+    page_ref[free_pages.top()] = 1;
     free_pages.pop();
   }
   stats.pages_reserved += need;
   return SSA_OK;
 }
 
+// Drop one reference per page; a page returns to the free list when its last
+// referer (donor or alias, SPEC kv-store design decision) releases it.
 void ssa_store::release(const std::vector<int32_t>& pages) {
-  for (int32_t p : pages) free_pages.push(p);
+  for (int32_t p : pages)
+    if (--page_ref[p] == 0) free_pages.push(p);
+}
+
+// Re-upload the device page table from entry `from` (after entries shifted).
+ssa_status ssa_store::upload_pages_from(Session& s, int64_t from, cudaStream_t st) {
+  s.d_valid = std::min<int64_t>(s.d_valid, from);
+  std::vector<int32_t> none;
+  const int64_t n = (int64_t)s.pages.size();
+  if (s.d_valid >= n) return SSA_OK;
+  // push_pages uploads [min(old, d_valid), n) where old = n: i.e. [d_valid, n)
+  return push_pages(s, none, st, true);
+}
+
+// Region-1 FIFO eviction of the n oldest retained R1 tokens (Alg. 1
+// L279-281; R0 frozen).  Host metadata + page-table upload on `st`.
+ssa_status ssa_store::evict(Session& s, int64_t n, cudaStream_t st) {
+  if (n <= 0) return SSA_OK;
+  const int64_t P = cfg.page_size;
+  const int64_t r0_pages = pad_prefix(s.n_prefix) / P;
+  s.r1_skip += n;
+  s.n_tokens -= n;
+  s.n_evicted += n;
+  int64_t drop = s.r1_skip / P;
+  if (s.n_tokens == s.n_prefix) drop = (int64_t)s.pages.size() - r0_pages;   // R1 empty: release all its pages
+  std::vector<int32_t> gone(s.pages.begin() + r0_pages, s.pages.begin() + r0_pages + drop);
+  s.pages.erase(s.pages.begin() + r0_pages, s.pages.begin() + r0_pages + drop);
+  s.r1_skip = s.n_tokens == s.n_prefix ? 0 : s.r1_skip - drop * P;
+  release(gone);
+  s.version += 1;
+  return upload_pages_from(s, r0_pages, st);
+}
+
+// Pages the eviction of n R1 tokens would return to the free list (the
+// pages it drops that no alias still references).
+int64_t ssa_store::pages_freed_by_evict(const Session& s, int64_t n) const {
+  if (n <= 0) return 0;
+  const int64_t P = cfg.page_size;
+  const int64_t r0_pages = pad_prefix(s.n_prefix) / P;
+  int64_t drop = (s.r1_skip + n) / P;
+  if (s.n_tokens - n == s.n_prefix) drop = (int64_t)s.pages.size() - r0_pages;
+  int64_t freed = 0;
+  for (int64_t i = 0; i < drop; ++i) freed += page_ref[s.pages[r0_pages + i]] == 1;
+  return freed;
+}
+
+// The retention guard of Alg. 1: if the session would exceed its
+// retention, evict |tokens| oldest R1 tokens first.  Computes, without
+// changing state, how many tokens that evicts, how many new pages the append
+// then needs and how many pages the eviction returns to the free list.
+ssa_status ssa_store::retention_plan(const Session& s, int64_t n_new, int64_t* n_evict, int64_t* need_pages,
+                                     int64_t* freed_pages) const {
+  *n_evict = 0;
+  if (s.retention > 0 && s.n_tokens + n_new > s.retention) {
+    if (n_new > s.n_tokens - s.n_prefix) {
+      set_error("retention: %lld new tokens but only %lld evictable Region-1 tokens", (long long)n_new,
+                (long long)(s.n_tokens - s.n_prefix));
+      return SSA_ERR_INVALID_ARG;
+    }
+    *n_evict = n_new;
+  }
+  Session after = s;
+  after.pages.clear();
+  const int64_t P = cfg.page_size;
+  const int64_t r0_pages = pad_prefix(s.n_prefix) / P;
+  int64_t drop = 0;
+  if (*n_evict > 0) {
+    drop = (s.r1_skip + *n_evict) / P;
+    after.r1_skip = s.r1_skip + *n_evict - drop * P;
+    after.n_tokens = s.n_tokens - *n_evict;
+    if (after.n_tokens == s.n_prefix) {
+      drop = (int64_t)s.pages.size() - r0_pages;
+      after.r1_skip = 0;
+    }
+  }
+  *need_pages = std::max<int64_t>(0, pages_for(after, after.n_tokens + n_new) - ((int64_t)s.pages.size() - drop));
+  *freed_pages = pages_freed_by_evict(s, *n_evict);
+  return SSA_OK;
+}
+
+// Apply the retention guard before an append of n_new tokens: all-or-none
+// (fails without state change if the eviction or the append cannot happen).
+ssa_status ssa_store::evict_for_append(Session& s, int64_t n_new, cudaStream_t st) {
+  int64_t n_ev = 0, need = 0, freed = 0;
+  ssa_status rc = retention_plan(s, n_new, &n_ev, &need, &freed);
+  if (rc != SSA_OK) return rc;
+  if (need > (int64_t)free_pages.size() + freed) {
+    set_error("pool exhausted: need %lld pages, %zu free", (long long)need, free_pages.size());
+    return SSA_ERR_POOL_EXHAUSTED;
+  }
+  return n_ev ? evict(s, n_ev, st) : SSA_OK;
 }
 
 // Append page ids to the session's host table and upload the delta.
-ssa_status ssa_store::push_pages(Session& s, const std::vector<int32_t>& pages, cudaStream_t st) {
-  if (pages.empty()) return SSA_OK;
+ssa_status ssa_store::push_pages(Session& s, const std::vector<int32_t>& pages, cudaStream_t st, bool force) {
+  if (pages.empty() && !force) return SSA_OK;
   const int64_t old = (int64_t)s.pages.size();
   s.pages.insert(s.pages.end(), pages.begin(), pages.end());
   const int64_t n = (int64_t)s.pages.size();
@@ -227,8 +322,9 @@ ssa_status ssa_store::push_pages(Session& s, const std::vector<int32_t>& pages, 
 void ssa_store::fill_cached(const Session& s, SegDesc* sg) const {
   sg->n_slots = (int32_t)slots_for(s, s.n_tokens);
   if (s.n_tokens > s.n_prefix) {
+    // one hole: R0's page pad and the evicted head of the first R1 page
     sg->hole_lo = (int32_t)s.n_prefix;
-    sg->hole_hi = (int32_t)pad_prefix(s.n_prefix);
+    sg->hole_hi = (int32_t)(pad_prefix(s.n_prefix) + s.r1_skip);
   } else {
     sg->hole_lo = sg->hole_hi = 0;
   }
@@ -601,6 +697,7 @@ ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
     return SSA_ERR_CUDA;
   }
   for (int64_t p = 0; p < cfg->num_pages; ++p) st->free_pages.push((int32_t)p);
+  st->page_ref.assign(cfg->num_pages, 0);
   st->sessions.reserve(std::min(cfg->max_sessions, 4096));
   *out = st;
   return SSA_OK;
@@ -679,8 +776,9 @@ static ssa_status do_append(ssa_store* st, Session& s, int32_t n_new, const void
                             const void* V, void* O, cudaStream_t stream) {
   const int L = st->cfg.num_layers;
   std::vector<int32_t> got;
-  ssa_status rc = st->reserve(s, s.n_tokens + n_new, &got);
+  ssa_status rc = st->evict_for_append(s, n_new, stream);
   if (rc != SSA_OK) return rc;
+  if ((rc = st->reserve(s, s.n_tokens + n_new, &got)) != SSA_OK) return rc;
   IoSet io;
   io.q = {Q, tensor_bytes(st, L, n_new, st->cfg.num_q_heads)};
   io.k = {K, tensor_bytes(st, L, n_new, st->cfg.num_kv_heads)};
@@ -769,8 +867,9 @@ ssa_status ssa_append_begin(ssa_store_t st, ssa_session_t id, int32_t n_new, int
   if (s->ticket_open) { set_error("append_begin: ticket already open"); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
   std::vector<int32_t> got;
-  ssa_status rc = st->reserve(*s, s->n_tokens + n_new, &got);
+  ssa_status rc = st->evict_for_append(*s, n_new, nullptr);
   if (rc != SSA_OK) return rc;
+  if ((rc = st->reserve(*s, s->n_tokens + n_new, &got)) != SSA_OK) return rc;
   const size_t before = s->pages.size();
   if ((rc = st->push_pages(*s, got, nullptr)) != SSA_OK) return rc;
   s->ticket_open = true;
@@ -863,9 +962,107 @@ ssa_status ssa_session_truncate(ssa_store_t st, ssa_session_t id, int64_t p, uin
     s->d_valid = std::min<int64_t>(s->d_valid, keep);
     st->release(back);
     s->n_tokens = p;
+    if (p == s->n_prefix) s->r1_skip = 0;   // Region 1 empty: its layout restarts at the R0 pad
     s->version += 1;
   }
   if (new_version) *new_version = s->version;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_evict_oldest(ssa_store_t st, ssa_session_t id, int64_t n, void* stream,
+                                    uint64_t* new_version) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (s->ticket_open) return SSA_ERR_STATE;
+  if (n < 0 || n > s->n_tokens - s->n_prefix) {
+    set_error("evict_oldest: n=%lld but %lld Region-1 tokens retained", (long long)n,
+              (long long)(s->n_tokens - s->n_prefix));
+    return SSA_ERR_INVALID_ARG;
+  }
+  cudaSetDevice(st->cfg.device);
+  ssa_status rc = st->evict(*s, n, (cudaStream_t)stream);
+  if (rc == SSA_OK && new_version) *new_version = s->version;
+  return rc;
+}
+
+ssa_status ssa_session_set_retention(ssa_store_t st, ssa_session_t id, int64_t max_tokens) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (max_tokens < 0) return SSA_ERR_INVALID_ARG;
+  s->retention = max_tokens;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_alias_prefix(ssa_store_t st, ssa_session_t donor_id, int64_t len, void* stream,
+                                    ssa_session_t* out) {
+  SSA_CHECK_STORE(st);
+  Session* d = st->get(donor_id);
+  if (!d) { set_error("unknown session %d", donor_id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (!out || len < 0 || len > d->n_tokens || (len > d->n_prefix && d->n_evicted > 0)) {
+    set_error("alias_prefix: len=%lld invalid for a donor of %lld tokens (%lld evicted)", (long long)len,
+              (long long)d->n_tokens, (long long)d->n_evicted);
+    return SSA_ERR_INVALID_ARG;
+  }
+  if (d->ticket_open) return SSA_ERR_STATE;
+  cudaSetDevice(st->cfg.device);
+  const int64_t P = st->cfg.page_size;
+  const int64_t end_slot = st->slots_for(*d, len);
+  const int64_t full = end_slot / P;                 // pages shared whole
+  const bool partial = (end_slot % P) != 0;          // the page holding token len-1 is copied
+  if (partial && st->free_pages.empty()) {
+    set_error("alias_prefix: pool exhausted");
+    return SSA_ERR_POOL_EXHAUSTED;
+  }
+  int live = 0;
+  int32_t id = -1;
+  for (int i = 0; i < (int)st->sessions.size(); ++i) {
+    if (st->sessions[i].live) live++;
+    else if (id < 0) id = i;
+  }
+  if (live >= st->cfg.max_sessions) {
+    set_error("session limit %d reached", st->cfg.max_sessions);
+    return SSA_ERR_SESSION_LIMIT;
+  }
+  if (id < 0) {
+    id = (int32_t)st->sessions.size();
+    st->sessions.emplace_back();
+    d = st->get(donor_id);   // the vector may have moved
+  }
+  Session& s = st->sessions[id];
+  int32_t* keep_d = s.d_pages;
+  int64_t keep_cap = s.d_cap;
+  s = Session();
+  s.d_pages = keep_d;
+  s.d_cap = keep_cap;
+  s.d_valid = 0;
+  s.live = true;
+  s.n_prefix = std::min(len, d->n_prefix);
+  s.n_tokens = len;
+  s.version = 1;
+  std::vector<int32_t> pages(d->pages.begin(), d->pages.begin() + full);
+  for (int32_t pg : pages) st->page_ref[pg]++;
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (partial) {
+    const int32_t dst = st->free_pages.top();   // lowest free id (R-9)
+    st->free_pages.pop();
+    st->page_ref[dst] = 1;
+    st->stats.pages_reserved += 1;
+    const int32_t src = d->pages[full];
+    // one page = [Hkv][P][d] contiguous per layer; layers are num_pages pages apart
+    const size_t blk = (size_t)st->cfg.num_kv_heads * P * st->cfg.head_dim * st->elem;
+    const size_t pitch = blk * (size_t)st->cfg.num_pages;
+    for (void* pool : {st->poolK, st->poolV}) {
+      char* b = static_cast<char*>(pool);
+      SSA_CUDA(st, cudaMemcpy2DAsync(b + (size_t)dst * blk, pitch, b + (size_t)src * blk, pitch, blk,
+                                     st->cfg.num_layers, cudaMemcpyDeviceToDevice, cs));
+    }
+    pages.push_back(dst);
+  }
+  ssa_status rc = st->push_pages(s, pages, cs, true);
+  if (rc != SSA_OK) return rc;
+  *out = id;
   return SSA_OK;
 }
 
@@ -969,6 +1166,27 @@ ssa_status ssa_batch_run(ssa_store_t st, int32_t layer, int32_t n_items, const s
   // Reserve pages for every APPEND item, in item order, all-or-none (R-7).
   ssa_status rc = SSA_OK;
   if (layer <= 0) {
+    // Retention guard for every APPEND item (Alg. 1), checked for the
+    // whole batch before any state changes: evictions, then reservations.
+    {
+      int64_t need = 0, freed = 0;
+      std::vector<std::pair<Session*, int64_t>> ev;
+      for (int i = 0; i < n_items; ++i) {
+        if (items[i].kind != SSA_WORK_APPEND) continue;
+        Session* s = st->get(items[i].session);
+        int64_t n_ev = 0, nd = 0, fr = 0;
+        if ((rc = st->retention_plan(*s, items[i].n_tokens, &n_ev, &nd, &fr)) != SSA_OK) return rc;
+        need += nd;
+        freed += fr;
+        if (n_ev) ev.push_back({s, n_ev});
+      }
+      if (need > (int64_t)st->free_pages.size() + freed) {
+        set_error("batch_run: pool exhausted (need %lld pages)", (long long)need);
+        return SSA_ERR_POOL_EXHAUSTED;
+      }
+      for (auto& e : ev)
+        if ((rc = st->evict(*e.first, e.second, cs)) != SSA_OK) return rc;
+    }
     std::vector<std::pair<Session*, std::vector<int32_t>>> res;
     for (int i = 0; i < n_items; ++i) {
       if (items[i].kind != SSA_WORK_APPEND) continue;
@@ -1045,6 +1263,8 @@ ssa_status ssa_session_get_info(ssa_store_t st, ssa_session_t id, ssa_session_in
   out->n_prefix = s->n_prefix;
   out->n_pages = (int64_t)s->pages.size();
   out->version = s->version;
+  out->n_evicted = s->n_evicted;
+  out->retention = s->retention;
   return SSA_OK;
 }
 
@@ -1095,7 +1315,7 @@ ssa_status ssa_session_read_kv(ssa_store_t st, ssa_session_t id, int32_t layer, 
   gp.start = start;
   gp.count = count;
   gp.n_prefix = s->n_prefix;
-  gp.n_prefix_slots_pad = (int32_t)st->pad_prefix(s->n_prefix);
+  gp.n_prefix_slots_pad = (int32_t)(st->pad_prefix(s->n_prefix) + s->r1_skip);
   gp.pages = s->d_pages;
   SSA_CUDA(st, cudaDeviceSynchronize());
   SSA_CUDA(st, launch_gather(gp, nullptr));
@@ -1144,8 +1364,9 @@ ssa_status ssa_session_digest(ssa_store_t st, ssa_session_t id, uint64_t* out) {
     for (int64_t t = 0; t < n; ++t) {
       uint8_t hdr[12];
       const int32_t l32 = l;
+      const int64_t pos = t < s->n_prefix ? t : t + s->n_evicted;   // positions never re-based (R-8)
       memcpy(hdr, &l32, 4);       // little-endian host (x86-64)
-      memcpy(hdr + 4, &t, 8);
+      memcpy(hdr + 4, &pos, 8);
       h = fnv1a(hdr, 12, h);
       h = fnv1a(k.data() + t * row, row, h);
       h = fnv1a(v.data() + t * row, row, h);

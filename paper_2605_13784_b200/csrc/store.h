@@ -21,6 +21,12 @@ struct Session {
   int64_t n_prefix = 0;   // Region 0 length
   int64_t n_tokens = 0;   // retained tokens (R0 + R1)
   uint64_t version = 0;   // data version t
+  // Region-1 FIFO eviction (Alg. 1): evicted R1 slots at the start of
+  // the first retained R1 page (0..P-1; whole evicted pages leave the table),
+  // total evicted tokens (positions are never re-based) and the retention cap.
+  int64_t r1_skip = 0;
+  int64_t n_evicted = 0;
+  int64_t retention = 0;  // 0 = unlimited
   std::vector<int32_t> pages;   // host page table: slot / P -> page id
   int32_t* d_pages = nullptr;   // device mirror
   int64_t d_cap = 0;
@@ -82,6 +88,7 @@ struct ssa_store {
   size_t pool_half_bytes = 0;
   std::vector<ssa::Session> sessions;
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_pages;
+  std::vector<int32_t> page_ref;   // referers per page (aliased prefixes share pages)
   bool failed = false;
   std::string fail_msg;
   ssa::UploadRing ring;
@@ -123,7 +130,13 @@ struct ssa_store {
   ssa::Session* get(ssa_session_t id);
   ssa_status reserve(ssa::Session& s, int64_t n_total, std::vector<int32_t>* got);
   void release(const std::vector<int32_t>& pages);
-  ssa_status push_pages(ssa::Session& s, const std::vector<int32_t>& pages, cudaStream_t st);
+  ssa_status push_pages(ssa::Session& s, const std::vector<int32_t>& pages, cudaStream_t st, bool force = false);
+  ssa_status upload_pages_from(ssa::Session& s, int64_t from, cudaStream_t st);
+  ssa_status evict(ssa::Session& s, int64_t n, cudaStream_t st);
+  ssa_status evict_for_append(ssa::Session& s, int64_t n_new, cudaStream_t st);
+  int64_t pages_freed_by_evict(const ssa::Session& s, int64_t n) const;
+  ssa_status retention_plan(const ssa::Session& s, int64_t n_new, int64_t* n_evict, int64_t* need_pages,
+                            int64_t* freed_pages) const;
   void fill_cached(const ssa::Session& s, ssa::SegDesc* sg) const;
   ssa_status ensure_scratch(size_t part_o_floats, size_t part_lse_floats, cudaStream_t st);
   ssa_status stage_inputs(ssa::IoSet* io, cudaStream_t st);

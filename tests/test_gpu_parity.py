@@ -529,3 +529,105 @@ def test_cta_pair_batch_and_needles(cuda):
         for (kind, sid, m, row), w in zip(items, want):
             ok, e = within(got[:, row:row + m], w, "bf16")
             assert ok, (stream_name, kind, e)
+
+
+@pytest.mark.parametrize("page_size", [16, 64])
+def test_retention_eviction_parity(cuda, page_size):
+    """Region-1 FIFO eviction (Alg. 1) through the retention guard and explicit
+    evict_oldest: attention over the retained keys, page tables (evicted pages leave, hole at
+    the head of the first R1 page) and digests (original positions) match the oracle."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d = 2, 32, 8, 128
+    spec = streams.StreamSpec("peaked", seed=31)
+    st = ssa.Store(L, hq, hkv, d, page_size=page_size, num_pages=8192 // page_size, dtype="bf16")
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=page_size, num_pages=8192 // page_size)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 100)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    rsid, _ = ref.session_create(100, Q, K, V)
+    st.set_retention(sid, 700)
+    ref.set_retention(rsid, 700)
+    tok = 100
+    for m in (300, 256, 200, 37, 129):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, tok, m)
+        O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        Oref, _ = ref.session_append(rsid, Q, K, V)
+        ok, e = within(from_dev(O), Oref, "bf16")
+        assert ok, (m, e)
+        assert st.page_table(sid) == ref.page_table(rsid), m
+        assert st.info(sid) == ref.info(rsid), m
+        tok += m
+    assert st.info(sid)["n_evicted"] > 0
+    st.evict_oldest(sid, 51)
+    ref.evict_oldest(rsid, 51)
+    assert st.page_table(sid) == ref.page_table(rsid)
+    assert st.digest(sid) == ref.digest(rsid)
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 33)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, ("query", e)
+    n_keep = ref.info(rsid)["n_tokens"]
+    Kb, Vb = st.read_kv(sid, 1, 0, n_keep)
+    assert np.array_equal(Kb, ref.sessions[rsid].k[1][:n_keep]) and np.array_equal(Vb, ref.sessions[rsid].v[1][:n_keep])
+    assert st.occupancy() == ref.occupancy()
+    # an append larger than the evictable Region 1 fails without state change
+    digest = st.digest(sid)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, tok, 800)
+    with pytest.raises(ssa.SsaError):
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda))
+    assert st.digest(sid) == digest and st.page_table(sid) == ref.page_table(rsid)
+
+
+def test_alias_prefix_parity(cuda):
+    """Metadata-only prefix aliasing: whole pages shared by reference, the page
+    holding token m-1 copied; independent appends on donor and alias, deferred free."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    spec = streams.StreamSpec("market", seed=32)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=256, dtype="bf16")
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=256)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 100)
+    sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    rsid, _ = ref.session_create(100, Q, K, V, compute=False)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 100, 900)
+    st.session_append(sid, None, to_dev(K, cuda), to_dev(V, cuda))
+    ref.session_append(rsid, Q, K, V, compute=False)
+    tids = {}
+    for m in (1000, 640, 57):
+        tids[m] = (st.alias_prefix(sid, m), ref.alias_prefix(rsid, m))
+        g, r = tids[m]
+        assert st.page_table(g) == ref.page_table(r), m
+        assert st.digest(g) == ref.digest(r), m
+        assert st.info(g) == ref.info(r), m
+        assert st.occupancy() == ref.occupancy(), m
+    # independent continuations: target 1000 and the donor
+    g, r = tids[1000]
+    for who, (gs, rs), dom in (("alias", (g, r), 5), ("donor", (sid, rsid), 6)):
+        Q, K, V = gen_qkv(spec, L, hq, hkv, d, dom, 0, 77)
+        O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_append(gs, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        Oref, _ = ref.session_append(rs, Q, K, V)
+        ok, e = within(from_dev(O), Oref, "bf16")
+        assert ok, (who, e)
+        assert st.page_table(gs) == ref.page_table(rs)
+    assert st.digest(tids[640][0]) == ref.digest(tids[640][1])   # untouched by the others' appends
+    # deferred free: destroying the donor keeps the shared pages alive for the aliases
+    st.session_destroy(sid)
+    ref.session_destroy(rsid)
+    assert st.occupancy() == ref.occupancy()
+    g, r = tids[640]
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 32)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(g, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(r, Qq, Kq, Vq), "bf16")
+    assert ok, e
+    # a new session reuses freed pages only; the aliases still read their own data
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 300, session=9)
+    n2 = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    r2, _ = ref.session_create(300, Q, K, V, compute=False)
+    assert st.page_table(n2) == ref.page_table(r2)
+    assert st.digest(g) == ref.digest(r)
