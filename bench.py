@@ -316,6 +316,73 @@ def leg_multitenant(torch, dev, stream, peaks, steps, warmup):
             "tokens_per_s": (24 * 256 + 24 * 32 + 4 * 1024) / (ms * 1e-3)}
 
 
+def leg_stateful_vs_recompute(torch, dev, stream, peaks, steps, warmup):
+    """SURVEY §8(d) in-repo speedup analogue of E1 / Table 1, attention
+    only: a 32-token query against the session's cache (stateful, Alg. 2) vs re-prefilling
+    [S; D_1..D_k; q] from scratch as one causal prompt (request-driven), same kernels,
+    Llama-3-8B attention shapes, 32 layers.  Context: the paper's end-to-end 2.4-5.9x is
+    on L40S with the whole model."""
+    import streams
+    import paper_2605_13784_b200 as ssa
+    L, hq, hkv, d, P = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"], CFG["P"]
+    out = {"workload": "one market session; 32-token query vs full causal re-prefill of n+32 tokens, 32 layers"}
+    for n in (2600, 14800, 32768):
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=n // P + 16, max_sessions=2, dtype="bf16")
+        spec = streams.StreamSpec("market", seed=7)
+        sid = build_session_n(st, torch, dev, spec, n)
+        q, k, v = gen_new(torch, dev, spec, 1, 0, CFG["q_len"])
+        o = torch.empty_like(q)
+        t_q = _timed(torch, stream, lambda: st.session_query(sid, q, k, v, o, stream=stream), steps, warmup)
+        # request-driven: the same n + 32 tokens as one stateless prompt (causal prefill from scratch)
+        Qc = torch.cat([gen_new(torch, dev, spec, 0, 0, n)[0], q], dim=1).contiguous()
+        Kc = torch.cat([torch.stack([streams.gen_tensor_torch(spec, 0, 0, l, streams.TENSOR_K, 0, n, hkv, d,
+                                                              device=dev) for l in range(L)]), k], dim=1).contiguous()
+        Vc = torch.cat([torch.stack([streams.gen_tensor_torch(spec, 0, 0, l, streams.TENSOR_V, 0, n, hkv, d,
+                                                              device=dev) for l in range(L)]), v], dim=1).contiguous()
+        Oc = torch.empty_like(Qc)
+        items = [(ssa.WORK_STATELESS, -1, n + CFG["q_len"], 0)]
+        t_r = _timed(torch, stream, lambda: st.batch_run(items, Qc, Kc, Vc, Oc, stream=stream), max(1, steps // 2), 1)
+        out[f"n{n}"] = {"stateful_query_ms": t_q, "recompute_ms": t_r, "speedup": t_r / t_q}
+        del Qc, Kc, Vc, Oc
+        st.close()
+        torch.cuda.empty_cache()
+    return out
+
+
+def leg_greedy_sample(torch, dev, stream, peaks, steps, warmup):
+    """on-device greedy sampling + logit gap (Eq. logit-gap
+    P:454-457) over a Llama-3 vocabulary (128,256 logits/row, fp32): one row (a decode step)
+    and 64 rows (the answers of a 64-question Flash Query batch).  HBM-bound: one read."""
+    import paper_2605_13784_b200 as ssa
+    vocab = 128256
+    st = ssa.Store(1, 4, 4, 64, page_size=16, num_pages=4, dtype="fp32")
+    out = {"workload": "argmax + logit gap over 128,256 fp32 logits per row (Llama-3 vocabulary)"}
+    for rows in (1, 64):
+        # >= 2 x L2 of logits, rotated, so every call reads HBM
+        n_buf = max(2, int(2 * 126e6 // (rows * vocab * 4)) + 1)
+        bufs = [torch.randn(rows, vocab, device=dev) for _ in range(n_buf)]
+        ids = torch.empty(rows, dtype=torch.int32, device=dev)
+        gap = torch.empty(rows, dtype=torch.float32, device=dev)
+        reps = 8 * n_buf
+        # one CUDA graph of `reps` launches (the per-call ctypes cost would otherwise
+        # dominate a microsecond kernel); scratch is allocated by the warm-up call
+        gs = torch.cuda.Stream(device=dev)
+        st.greedy_sample(bufs[0], ids, gap, stream=gs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for r in range(reps):
+                st.greedy_sample(bufs[r % n_buf], ids, gap, stream=gs)
+        ms = _timed(torch, stream, graph.replay, steps, warmup) / reps
+        nb = rows * vocab * 4
+        out[f"rows{rows}"] = {"us": ms * 1e3, "gbs": nb / (ms * 1e-3) / 1e9,
+                              "hbm_frac": nb / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+        del bufs
+    st.close()
+    out["paper_context"] = "host sync + scan costs 0.5-1 ms per token on server GPUs (P:383)"
+    return out
+
+
 def leg_split128k(torch, dev, stream, peaks, steps, warmup):
     """BJ.configs[4] at N=1: one 131,072-token session, 1-token and 32-token queries over 32 layers."""
     import streams
@@ -500,6 +567,12 @@ def run_ours(args):
     if world == 1 and "tenant" in want:
         guarded("multi_tenant", lambda: leg_multitenant(torch, dev, stream, peaks_l, 3, 1))
         torch.cuda.empty_cache()
+    if world == 1 and "argmax" in want:
+        guarded("greedy_sample", lambda: leg_greedy_sample(torch, dev, stream, peaks_l, 3, 1))
+        torch.cuda.empty_cache()
+    if world == 1 and "speedup" in want:
+        guarded("stateful_vs_recompute", lambda: leg_stateful_vs_recompute(torch, dev, stream, peaks_l, 3, 1))
+        torch.cuda.empty_cache()
     if "split" in want:
         if world == 1:
             guarded("split_kv_128k", lambda: leg_split128k(torch, dev, stream, peaks_l, 3, 1))
@@ -577,7 +650,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--legs", default="flash,tenant,split",
+    ap.add_argument("--legs", default="flash,tenant,speedup,argmax,split",
                     help="extra single-GPU legs (configs 3-5) reported in the same JSON line; '' to skip")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -251,6 +251,25 @@ ssa_status ssa_batch_run(ssa_store_t store, int32_t layer, int32_t n_items,
                          const void *V, void *O, void *stream);
 
 /* ----------------------------------------------------------------------------
+ * On-device greedy sampling
+ * -------------------------------------------------------------------------- */
+/* For each of n_rows rows of `vocab` logits (dtype SSA_FP32 or SSA_BF16, row r
+ * at logits + r * row_stride elements): out_ids[r] = argmax with ties broken
+ * toward the lowest id (SPEC greedy_sample), out_gap[r] = l1 - l2 computed in
+ * fp32, the logit gap of Eq. flash-cache / Eq. logit-gap
+ * (P:454-457), where l2 is the second-highest VALUE (equal to l1 when the top
+ * value occurs twice, so the gap is 0), and optionally out_top2[2r..2r+1] =
+ * (l1, l2).  NaN logits are ignored; a row with no non-NaN logit gives id -1
+ * and gap 0.  With `draft` (n_rows proposed ids) *out_n_accept = the number of
+ * leading rows whose argmax equals the draft (the batched speculative check of
+ * P:385).  All pointers are device pointers; out_gap, out_top2, draft may be
+ * NULL.  One launch on `stream`, one read of the logits (HBM-bound); the
+ * store provides scratch.  Errors: SSA_ERR_INVALID_ARG. */
+ssa_status ssa_greedy_sample(ssa_store_t store, ssa_dtype dtype, int32_t n_rows, int32_t vocab,
+                             int64_t row_stride, const void *logits, int32_t *out_ids, float *out_gap,
+                             float *out_top2, const int32_t *draft, int32_t *out_n_accept, void *stream);
+
+/* ----------------------------------------------------------------------------
  * Introspection (tests, not hot path)
  * -------------------------------------------------------------------------- */
 typedef struct {

@@ -556,6 +556,33 @@ def session_digest(k_layers, v_layers, n_tokens, positions=None) -> int:
     return h
 
 
+def greedy_sample(logits: np.ndarray):
+    """Greedy sampling of P:383-385 with the logit gap of Eq. flash-cache and
+    Eq. logit-gap, per SPEC greedy_sample: for each row, the argmax with ties
+    toward the lowest token id and gap = l1 - l2, l2 the second-highest value (== l1 on a
+    tie at the top).  Rows are fp32 values or bf16 bits (uint16, decoded exactly); the gap
+    is one fp32 subtraction, as the device computes it.  NaN logits are ignored; a row
+    without a non-NaN logit gives (-1, 0).  Returns (ids int32 [rows], gap float32 [rows])."""
+    x = logits
+    if x.dtype == np.uint16:
+        x = (x.astype(np.uint32) << 16).view(np.float32)
+    x = np.asarray(x, dtype=np.float32)
+    ids = np.empty(x.shape[0], dtype=np.int32)
+    gap = np.empty(x.shape[0], dtype=np.float32)
+    for r in range(x.shape[0]):
+        keep = np.flatnonzero(~np.isnan(x[r]))
+        if keep.size == 0:
+            ids[r], gap[r] = -1, 0.0
+            continue
+        vals = x[r][keep]
+        j = int(np.argmax(vals))                 # first occurrence = lowest id among ties
+        l1 = vals[j]
+        l2 = np.sort(vals)[-2] if vals.size > 1 else np.float32(-np.inf)
+        ids[r] = keep[j]
+        gap[r] = np.float32(l1) - np.float32(l2)
+    return ids, gap
+
+
 def memory_model_bytes(num_layers, d, n_ctx, sizeof) -> int:
     """Eq. (memory) P:778-781: M_KV = 2 * L * d * n_ctx * sizeof(dtype)."""
     return 2 * num_layers * d * n_ctx * sizeof

@@ -88,6 +88,7 @@ def _load():
         "ssa_session_set_retention": (i32, [vp, i32, i64]),
         "ssa_session_alias_prefix": (i32, [vp, i32, i64, vp, P(i32)]),
         "ssa_debug_trace": (i32, [vp, ctypes.c_size_t]),
+        "ssa_greedy_sample": (i32, [vp, i32, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp]),
         "ssa_session_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "ssa_flash_query_batch": (i32, [vp, i32, i32, i32, P(i32), vp, vp, vp, vp, vp]),
         "ssa_batch_run": (i32, [vp, i32, i32, P(WorkItem), vp, vp, vp, vp, vp]),
@@ -250,6 +251,19 @@ class Store:
         _check(lib.ssa_session_alias_prefix(self._h, donor, len_tokens, _stream(stream), ctypes.byref(out)),
                "session_alias_prefix")
         return out.value
+
+    def greedy_sample(self, logits, out_ids, out_gap=None, out_top2=None, draft=None, out_n_accept=None,
+                      stream=None):
+        """On-device greedy sampling: per row argmax (lowest id on ties) and logit
+        gap l1 - l2 (Eq. logit-gap); optional draft-window acceptance.  `logits` is a
+        2-D torch tensor (fp32 or bf16, rows contiguous); outputs are device tensors."""
+        import torch
+        if logits.dim() != 2 or logits.stride(1) != 1:
+            raise ValueError("logits must be [rows][vocab] with unit column stride")
+        dt = {torch.float32: FP32, torch.bfloat16: BF16}[logits.dtype]
+        _check(lib.ssa_greedy_sample(self._h, dt, logits.shape[0], logits.shape[1], logits.stride(0), logits.data_ptr(),
+                                     _ptr(out_ids), _ptr(out_gap), _ptr(out_top2), _ptr(draft), _ptr(out_n_accept),
+                                     _stream(stream)), "greedy_sample")
 
     def session_destroy(self, sid):
         _check(lib.ssa_session_destroy(self._h, sid), "session_destroy")

@@ -145,11 +145,29 @@ struct CombineParams {
   int32_t write_o;
 };
 
+// On-device greedy sampling (kernels_sample.cu).
+struct SampleParams {
+  const void* logits;      // [n_rows][row_stride] fp32 or bf16
+  int64_t row_stride;      // elements
+  int32_t vocab;
+  int32_t n_rows;
+  int32_t splits;          // CTAs per row
+  void* partials;          // [n_rows][splits] reduction triples (scratch)
+  int32_t* row_counters;   // [n_rows + 1], zero between calls
+  int32_t* out_ids;        // [n_rows] device
+  float* out_gap;          // [n_rows] device or null
+  float* out_top;          // [n_rows][2] (l1, l2) device or null
+  const int32_t* draft;    // [n_rows] device or null
+  int32_t* out_n_accept;   // device, used when draft != null
+};
+
 // Kernel launchers (kernels_*.cu).  Return cudaGetLastError() after launch.
 cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits);
 cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
 cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
+cudaError_t launch_greedy(const SampleParams& p, bool bf16, cudaStream_t s);
+size_t sample_partial_bytes();
 // Merge `world` rank partials (packed chunks [O fp32 rows*Hq*D | lse rows*Hq]) into O.
 cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
                                cudaStream_t s);

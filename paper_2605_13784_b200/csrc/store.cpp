@@ -715,6 +715,8 @@ ssa_store::~ssa_store() {
   if (part_lse) cudaFree(part_lse);
   if (stage) cudaFree(stage);
   if (counters) cudaFree(counters);
+  if (sample_part) cudaFree(sample_part);
+  if (sample_cnt) cudaFree(sample_cnt);
   destroy_comm();
 }
 
@@ -1338,6 +1340,55 @@ ssa_status ssa_session_load_kv(ssa_store_t st, ssa_session_t id, int64_t count, 
   if (s->ticket_open) return SSA_ERR_STATE;
   cudaSetDevice(st->cfg.device);
   return do_append(st, *s, (int32_t)count, nullptr, K, V, nullptr, (cudaStream_t)stream);
+}
+
+// ---- on-device greedy sampling
+ssa_status ssa_greedy_sample(ssa_store_t st, ssa_dtype dtype, int32_t n_rows, int32_t vocab, int64_t row_stride,
+                             const void* logits, int32_t* out_ids, float* out_gap, float* out_top2,
+                             const int32_t* draft, int32_t* out_n_accept, void* stream) {
+  SSA_CHECK_STORE(st);
+  if (n_rows <= 0 || n_rows > 65535 || vocab <= 0 || row_stride < vocab || !logits || !out_ids ||
+      (dtype != SSA_FP32 && dtype != SSA_BF16) || (draft && !out_n_accept)) {
+    set_error("greedy_sample: invalid arguments");
+    return SSA_ERR_INVALID_ARG;
+  }
+  cudaSetDevice(st->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  // about four CTAs per SM over all rows, at least 4096 logits per CTA
+  int splits = std::max(1, (4 * st->num_sms + n_rows - 1) / n_rows);
+  splits = std::min(splits, std::max(1, vocab / 4096));
+  const size_t part = (size_t)n_rows * splits * sample_partial_bytes();
+  if (part > st->sample_part_cap) {
+    SSA_CUDA(st, cudaDeviceSynchronize());
+    if (st->sample_part) cudaFree(st->sample_part);
+    st->sample_part = nullptr;
+    st->sample_part_cap = std::max(part, 2 * st->sample_part_cap);
+    SSA_CUDA(st, cudaMalloc(&st->sample_part, st->sample_part_cap));
+  }
+  if ((size_t)n_rows + 1 > st->sample_cnt_cap) {
+    SSA_CUDA(st, cudaDeviceSynchronize());
+    if (st->sample_cnt) cudaFree(st->sample_cnt);
+    st->sample_cnt = nullptr;
+    st->sample_cnt_cap = std::max<size_t>(n_rows + 1, 2 * st->sample_cnt_cap);
+    SSA_CUDA(st, cudaMalloc(&st->sample_cnt, st->sample_cnt_cap * sizeof(int32_t)));
+    SSA_CUDA(st, cudaMemset(st->sample_cnt, 0, st->sample_cnt_cap * sizeof(int32_t)));
+  }
+  SampleParams sp{};
+  sp.logits = logits;
+  sp.row_stride = row_stride;
+  sp.vocab = vocab;
+  sp.n_rows = n_rows;
+  sp.splits = splits;
+  sp.partials = st->sample_part;
+  sp.row_counters = st->sample_cnt;
+  sp.out_ids = out_ids;
+  sp.out_gap = out_gap;
+  sp.out_top = out_top2;
+  sp.draft = draft;
+  sp.out_n_accept = out_n_accept;
+  SSA_CUDA(st, launch_greedy(sp, dtype == SSA_BF16, cs));
+  st->stats.kernel_launches++;
+  return SSA_OK;
 }
 
 // FNV-1a 64 over the session's records (library's own implementation; the

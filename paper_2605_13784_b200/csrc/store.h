@@ -99,6 +99,10 @@ struct ssa_store {
   void* stage = nullptr;
   size_t stage_cap = 0;
   int32_t* counters = nullptr;   // fused-merge group counters (zero between launches)
+  void* sample_part = nullptr;   // greedy sampling: per-(row, split) partials
+  size_t sample_part_cap = 0;
+  int32_t* sample_cnt = nullptr; // per-row tickets (zero between launches)
+  size_t sample_cnt_cap = 0;
   size_t counters_cap = 0;
   int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0, opt_fused_merge = 0;
 #ifndef SSA_CTA_PAIR_DEFAULT

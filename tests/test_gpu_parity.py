@@ -631,3 +631,46 @@ def test_alias_prefix_parity(cuda):
     r2, _ = ref.session_create(300, Q, K, V, compute=False)
     assert st.page_table(n2) == ref.page_table(r2)
     assert st.digest(g) == ref.digest(r)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("rows,vocab,stride", [(1, 128256, 128256), (7, 128256, 128256), (64, 128256, 128264),
+                                               (5, 1, 1), (3, 33, 35), (9, 4097, 4097), (4, 1001, 1003)])
+def test_greedy_sample_parity(cuda, dtype, rows, vocab, stride):
+    """On-device greedy sampling: argmax ids bit-exact (ties toward the lowest id,
+    including ties planted across the kernel's split boundaries), logit gap bit-exact (one fp32
+    subtraction on both sides), NaN ignored, strided / unaligned rows."""
+    import torch
+    ssa = _ssa()
+    st = ssa.Store(1, 4, 4, 64, page_size=16, num_pages=4, dtype="fp32")
+    rng = np.random.default_rng(rows * 1000 + vocab)
+    x = rng.standard_normal((rows, stride)).astype(np.float32) * 4
+    for r in range(rows):
+        top = float(x[r, :vocab].max()) + 1.0
+        for j in rng.choice(vocab, size=min(vocab, 1 + r % 3), replace=False):   # planted ties
+            x[r, j] = top
+        if vocab > 8 and r % 2:
+            x[r, rng.integers(0, vocab)] = np.nan
+    if vocab > 4096:
+        x[0, [4095, 4096]] = x[0, :vocab].max() + 2.0                              # tie across a split edge
+    if dtype == "bf16":
+        xb = oracle_bits = (x.view(np.uint32) >> 16).astype(np.uint16)              # truncate to bf16 bits
+        dev = torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).to(cuda)
+        want_ids, want_gap = oracle.greedy_sample(oracle_bits[:, :vocab])
+    else:
+        dev = torch.from_numpy(x).to(cuda)
+        want_ids, want_gap = oracle.greedy_sample(x[:, :vocab])
+    logits = dev[:, :vocab]
+    ids = torch.empty(rows, dtype=torch.int32, device=cuda)
+    gap = torch.empty(rows, dtype=torch.float32, device=cuda)
+    draft = torch.from_numpy(want_ids.copy()).to(cuda)
+    if rows > 2:
+        draft[rows // 2] += 1                                                        # first mismatch
+    n_acc = torch.zeros(1, dtype=torch.int32, device=cuda)
+    for _ in range(2):                                                               # counters reset between calls
+        st.greedy_sample(logits, ids, gap, draft=draft, out_n_accept=n_acc)
+        got_ids, got_gap = ids.cpu().numpy(), gap.cpu().numpy()
+        assert np.array_equal(got_ids, want_ids)
+        assert np.array_equal(got_gap.view(np.uint32), want_gap.view(np.uint32))
+        assert int(n_acc.item()) == (rows // 2 if rows > 2 else rows)
+    st.close()

@@ -395,3 +395,39 @@ def test_batch_snapshot_semantics():
         ref = oracle.full_recompute(Q[l, :5], K[l, :5], V[l, :5], 2, oracle.default_scale(8))
         assert np.max(np.abs(outs[2][l] - ref)) <= 1e-12
     assert a.digest(sid) == b.digest(sid2) and a.page_table(sid) == b.page_table(sid2)
+
+
+# --------------------------------------------------------------------------- greedy sampling
+def test_greedy_sample_spec_examples():
+    """SPEC greedy_sample examples (Eq. logit-gap)."""
+    ids, gap = oracle.greedy_sample(np.array([[0.5, 0.5, 0.1]], dtype=np.float32))
+    assert ids[0] == 0 and gap[0] == 0.0                         # tie toward the lowest id, gap 0
+    ids, gap = oracle.greedy_sample(np.array([[0.3, 3.1, -1.0, 0.9]], dtype=np.float32))
+    assert ids[0] == 1 and gap[0] == np.float32(3.1) - np.float32(0.9)   # "top 3.1, second 0.9 -> 2.2"
+    assert abs(float(gap[0]) - 2.2) < 1e-6
+    hot = np.zeros((1, 97), dtype=np.float32)
+    hot[0, 41] = 1.75
+    ids, gap = oracle.greedy_sample(hot)
+    assert ids[0] == 41 and gap[0] == 1.75                       # one-hot: (k, hot - 0)
+
+
+def test_greedy_sample_brute_force_and_invariance():
+    rng = np.random.default_rng(5)
+    x = rng.integers(-3, 4, size=(40, 23)).astype(np.float32)    # many ties
+    ids, gap = oracle.greedy_sample(x)
+    for r in range(x.shape[0]):
+        row = [float(v) for v in x[r]]
+        best = max(row)
+        assert ids[r] == row.index(best)                         # first index of the max
+        rest = sorted(row)[:-1]
+        assert gap[r] == best - rest[-1]
+    ids2, _ = oracle.greedy_sample(x + np.float32(1000.0))       # argmax invariance (SPEC)
+    assert np.array_equal(ids, ids2)
+    y = x.copy()
+    y[:, 0] = np.nan                                             # NaNs are ignored
+    ids3, _ = oracle.greedy_sample(y)
+    for r in range(y.shape[0]):
+        vals = [float(v) if j else -np.inf for j, v in enumerate(x[r])]
+        assert ids3[r] == vals.index(max(vals))
+    ids4, gap4 = oracle.greedy_sample(np.full((1, 5), np.nan, dtype=np.float32))
+    assert ids4[0] == -1 and gap4[0] == 0.0
