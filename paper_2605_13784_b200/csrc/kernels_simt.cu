@@ -184,27 +184,33 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
 // w_s = 2^(lse_s - L) / sum_s 2^(lse_s - L) are computed once into smem, then
 // the 128-bit-vectorized weighted sum runs over all (row, 4-column) pairs.
 // Partials carry normalized o_s and lse_s in log2 units (reading R-11).
+constexpr int kCombineRows = 32;   // rows of a group per combine CTA
+
 template <typename T>
 __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
-  extern __shared__ float wsm[];                       // [n_splits][rows_tile]
-  const int g = blockIdx.x, ly = blockIdx.y;
+  extern __shared__ float wsm[];                       // [n_splits][kCombineRows]
+  const int g = blockIdx.x, ly = blockIdx.y, r0 = blockIdx.z * kCombineRows;
   const Group gr = p.groups[g];
-  const SegDesc sg = p.segs[gr.seg];
   const int rows = gr.q_ntok * p.G;
+  if (r0 >= rows) return;
+  const int nr = min(kCombineRows, rows - r0);
+  const SegDesc sg = p.segs[gr.seg];
   const int RT = p.rows_tile;
   const int64_t slot0 = (int64_t)ly * p.n_units + gr.unit0;
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+  const int NS = gr.n_splits;
+  for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+    const int r = r0 + rr;
     float L = -CUDART_INF_F;
-    for (int s = 0; s < gr.n_splits; ++s) L = fmaxf(L, p.part_lse[(slot0 + s) * RT + r]);
+    for (int s = 0; s < NS; ++s) L = fmaxf(L, p.part_lse[(slot0 + s) * RT + r]);
     float wsum = 0.f;
-    for (int s = 0; s < gr.n_splits; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const float ls = p.part_lse[(slot0 + s) * RT + r];
       const float w = ls == -CUDART_INF_F ? 0.f : exp2f(ls - L);
-      wsm[s * RT + r] = w;
+      wsm[s * kCombineRows + rr] = w;
       wsum += w;
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-    for (int s = 0; s < gr.n_splits; ++s) wsm[s * RT + r] *= inv;
+    for (int s = 0; s < NS; ++s) wsm[s * kCombineRows + rr] *= inv;
     if (p.lse_out) {
       const int64_t row = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0 + gr.q_tok0 + r / p.G;
       p.lse_out[row * p.Hq + gr.kv_head * p.G + r % p.G] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
@@ -214,12 +220,28 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
   if (!p.write_o) return;
   const int64_t in_row0 = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0;
   const int d4 = p.D / 4;
-  for (int idx = threadIdx.x; idx < rows * d4; idx += blockDim.x) {
-    const int r = idx / d4, e = (idx % d4) * 4;
+  for (int idx = threadIdx.x; idx < nr * d4; idx += blockDim.x) {
+    const int rr = idx / d4, r = r0 + rr, e = (idx % d4) * 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < gr.n_splits; ++s) {
-      const float w = wsm[s * RT + r];
-      const float4 v = *reinterpret_cast<const float4*>(p.part_o + ((slot0 + s) * RT + r) * p.D + e);
+    const float4* src = reinterpret_cast<const float4*>(p.part_o + ((slot0)*RT + r) * p.D + e);
+    const int64_t split_stride4 = (int64_t)RT * p.D / 4;   // float4s between consecutive splits
+    int s = 0;
+    for (; s + 4 <= NS; s += 4) {   // four independent loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (s + u) * split_stride4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float w = wsm[(s + u) * kCombineRows + rr];
+        acc.x = fmaf(w, v[u].x, acc.x);
+        acc.y = fmaf(w, v[u].y, acc.y);
+        acc.z = fmaf(w, v[u].z, acc.z);
+        acc.w = fmaf(w, v[u].w, acc.w);
+      }
+    }
+    for (; s < NS; ++s) {
+      const float w = wsm[s * kCombineRows + rr];
+      const float4 v = __ldcs(src + s * split_stride4);
       acc.x = fmaf(w, v.x, acc.x);
       acc.y = fmaf(w, v.y, acc.y);
       acc.z = fmaf(w, v.z, acc.z);
@@ -362,8 +384,8 @@ cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaS
 
 cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits) {
   if (p.n_groups == 0 || n_layers == 0) return cudaSuccess;
-  dim3 grid(p.n_groups, n_layers);
-  const size_t smem = sizeof(float) * (size_t)max_splits * p.rows_tile;
+  dim3 grid(p.n_groups, n_layers, (p.rows_tile + kCombineRows - 1) / kCombineRows);
+  const size_t smem = sizeof(float) * (size_t)max_splits * kCombineRows;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(bf16 ? (const void*)combine_kernel<__nv_bfloat16> : (const void*)combine_kernel<float>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
