@@ -64,7 +64,7 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
       if (n > max_splits) { ok = false; break; }
       for (int64_t s = 0; s < n; ++s) {
         const int64_t t = it.tiles * (s + 1) / n - it.tiles * s / n;
-        unit_cost.push_back((double)t + c.unit_overhead_tiles + (n > 1 ? 1.0 : 0.0));
+        unit_cost.push_back((double)t + c.unit_overhead_tiles + (n > 1 ? c.split_overhead_tiles : 0.0));
       }
     }
     if (!ok) continue;

@@ -16,6 +16,7 @@ struct PlanConfig {
   int max_splits = 0;        // 0 = unlimited
   int min_tiles_per_unit = 1;
   double unit_overhead_tiles = 1.0;
+  double split_overhead_tiles = 1.0;   // extra cost of a split unit (partial write + merge), in tiles
   int fault = 0;
   bool force_groups = false;  // every item writes partials (sharded query)
   bool pair_slots = false;    // units run in two-slot (tcgen05) CTAs: avoid lone units

@@ -157,6 +157,13 @@ ssa_status ssa_store::drain_timing() {
 
 int64_t ssa_store::pad_prefix(int64_t n_prefix) const { return ceil_div64(n_prefix, cfg.page_size) * cfg.page_size; }
 
+// Planner cost of a split tcgen05 unit beyond its tiles (the partial write,
+// the merge, and the CTA prologue a longer unit would amortise), in K/V tiles.
+#ifndef SSA_TC_SPLIT_OVERHEAD
+#define SSA_TC_SPLIT_OVERHEAD 4.0
+#endif
+static constexpr double kTcSplitOverheadTiles = SSA_TC_SPLIT_OVERHEAD;
+
 // Slot of retained token t of a session (reading R-9: R0 padded to a page
 // boundary; R-8: R1 tokens evicted from the front leave r1_skip empty slots
 // at the start of the first retained R1 page).
@@ -420,6 +427,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     pc.max_splits = (int)opt_max_splits;
     pc.min_tiles_per_unit = use_tc ? 2 : 2;
     pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
+    pc.split_overhead_tiles = use_tc ? kTcSplitOverheadTiles : 1.0;
     pc.fault = (int)opt_fault;
     pc.force_groups = opts.force_groups;
     pc.pair_slots = use_tc;
@@ -1447,6 +1455,11 @@ int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_
   pc.ctas_per_sm = ctas_per_sm;
   pc.max_splits = max_splits;
   pc.pair_slots = key_tile == tc_key_tile();   // the tcgen05 key tile selects two-slot CTAs
+  if (pc.pair_slots) {                          // mirror run()'s tcgen05 cost model
+    pc.min_tiles_per_unit = 2;
+    pc.unit_overhead_tiles = 2.0;
+    pc.split_overhead_tiles = kTcSplitOverheadTiles;
+  }
   Plan plan;
   plan_units(segs, pc, &plan);
   const int32_t n = (int32_t)plan.units.size();
