@@ -434,8 +434,14 @@ def leg_split128k_sharded(torch, dev, stream, peaks, steps, warmup, world, rank)
         else:
             st.load_kv(sid, K, V)
         tok += m
-    init_comm(st)
-    out = {"workload": f"BJ.configs[4]: n=131,072 split over {world} GPUs, queries over 32 layers, NCCL all-gather"}
+    p2p = os.environ.get("SSA_BENCH_P2P") == "1"
+    if p2p:   # A9 over peer memory (validated on one GPU only; opt-in)
+        from paper_2605_13784_b200.sharding import attach_symmetric, chunk_floats
+        keep = attach_symmetric(st, chunk_floats(32, L, hq, d))  # noqa: F841
+    else:
+        init_comm(st)
+    out = {"workload": f"BJ.configs[4]: n=131,072 split over {world} GPUs, queries over 32 layers, "
+                       + ("peer-memory push + flag merge" if p2p else "NCCL all-gather")}
     for qn in (1, 32):
         q, k, v = gen_new(torch, dev, spec, 1, 0, qn)
         o = torch.empty_like(q)

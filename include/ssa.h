@@ -377,6 +377,24 @@ ssa_status ssa_sharded_query(ssa_store_t store, ssa_session_t session, int32_t l
 
 ssa_status ssa_comm_destroy(ssa_store_t store);
 
+/* A9 over peer memory instead of NCCL: the rank partial is pushed straight
+ * into every rank's gathered buffer by the kernel that produces it (NVLink
+ * P2P stores from the split-KV combine epilogue), a system-scope release of a
+ * per-rank epoch flag follows on the same stream, and each rank's merge waits
+ * (acquire) for all flags of the epoch -- no collective launch, no staging copy.
+ * peer_bufs[q] / peer_flags[q] (host arrays of `world` device addresses valid
+ * in this process, e.g. from torch symmetric memory) are rank q's gathered
+ * buffer ([world][chunk] fp32, buf_bytes each, chunk = rows*Hq*(D+1) as in
+ * ssa_sharded_partial) and its uint32 flag array [world] (zero-initialised,
+ * epochs increase by one per push).  Replaces any NCCL communicator.  After
+ * attaching, ssa_sharded_query = ssa_sharded_push + ssa_sharded_merge.
+ * Errors: SSA_ERR_INVALID_ARG (null / out-of-range), SSA_ERR_STATE (not attached). */
+ssa_status ssa_comm_attach_peers(ssa_store_t store, int32_t rank, int32_t world, const uint64_t *peer_bufs,
+                                 const uint64_t *peer_flags, size_t buf_bytes);
+ssa_status ssa_sharded_push(ssa_store_t store, ssa_session_t session, int32_t layer, int32_t n_q,
+                            const void *Q, const void *K, const void *V, void *stream);
+ssa_status ssa_sharded_merge(ssa_store_t store, int32_t layer, int32_t n_q, void *O, void *stream);
+
 /* Building blocks of ssa_sharded_query, usable without NCCL.
  * ssa_sharded_partial: the rank partial of the n_q query rows over this
  * store's shard of the session (include_tail != 0: this rank also covers the

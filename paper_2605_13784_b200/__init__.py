@@ -104,6 +104,9 @@ def _load():
         "ssa_comm_init": (i32, [vp, i32, i32, P(ctypes.c_uint8)]),
         "ssa_sharded_query": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "ssa_comm_destroy": (i32, [vp]),
+        "ssa_comm_attach_peers": (i32, [vp, i32, i32, P(u64), P(u64), ctypes.c_size_t]),
+        "ssa_sharded_push": (i32, [vp, i32, i32, i32, vp, vp, vp, vp]),
+        "ssa_sharded_merge": (i32, [vp, i32, i32, vp, vp]),
         "ssa_sharded_partial": (i32, [vp, i32, i32, i32, vp, vp, vp, i32, vp, vp]),
         "ssa_merge_rank_partials": (i32, [vp, i32, i64, vp, vp, vp]),
         "ssa_status_str": (ctypes.c_char_p, [i32]),
@@ -356,6 +359,21 @@ class Store:
     def merge_rank_partials(self, world, rows, parts, O, stream=None):
         _check(lib.ssa_merge_rank_partials(self._h, world, rows, _ptr(parts), _ptr(O), _stream(stream)),
                "merge_rank_partials")
+
+    def comm_attach_peers(self, rank, world, peer_bufs, peer_flags, buf_bytes):
+        """A9 over peer memory (no NCCL): peer_bufs / peer_flags are `world` device addresses."""
+        pb = (ctypes.c_uint64 * world)(*[int(x) for x in peer_bufs])
+        pf = (ctypes.c_uint64 * world)(*[int(x) for x in peer_flags])
+        _check(lib.ssa_comm_attach_peers(self._h, rank, world, pb, pf, buf_bytes), "comm_attach_peers")
+
+    def sharded_push(self, sid, Q, K, V, layer=-1, stream=None, n_q=None):
+        n = n_q if n_q is not None else _ntok(Q)
+        _check(lib.ssa_sharded_push(self._h, sid, layer, n, _ptr(Q), _ptr(K), _ptr(V), _stream(stream)),
+               "sharded_push")
+
+    def sharded_merge(self, O, layer=-1, stream=None, n_q=None):
+        n = n_q if n_q is not None else _ntok(O)
+        _check(lib.ssa_sharded_merge(self._h, layer, n, _ptr(O), _stream(stream)), "sharded_merge")
 
     def comm_destroy(self):
         _check(lib.ssa_comm_destroy(self._h), "comm_destroy")

@@ -73,12 +73,23 @@ struct CommState {
   int rank = 0, world = 1;
   float* buf = nullptr;     // [send chunk | world gathered chunks]
   size_t cap = 0;           // floats
+  // peer-memory path (ssa_comm_attach_peers): every rank's gathered buffer
+  // [world][chunk] floats and flag array [world] uint32, mapped in this process
+  bool peers = false;
+  std::vector<uint64_t> peer_buf, peer_flag;
+  size_t peer_bytes = 0;
+  uint64_t* d_peer_flag = nullptr;   // device copy of peer_flag
+  uint64_t* d_peer_chunk = nullptr;  // device: this rank's chunk slot in every peer buffer
+  int64_t chunk_for = -1;            // chunk size d_peer_chunk was built for
+  uint32_t epoch = 0;
 };
 
 void ssa_store::destroy_comm() {
   if (!comm) return;
   if (comm->comm && nccl().comm_destroy) nccl().comm_destroy(comm->comm);
   if (comm->buf) cudaFree(comm->buf);
+  if (comm->d_peer_flag) cudaFree(comm->d_peer_flag);
+  if (comm->d_peer_chunk) cudaFree(comm->d_peer_chunk);
   delete comm;
   comm = nullptr;
 }
@@ -183,11 +194,110 @@ ssa_status ssa_merge_rank_partials(ssa_store_t st, int32_t world, int64_t rows, 
   return st->unstage_output(&io, cs);
 }
 
+ssa_status ssa_comm_attach_peers(ssa_store_t st, int32_t rank, int32_t world, const uint64_t* peer_bufs,
+                                 const uint64_t* peer_flags, size_t buf_bytes) {
+  ssa_status rc = check_store(st);
+  if (rc != SSA_OK) return rc;
+  if (world <= 0 || rank < 0 || rank >= world || !peer_bufs || !peer_flags || buf_bytes == 0) return SSA_ERR_INVALID_ARG;
+  for (int q = 0; q < world; ++q)
+    if (!peer_bufs[q] || !peer_flags[q]) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  st->destroy_comm();
+  CommState* c = new CommState();
+  c->rank = rank;
+  c->world = world;
+  c->peers = true;
+  c->peer_buf.assign(peer_bufs, peer_bufs + world);
+  c->peer_flag.assign(peer_flags, peer_flags + world);
+  c->peer_bytes = buf_bytes;
+  st->comm = c;
+  COMM_CUDA(st, cudaMalloc(&c->d_peer_flag, world * sizeof(uint64_t)));
+  COMM_CUDA(st, cudaMalloc(&c->d_peer_chunk, world * sizeof(uint64_t)));
+  COMM_CUDA(st, cudaMemcpy(c->d_peer_flag, peer_flags, world * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  return SSA_OK;
+}
+
+ssa_status ssa_sharded_push(ssa_store_t st, ssa_session_t id, int32_t layer, int32_t n_q, const void* Q,
+                            const void* K, const void* V, void* stream) {
+  ssa_status rc = check_store(st);
+  if (rc != SSA_OK) return rc;
+  CommState* c = st->comm;
+  if (!c || !c->peers) { set_error("sharded_push: ssa_comm_attach_peers first"); return SSA_ERR_STATE; }
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (n_q <= 0 || !Q || !K || !V || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;
+  const int64_t rows = Lin * n_q;
+  const int64_t chunk = rows * st->cfg.num_q_heads * (int64_t)(st->cfg.head_dim + 1);
+  if ((size_t)(c->world * chunk) * sizeof(float) > c->peer_bytes) {
+    set_error("sharded_push: peer buffers hold %zu bytes, need %lld", c->peer_bytes,
+              (long long)(c->world * chunk * (int64_t)sizeof(float)));
+    return SSA_ERR_INVALID_ARG;
+  }
+  if (c->chunk_for != chunk) {   // this rank's chunk slot in every peer's gathered buffer
+    std::vector<uint64_t> slot(c->world);
+    for (int q = 0; q < c->world; ++q) slot[q] = c->peer_buf[q] + (uint64_t)c->rank * chunk * sizeof(float);
+    COMM_CUDA(st, cudaMemcpyAsync(c->d_peer_chunk, slot.data(), c->world * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                  cs));
+    COMM_CUDA(st, cudaStreamSynchronize(cs));
+    c->chunk_for = chunk;
+  }
+  const size_t el = st->elem;
+  IoSet io;
+  io.q = {Q, (size_t)rows * st->cfg.num_q_heads * st->cfg.head_dim * el};
+  io.k = {K, (size_t)rows * st->cfg.num_kv_heads * st->cfg.head_dim * el};
+  io.v = {V, (size_t)rows * st->cfg.num_kv_heads * st->cfg.head_dim * el};
+  if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
+  SegDesc sg{};
+  sg.row0 = 0;
+  sg.m = n_q;
+  sg.tail_m = c->rank == c->world - 1 ? n_q : 0;   // the tail owner (R-12)
+  st->fill_cached(*s, &sg);
+  sg.append_slot0 = -1;
+  std::vector<SegDesc> segs{sg};
+  RunOpts opts;
+  opts.force_groups = true;
+  opts.peer_chunk = c->d_peer_chunk;
+  opts.n_peers = c->world;
+  opts.lse_off = rows * st->cfg.num_q_heads * (int64_t)st->cfg.head_dim;
+  if ((rc = st->run(segs, io, n_q, layer < 0 ? 0 : layer, (int32_t)Lin, 1, true, true, cs, opts)) != SSA_OK) return rc;
+  c->epoch += 1;
+  COMM_CUDA(st, launch_signal_peers(c->d_peer_flag, c->world, c->rank, c->epoch, cs));
+  st->stats.kernel_launches++;
+  return SSA_OK;
+}
+
+ssa_status ssa_sharded_merge(ssa_store_t st, int32_t layer, int32_t n_q, void* O, void* stream) {
+  ssa_status rc = check_store(st);
+  if (rc != SSA_OK) return rc;
+  CommState* c = st->comm;
+  if (!c || !c->peers) { set_error("sharded_merge: ssa_comm_attach_peers first"); return SSA_ERR_STATE; }
+  if (n_q <= 0 || !O || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int64_t rows = (layer < 0 ? st->cfg.num_layers : 1) * (int64_t)n_q;
+  IoSet io;
+  io.o = {O, (size_t)rows * st->cfg.num_q_heads * st->cfg.head_dim * st->elem};
+  if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
+  const float* gathered = reinterpret_cast<const float*>(c->peer_buf[c->rank]);
+  const uint32_t* flags = reinterpret_cast<const uint32_t*>(c->peer_flag[c->rank]);
+  COMM_CUDA(st, launch_merge_ranks(gathered, c->world, rows, st->cfg.num_q_heads, st->cfg.head_dim, io.o.dev,
+                                   st->cfg.dtype == SSA_BF16, cs, flags, c->epoch));
+  st->stats.kernel_launches++;
+  return st->unstage_output(&io, cs);
+}
+
 ssa_status ssa_sharded_query(ssa_store_t st, ssa_session_t id, int32_t layer, int32_t n_q, const void* Q,
                              const void* K, const void* V, void* O, void* stream) {
   ssa_status rc = check_store(st);
   if (rc != SSA_OK) return rc;
-  if (!st->comm) { set_error("sharded_query: ssa_comm_init first"); return SSA_ERR_STATE; }
+  if (!st->comm) { set_error("sharded_query: ssa_comm_init or ssa_comm_attach_peers first"); return SSA_ERR_STATE; }
+  if (st->comm->peers) {
+    if ((rc = ssa_sharded_push(st, id, layer, n_q, Q, K, V, stream)) != SSA_OK) return rc;
+    return ssa_sharded_merge(st, layer, n_q, O, stream);
+  }
   if (n_q <= 0 || !O || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
   CommState* c = st->comm;

@@ -211,9 +211,15 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
     for (int s = 0; s < NS; ++s) wsm[s * kCombineRows + rr] *= inv;
-    if (p.lse_out) {
+    if (p.lse_out || p.n_peers > 0) {
       const int64_t row = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0 + gr.q_tok0 + r / p.G;
-      p.lse_out[row * p.Hq + gr.kv_head * p.G + r % p.G] = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+      const float lse = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
+      const int64_t at = row * p.Hq + gr.kv_head * p.G + r % p.G;
+      if (p.n_peers > 0) {
+        for (int q = 0; q < p.n_peers; ++q) reinterpret_cast<float*>(p.peer_chunk[q])[p.lse_off + at] = lse;
+      } else {
+        p.lse_out[at] = lse;
+      }
     }
   }
   __syncthreads();
@@ -249,7 +255,11 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
     }
     const int64_t row = in_row0 + gr.q_tok0 + r / p.G;
     const int h = gr.kv_head * p.G + r % p.G;
-    if (p.o_f32) {
+    if (p.n_peers > 0) {
+      // the rank partial goes straight into every peer's gathered buffer
+      for (int q = 0; q < p.n_peers; ++q)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.peer_chunk[q]) + (row * p.Hq + h) * p.D + e) = acc;
+    } else if (p.o_f32) {
       *reinterpret_cast<float4*>(p.o_f32 + (row * p.Hq + h) * p.D + e) = acc;
     } else {
       T* out = static_cast<T*>(p.O) + (row * p.Hq + h) * p.D + e;
@@ -265,7 +275,23 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
 // [O fp32 rows*Hq*D | lse rows*Hq] (log2 units), reading R-11.
 template <typename T>
 __global__ void __launch_bounds__(256) merge_ranks_kernel(const float* parts, int world, int64_t rows, int Hq, int D,
-                                                          T* O) {
+                                                          T* O, const uint32_t* flags, uint32_t epoch) {
+  if (flags) {
+    // peer-memory path: wait until every rank released this epoch's chunk
+    if (threadIdx.x < world) {
+      uint32_t v;
+      uint64_t t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        // a peer that never pushes (failed or absent rank): fail the launch
+        // loudly after 10 s instead of hanging the GPU
+        if (t - t0 > 10000000000ull) __trap();
+      } while ((int32_t)(v - epoch) < 0);
+    }
+    __syncthreads();
+  }
   const int64_t rh = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (rh >= rows * Hq) return;
@@ -356,12 +382,28 @@ cudaError_t launch_simt_t(const AttnParams& p, int n_layers, cudaStream_t s) {
 int simt_rows_tile(int G, int D) { (void)G; (void)D; return kRT; }
 
 cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
-                               cudaStream_t s) {
+                               cudaStream_t s, const uint32_t* flags, uint32_t epoch) {
   const int64_t warps = rows * Hq;
   if (warps == 0) return cudaSuccess;
   const int blocks = (int)((warps + 7) / 8);
-  if (bf16) merge_ranks_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<__nv_bfloat16*>(O));
-  else merge_ranks_kernel<float><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<float*>(O));
+  if (bf16)
+    merge_ranks_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<__nv_bfloat16*>(O),
+                                                             flags, epoch);
+  else
+    merge_ranks_kernel<float><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<float*>(O), flags, epoch);
+  return cudaGetLastError();
+}
+
+__global__ void signal_peers_kernel(const uint64_t* peer_flags, int n_peers, int rank, uint32_t epoch) {
+  const int q = threadIdx.x;
+  if (q >= n_peers) return;
+  __threadfence_system();   // the pushed chunk (previous kernel on this stream) before the flag
+  uint32_t* f = reinterpret_cast<uint32_t*>(peer_flags[q]) + rank;
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+}
+
+cudaError_t launch_signal_peers(const uint64_t* peer_flags, int n_peers, int rank, uint32_t epoch, cudaStream_t s) {
+  signal_peers_kernel<<<1, 32 * ((n_peers + 31) / 32), 0, s>>>(peer_flags, n_peers, rank, epoch);
   return cudaGetLastError();
 }
 int simt_key_tile() { return kBK; }

@@ -143,6 +143,12 @@ struct CombineParams {
   int32_t in_layer_stride;
   int32_t Hq, G, D;
   int32_t write_o;
+  // peer push (A9 over peer memory): when n_peers > 0 the fp32 O / lse rows are
+  // written to every peer's gathered buffer (chunk base peer_chunk[q]; lse at
+  // +lse_off floats) instead of o_f32 / lse_out
+  const uint64_t* peer_chunk;
+  int32_t n_peers;
+  int64_t lse_off;
 };
 
 // On-device greedy sampling (kernels_sample.cu).
@@ -170,7 +176,9 @@ cudaError_t launch_greedy(const SampleParams& p, bool bf16, cudaStream_t s);
 size_t sample_partial_bytes();
 // Merge `world` rank partials (packed chunks [O fp32 rows*Hq*D | lse rows*Hq]) into O.
 cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
-                               cudaStream_t s);
+                               cudaStream_t s, const uint32_t* flags = nullptr, uint32_t epoch = 0);
+// Release `epoch` into flag slot `rank` of every peer (after the stream's prior work).
+cudaError_t launch_signal_peers(const uint64_t* peer_flags, int n_peers, int rank, uint32_t epoch, cudaStream_t s);
 int simt_rows_tile(int G, int D);     // rows per SIMT unit
 int simt_key_tile();                  // keys per SIMT tile
 

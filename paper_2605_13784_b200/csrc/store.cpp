@@ -542,7 +542,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.fault = (int32_t)opt_fault;
     ap.pairs = d_pairs;
     ap.n_pairs = (int32_t)pairs.size();
-    const bool fused = use_tc && !plan.groups.empty() && opt_fused_merge;
+    const bool fused = use_tc && !plan.groups.empty() && opt_fused_merge && opts.n_peers == 0;
     if (fused) {
       const size_t need = (size_t)n_layers * plan.groups.size();
       if (need > counters_cap) {
@@ -592,6 +592,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       cp.G = G;
       cp.D = D;
       cp.write_o = 1;
+      cp.peer_chunk = opts.peer_chunk;
+      cp.n_peers = opts.n_peers;
+      cp.lse_off = opts.lse_off;
       cudaEvent_t t1 = tick(st);
       int max_split = 1;
       for (auto& g : plan.groups) max_split = std::max(max_split, g.n_splits);

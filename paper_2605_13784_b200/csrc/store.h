@@ -58,6 +58,9 @@ struct RunOpts {
   bool force_groups = false;   // all outputs as partials through the combine
   float* o_f32 = nullptr;      // combine writes fp32 O here (O layout)
   float* lse_out = nullptr;    // combine writes lse (log2) here, [rows][Hq]
+  const uint64_t* peer_chunk = nullptr;   // device: combine pushes fp32 O / lse to these peer chunks
+  int32_t n_peers = 0;
+  int64_t lse_off = 0;
 };
 
 // tcgen05 path (kernels_tc.cu)

@@ -7,6 +7,9 @@
   session of its own store; ``Store.sharded_query`` computes the rank partial,
   exchanges (O, lse) with one NCCL all-gather and merges.  The NCCL unique id is
   bootstrapped through any torch.distributed process group (gloo or nccl).
+* The same exchange over peer memory (``attach_symmetric``): the kernel that
+  produces a rank partial stores it into every rank's buffer over NVLink and
+  releases a flag; each rank's merge acquires all flags (no NCCL launch).
 """
 from __future__ import annotations
 
@@ -60,3 +63,29 @@ def max_over_ranks(value: float, group=None, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def chunk_floats(n_q: int, num_layers: int, num_q_heads: int, head_dim: int) -> int:
+    """fp32 words of one rank partial of an all-layer query of n_q tokens (O rows + lse)."""
+    return n_q * num_layers * num_q_heads * (head_dim + 1)
+
+
+def attach_symmetric(store, max_chunk_floats: int, group=None):
+    """Allocate the gathered buffer ([world][chunk]) and the flag array in torch symmetric
+    memory over `group`, exchange the peer addresses and attach them to `store`
+    (ssa_comm_attach_peers).  Returns the (buffer, flags) tensors, which must stay alive."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    buf = symm_mem.empty(world * max_chunk_floats, dtype=torch.float32, device=dev)
+    flags = symm_mem.empty(max(world, 4), dtype=torch.int32, device=dev)
+    flags.zero_()
+    gname = group.group_name if group is not None else dist.group.WORLD.group_name
+    hb = symm_mem.rendezvous(buf, gname)
+    hf = symm_mem.rendezvous(flags, gname)
+    dist.barrier(group)
+    store.comm_attach_peers(rank, world, list(hb.buffer_ptrs), list(hf.buffer_ptrs),
+                            world * max_chunk_floats * 4)
+    return buf, flags

@@ -674,3 +674,115 @@ def test_greedy_sample_parity(cuda, dtype, rows, vocab, stride):
         assert np.array_equal(got_gap.view(np.uint32), want_gap.view(np.uint32))
         assert int(n_acc.item()) == (rows // 2 if rows > 2 else rows)
     st.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("nq", [1, 32])
+def test_sharded_peer_push_virtual_ranks(cuda, world, nq):
+    """A9 over peer memory, `world` virtual ranks on one GPU: each rank's combine epilogue stores
+    its partial into every rank's gathered buffer and releases an epoch flag; every rank's merge
+    acquires the flags and merges.  Two rounds exercise the epoch protocol."""
+    import torch
+    from paper_2605_13784_b200.sharding import chunk_floats, shard_range
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    n = 3001
+    spec = streams.StreamSpec("market", seed=41)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    ch = chunk_floats(nq, L, hq, d)
+    bufs = [torch.zeros(world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
+    flags = [torch.zeros(max(world, 4), dtype=torch.int32, device=cuda) for _ in range(world)]
+    stores, sids = [], []
+    for r in range(world):
+        lo, hi = shard_range(n, r, world)
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+        sids.append(st.session_create(None, to_dev(K[:, lo:hi], cuda), to_dev(V[:, lo:hi], cuda)))
+        st.comm_attach_peers(r, world, [b.data_ptr() for b in bufs], [f.data_ptr() for f in flags],
+                             world * ch * 4)
+        stores.append(st)
+    for rnd in range(2):
+        Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1 + rnd, 0, nq)
+        want = ref.session_query(rsid, Qq, Kq, Vq)
+        for r in range(world):
+            stores[r].sharded_push(sids[r], to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda))
+        for r in range(world):
+            O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+            stores[r].sharded_merge(O)
+            ok, e = within(from_dev(O), want, "bf16")
+            assert ok, (rnd, r, e)
+        torch.cuda.synchronize()
+        assert all(int(f[r].item()) == rnd + 1 for f in flags for r in range(world))
+
+
+def test_sharded_symmetric_memory_world1(cuda):
+    """The torch-symmetric-memory attach path (world 1 on one GPU): push + merge == oracle."""
+    import os
+    import tempfile
+    import torch
+    import torch.distributed as dist
+    from paper_2605_13784_b200.sharding import attach_symmetric, chunk_floats
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except Exception as exc:   # pragma: no cover
+        pytest.skip(f"no symmetric memory: {exc}")
+    ssa = _ssa()
+    spec = streams.StreamSpec("peaked", seed=42)
+    st, ref, sid, rsid, tok, _ = _llama_session(cuda, spec, n0=900, appends=(100,))
+    init_here = not dist.is_initialized()
+    if init_here:
+        f = tempfile.NamedTemporaryFile(delete=False)
+        dist.init_process_group("nccl", init_method=f"file://{f.name}", rank=0, world_size=1,
+                                device_id=torch.device(cuda))
+    try:
+        try:
+            keep = attach_symmetric(st, chunk_floats(32, LL["L"], LL["hq"], LL["d"]))
+        except Exception as exc:
+            pytest.skip(f"symmetric memory unavailable here: {type(exc).__name__}: {exc}")
+        Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
+        O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+        st.sharded_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), O)
+        ok, e = within(from_dev(O), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+        assert ok, e
+        del keep
+    finally:
+        if init_here:
+            dist.destroy_process_group()
+
+
+def test_sharded_peer_push_two_processes(cuda):
+    """A9 over peer memory across two processes on one GPU: the gathered buffers and flags are
+    CUDA-IPC mapped into both processes (torch.multiprocessing), so the pushes, the system-scope
+    flag release and the acquiring merge cross a process boundary as they do across GPUs."""
+    import torch
+    import torch.multiprocessing as mp
+    import p2p_worker
+    from paper_2605_13784_b200.sharding import chunk_floats
+    L, hq, hkv, d, P, n, world = 2, 32, 8, 128, 64, 3001, 2
+    spec = streams.StreamSpec("market", seed=44)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+    qs = [gen_qkv(spec, L, hq, hkv, d, 1 + r, 0, 32) for r in range(3)]
+    ch = chunk_floats(32, L, hq, d)
+    bufs = [torch.zeros(world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
+    flags = [torch.zeros(4, dtype=torch.int32, device=cuda) for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    procs = [ctx.Process(target=p2p_worker.run,
+                         args=(r, world, bufs, flags, K, V, [q[0] for q in qs], [q[1] for q in qs],
+                               [q[2] for q in qs], out_q, n, (L, hq, hkv, d, P)))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(out_q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    for i, (Qq, Kq, Vq) in enumerate(qs):
+        want = ref.session_query(rsid, Qq, Kq, Vq)
+        for r in range(world):
+            ok, e = within(results[r][i], want, "bf16")
+            assert ok, (r, i, e)
+    assert all(int(f[r].item()) == 3 for f in flags for r in range(world))
