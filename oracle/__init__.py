@@ -17,6 +17,8 @@ What it computes:
 * ``full_recompute`` — the naive approach of P:42: causal attention over the
   whole concatenation [S; D_1..D_k; Q_j] from scratch, no session state.
 * ``merge_partials`` — split-KV log-sum-exp merge (reading R-11).
+* ``qkv_projection`` / ``rope`` / ``qkv_rope`` / ``round_bf16`` — the fused
+  data-plane projection before attention (reading R-19).
 * ``OracleStore`` — the session model: retained tokens, versions ("data
   version t"), the page allocator replica (lowest free id first, R0 padded to a
   page boundary; reading R-9) and the FNV-1a-64 digest.
@@ -592,3 +594,54 @@ def query_macs(n_cached: int, m: int, num_q_heads: int, d: int) -> int:
     """MACs of QK^T for m new rows over n cached keys ("O(m*n)"):
     Hq * d * sum_{i<m} (n + i + 1)  (the same count again for PV)."""
     return num_q_heads * d * (m * n_cached + m * (m + 1) // 2)
+
+
+# ----------------------------------------------------------------------------
+# fused data-plane projection (SURVEY §8(f) rank 2; `Forward` of Alg. 1 L282)
+# ----------------------------------------------------------------------------
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """fp64 -> bf16 bit patterns (uint16), one round-to-nearest-even to an 8-bit
+    significand (reading R-10: outputs are rounded once).  Finite normal range only."""
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)                         # x = m * 2^e, 0.5 <= |m| < 1
+    q = np.round(m * 256.0)                    # 8 significant bits, half to even
+    y = np.ldexp(q, e - 8).astype(np.float32)  # exact: q has <= 9 bits
+    return (y.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def qkv_projection(x: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """[Q | K | V] = X W^T: the q/k/v projections of the paper's model (Llama-3.1-8B,
+    P:641) inside `Forward` (Alg. 1).  x [n][hidden], w [n_out][hidden]
+    (nn.Linear weight), bf16 bits or floats, decoded exactly; one fp64 matmul."""
+    return to_f64(x) @ to_f64(w).T
+
+
+def rope(x: np.ndarray, positions, theta: float) -> np.ndarray:
+    """Rotary position embedding, rotate-half form (reading R-19; the paper's model
+    uses RoPE, SURVEY A-6): for x [n][H][d] and pair j < d/2 of every head,
+        angle = positions[i] * theta^(-2j/d)
+        x'[j]       = x[j] cos(angle) - x[j + d/2] sin(angle)
+        x'[j + d/2] = x[j + d/2] cos(angle) + x[j] sin(angle)."""
+    x = np.asarray(x, dtype=np.float64)
+    d = x.shape[-1]
+    half = d // 2
+    inv = np.array([theta ** (-2.0 * j / d) for j in range(half)], dtype=np.float64)
+    ang = np.asarray(positions, dtype=np.float64)[:, None] * inv[None, :]
+    c = np.cos(ang)[:, None, :]
+    s = np.sin(ang)[:, None, :]
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def qkv_rope(x, w, num_q_heads: int, num_kv_heads: int, head_dim: int, pos0: int, theta: float):
+    """The fused projection's result in fp64: Q, K, V of shapes [n][Hq][d], [n][Hkv][d],
+    [n][Hkv][d]; RoPE on Q and K at positions pos0 .. pos0+n-1 (theta <= 0: none)."""
+    y = qkv_projection(x, w)
+    n = y.shape[0]
+    q = y[:, : num_q_heads * head_dim].reshape(n, num_q_heads, head_dim)
+    k = y[:, num_q_heads * head_dim: (num_q_heads + num_kv_heads) * head_dim].reshape(n, num_kv_heads, head_dim)
+    v = y[:, (num_q_heads + num_kv_heads) * head_dim:].reshape(n, num_kv_heads, head_dim)
+    if theta > 0:
+        pos = np.arange(pos0, pos0 + n)
+        q, k = rope(q, pos, theta), rope(k, pos, theta)
+    return q, k, v
