@@ -251,6 +251,45 @@ ssa_status ssa_batch_run(ssa_store_t store, int32_t layer, int32_t n_items,
                          const void *V, void *O, void *stream);
 
 /* ----------------------------------------------------------------------------
+ * Fused data-plane projection before attention
+ * -------------------------------------------------------------------------- */
+/* The `Forward` of Alg. 1 L282 up to the attention inputs, for a
+ * Llama-shaped layer (the paper's model):
+ *     [Q | K | V] = X W^T,   Q, K <- RoPE(., pos),   V unchanged,
+ * with X [n][hidden] bf16 token rows and W the nn.Linear weight
+ * [(num_q_heads + 2 num_kv_heads) * head_dim][hidden] bf16 (rows: the Q heads,
+ * then the K heads, then the V heads).  RoPE is the rotate-half form (R-19):
+ * for pair j < head_dim/2 of a head, angle = pos * rope_theta^(-2j/head_dim),
+ *     x'[j]       = x[j] cos - x[j + head_dim/2] sin,
+ *     x'[j + d/2] = x[j + d/2] cos + x[j] sin;
+ * rope_theta <= 0 disables it.  fp32 accumulation, one bf16 rounding (RNE).
+ * Requires a bf16 store with head_dim 128, hidden % 64 == 0, an sm_100 GPU;
+ * X, W and all outputs are DEVICE pointers.  One launch (tcgen05 GEMM with
+ * split-K over a thread-block cluster and a RoPE / store epilogue).
+ *
+ * ssa_qkv_rope: token row i has position pos0 + i; writes Q [n][Hq][d] and
+ *   K, V [n][Hkv][d].  No store state is read or changed.
+ * ssa_append_layer_fused: the per-layer append of an open ticket (as
+ *   ssa_append_layer) whose Q/K/V come from X: positions continue the session
+ *   (n_tokens + evicted tokens, never re-based, R-8); the projection epilogue
+ *   writes K and V straight into the ticket's pages (no scatter launch), then
+ *   the data-plane attention writes O [n_new][Hq][d].
+ * ssa_session_query_fused: ssa_session_query for one layer with Q/K/V from
+ *   X [n_q][hidden] at the positions after the cache; no state change.
+ * Errors: SSA_ERR_INVALID_ARG (shape, dtype, host pointers), as
+ *   ssa_append_layer / ssa_session_query otherwise.  Q/K/V scratch of the
+ *   fused calls is store-owned. */
+ssa_status ssa_qkv_rope(ssa_store_t store, int32_t n, int32_t hidden, int64_t pos0,
+                        float rope_theta, const void *X, const void *W, void *Q, void *K,
+                        void *V, void *stream);
+ssa_status ssa_append_layer_fused(ssa_store_t store, ssa_session_t session, int32_t ticket,
+                                  int32_t layer, int32_t hidden, float rope_theta,
+                                  const void *X, const void *W, void *O, void *stream);
+ssa_status ssa_session_query_fused(ssa_store_t store, ssa_session_t session, int32_t layer,
+                                   int32_t n_q, int32_t hidden, float rope_theta,
+                                   const void *X, const void *W, void *O, void *stream);
+
+/* ----------------------------------------------------------------------------
  * On-device greedy sampling
  * -------------------------------------------------------------------------- */
 /* For each of n_rows rows of `vocab` logits (dtype SSA_FP32 or SSA_BF16, row r
@@ -340,10 +379,11 @@ ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value
 /* Kernel timing recorded while SSA_OPT_TIMING is on, per kernel class
  * (SSA_TIMING_KINDS entries): [0] data-plane attention (create/append/batch),
  * [1] query-plane attention (query/flash/sharded), [2] data-plane split-KV
- * combine, [3] query-plane combine, [4] KV append scatter.
+ * combine, [3] query-plane combine, [4] KV append scatter, [5] fused QKV
+ * projection + RoPE (ssa_qkv_rope and the *_fused calls).
  * ms[i] = summed device time of launches of class i, count[i] = launches.
  * Synchronizes the recorded events; reset != 0 clears the record. */
-#define SSA_TIMING_KINDS 5
+#define SSA_TIMING_KINDS 6
 ssa_status ssa_store_timing(ssa_store_t store, double ms[SSA_TIMING_KINDS],
                             int64_t count[SSA_TIMING_KINDS], int32_t reset);
 

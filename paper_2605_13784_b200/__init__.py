@@ -18,7 +18,7 @@ __all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", 
            "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING", "OPT_FUSED_MERGE",
            "OPT_CTA_PAIR",
            "debug_plan", "TIMING_KINDS"]
-TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter")
+TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter", "qkv_rope")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libssa.so")
@@ -109,6 +109,9 @@ def _load():
         "ssa_sharded_merge": (i32, [vp, i32, i32, vp, vp]),
         "ssa_sharded_partial": (i32, [vp, i32, i32, i32, vp, vp, vp, i32, vp, vp]),
         "ssa_merge_rank_partials": (i32, [vp, i32, i64, vp, vp, vp]),
+        "ssa_qkv_rope": (i32, [vp, i32, i32, i64, ctypes.c_float, vp, vp, vp, vp, vp, vp]),
+        "ssa_append_layer_fused": (i32, [vp, i32, i32, i32, i32, ctypes.c_float, vp, vp, vp, vp]),
+        "ssa_session_query_fused": (i32, [vp, i32, i32, i32, i32, ctypes.c_float, vp, vp, vp, vp]),
         "ssa_status_str": (ctypes.c_char_p, [i32]),
         "ssa_last_error": (ctypes.c_char_p, []),
         "ssa_abi_version": (i32, []),
@@ -224,6 +227,23 @@ class Store:
     def append_layer(self, sid, ticket, layer, Q, K, V, O=None, stream=None):
         _check(lib.ssa_append_layer(self._h, sid, ticket, layer, _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
                                     _stream(stream)), "append_layer")
+
+    # -- fused projection (SURVEY §8(f) rank 2; Alg. 1 L282 `Forward`) ---------
+    def qkv_rope(self, X, W, Q, K, V, pos0=0, rope_theta=500000.0, stream=None):
+        """[Q|K|V] = X W^T with RoPE on Q and K at positions pos0.. (device tensors;
+        X [n][hidden], W [(Hq+2Hkv)*d][hidden], Q [n][Hq][d], K/V [n][Hkv][d], bf16)."""
+        _check(lib.ssa_qkv_rope(self._h, X.shape[0], X.shape[1], pos0, rope_theta, _ptr(X), _ptr(W), _ptr(Q),
+                                _ptr(K), _ptr(V), _stream(stream)), "qkv_rope")
+
+    def append_layer_fused(self, sid, ticket, layer, X, W, O, rope_theta=500000.0, stream=None):
+        """Per-layer append whose Q/K/V come from the fused projection of X; K/V go
+        straight into the ticket's pages."""
+        _check(lib.ssa_append_layer_fused(self._h, sid, ticket, layer, X.shape[1], rope_theta, _ptr(X), _ptr(W),
+                                          _ptr(O), _stream(stream)), "append_layer_fused")
+
+    def session_query_fused(self, sid, layer, X, W, O, rope_theta=500000.0, stream=None):
+        _check(lib.ssa_session_query_fused(self._h, sid, layer, X.shape[0], X.shape[1], rope_theta, _ptr(X), _ptr(W),
+                                           _ptr(O), _stream(stream)), "session_query_fused")
 
     def append_commit(self, sid, ticket):
         ver = ctypes.c_uint64()

@@ -168,10 +168,31 @@ struct SampleParams {
 };
 
 // Kernel launchers (kernels_*.cu).  Return cudaGetLastError() after launch.
+// Fused data-plane projection (kernels_qkv.cu).
+struct QkvParams {
+  const void* X;          // [m][hidden] bf16 token rows
+  const void* W;          // [(Hq + 2 Hkv) D][hidden] bf16 (nn.Linear weight: Q, K, V head rows)
+  void* Q;                // [m][Hq][D] bf16
+  void* K;                // [m][Hkv][D] bf16, or null (paged destination only)
+  void* V;
+  int32_t m, hidden, Hq, Hkv, D;
+  int64_t pos0;           // absolute position of token row 0 (never re-based, R-8)
+  double rope_theta;      // <= 0: no rotary embedding
+  void* poolK;            // optional paged destination: [L][num_pages][Hkv][P][D]
+  void* poolV;
+  const int32_t* pages;   // device page table of the session (slot / P -> page)
+  int64_t page_base;      // layer * num_pages
+  int32_t slot0, P;       // slot of token row 0
+  int32_t splits;         // split-K factor = thread-block cluster size
+};
+
 cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits);
 cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
 cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
+cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s);
+bool qkv_supported(int D, int hidden);
+int qkv_choose_splits(int m, int n_heads, int hidden, int num_sms);
 cudaError_t launch_greedy(const SampleParams& p, bool bf16, cudaStream_t s);
 size_t sample_partial_bytes();
 // Merge `world` rank partials (packed chunks [O fp32 rows*Hq*D | lse rows*Hq]) into O.

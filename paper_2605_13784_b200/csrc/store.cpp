@@ -382,6 +382,7 @@ ssa_status ssa_store::stage_inputs(IoSet* io, cudaStream_t st) {
   if (need > stage_cap) {
     SSA_CUDA(this, cudaDeviceSynchronize());
     if (stage) cudaFree(stage);
+  if (qkv_scratch) cudaFree(qkv_scratch);
     stage = nullptr;
     stage_cap = std::max(need, stage_cap * 2);
     SSA_CUDA(this, cudaMalloc(&stage, stage_cap));
@@ -481,7 +482,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   SSA_CUDA(this, ring.to_device(off, total, st));
 
   // ---- KA: scatter new K/V into pages
-  if (!app_segs.empty()) {
+  if (!app_segs.empty() && !opts.skip_scatter) {
     ScatterParams sp{};
     sp.K = io.k.dev;
     sp.V = io.v.dev;
@@ -1478,3 +1479,127 @@ int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_
 }
 
 }  // extern "C"
+
+// ---- fused data-plane projection (Alg. 1 L282 `Forward`)
+static bool qkv_args_ok(ssa_store* st, int32_t n, int32_t hidden, const void* X, const void* W) {
+  if (n <= 0 || !X || !W || st->cfg.dtype != SSA_BF16 || !st->sm100 || !qkv_supported(st->cfg.head_dim, hidden)) {
+    set_error("qkv: needs bf16, head_dim 128, hidden %% 64 == 0, sm_100 and n > 0");
+    return false;
+  }
+  if (!is_device_ptr(X) || !is_device_ptr(W)) {
+    set_error("qkv: X and W must be device pointers");
+    return false;
+  }
+  return true;
+}
+
+static ssa_status qkv_launch(ssa_store* st, int32_t n, int32_t hidden, int64_t pos0, float rope_theta,
+                             const void* X, const void* W, void* Q, void* K, void* V, const Session* paged,
+                             int32_t layer, int64_t slot0, cudaStream_t cs) {
+  QkvParams qp{};
+  qp.X = X;
+  qp.W = W;
+  qp.Q = Q;
+  qp.K = K;
+  qp.V = V;
+  qp.m = n;
+  qp.hidden = hidden;
+  qp.Hq = st->cfg.num_q_heads;
+  qp.Hkv = st->cfg.num_kv_heads;
+  qp.D = st->cfg.head_dim;
+  qp.pos0 = pos0;
+  qp.rope_theta = rope_theta;
+  if (paged) {
+    qp.poolK = st->poolK;
+    qp.poolV = st->poolV;
+    qp.pages = paged->d_pages;
+    qp.page_base = (int64_t)layer * st->cfg.num_pages;
+    qp.slot0 = (int32_t)slot0;
+    qp.P = st->cfg.page_size;
+  }
+  qp.splits = qkv_choose_splits(n, qp.Hq + 2 * qp.Hkv, hidden, st->num_sms);
+  cudaEvent_t t0 = st->tick(cs);
+  SSA_CUDA(st, launch_qkv_rope(qp, cs));
+  if (t0) st->timed_push(5, t0, st->tick(cs));
+  st->stats.kernel_launches++;
+  return SSA_OK;
+}
+
+ssa_status ssa_qkv_rope(ssa_store_t st, int32_t n, int32_t hidden, int64_t pos0, float rope_theta, const void* X,
+                        const void* W, void* Q, void* K, void* V, void* stream) {
+  SSA_CHECK_STORE(st);
+  if (!qkv_args_ok(st, n, hidden, X, W) || !Q || !K || !V || pos0 < 0) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  return qkv_launch(st, n, hidden, pos0, rope_theta, X, W, Q, K, V, nullptr, 0, 0, (cudaStream_t)stream);
+}
+
+static ssa_status qkv_scratch(ssa_store* st, int64_t n, void** q, void** k, void** v) {
+  const size_t eq = (size_t)n * st->cfg.num_q_heads * st->cfg.head_dim * 2;
+  const size_t ek = (size_t)n * st->cfg.num_kv_heads * st->cfg.head_dim * 2;
+  const size_t need = eq + 2 * ek;
+  if (need > st->qkv_scratch_cap) {
+    SSA_CUDA(st, cudaDeviceSynchronize());
+    if (st->qkv_scratch) cudaFree(st->qkv_scratch);
+    st->qkv_scratch = nullptr;
+    st->qkv_scratch_cap = std::max(need, 2 * st->qkv_scratch_cap);
+    SSA_CUDA(st, cudaMalloc(&st->qkv_scratch, st->qkv_scratch_cap));
+  }
+  *q = st->qkv_scratch;
+  *k = static_cast<uint8_t*>(st->qkv_scratch) + eq;
+  *v = static_cast<uint8_t*>(st->qkv_scratch) + eq + ek;
+  return SSA_OK;
+}
+
+ssa_status ssa_append_layer_fused(ssa_store_t st, ssa_session_t id, int32_t ticket, int32_t layer, int32_t hidden,
+                                  float rope_theta, const void* X, const void* W, void* O, void* stream) {
+  SSA_CHECK_STORE(st);
+  ssa_status rc = SSA_OK;
+  Session* s = check_ticket(st, id, ticket, &rc);
+  if (!s) return rc;
+  if (layer < 0 || layer >= st->cfg.num_layers || !O || !is_device_ptr(O)) return SSA_ERR_INVALID_ARG;
+  if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W)) return SSA_ERR_INVALID_ARG;
+  if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
+  cudaSetDevice(st->cfg.device);
+  const int32_t n_new = s->ticket_n_new;
+  void *q, *k, *v;
+  if ((rc = qkv_scratch(st, n_new, &q, &k, &v)) != SSA_OK) return rc;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int64_t slot0 = st->slot_of(*s, s->n_tokens);
+  // positions never re-based (R-8): the next token's position counts evicted tokens
+  const int64_t pos0 = s->n_tokens + s->n_evicted;
+  if ((rc = qkv_launch(st, n_new, hidden, pos0, rope_theta, X, W, q, k, v, s, layer, slot0, cs)) != SSA_OK) return rc;
+  IoSet io;
+  io.q = {q, tensor_bytes(st, 1, n_new, st->cfg.num_q_heads)};
+  io.k = {k, tensor_bytes(st, 1, n_new, st->cfg.num_kv_heads)};
+  io.v = {v, tensor_bytes(st, 1, n_new, st->cfg.num_kv_heads)};
+  io.o = {O, tensor_bytes(st, 1, n_new, st->cfg.num_q_heads)};
+  if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
+  SegDesc sg{};
+  sg.m = n_new;
+  sg.tail_m = sg.m;
+  st->fill_cached(*s, &sg);
+  sg.append_slot0 = (int32_t)slot0;
+  std::vector<SegDesc> segs{sg};
+  RunOpts ro;
+  ro.skip_scatter = true;   // the projection epilogue wrote K/V into the pages
+  if ((rc = st->run(segs, io, n_new, layer, 1, 0, true, false, cs, ro)) != SSA_OK) return rc;
+  s->ticket_done[layer] = 1;
+  return SSA_OK;
+}
+
+ssa_status ssa_session_query_fused(ssa_store_t st, ssa_session_t id, int32_t layer, int32_t n_q, int32_t hidden,
+                                   float rope_theta, const void* X, const void* W, void* O, void* stream) {
+  SSA_CHECK_STORE(st);
+  Session* s = st->get(id);
+  if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
+  if (layer < 0 || layer >= st->cfg.num_layers || !O || !is_device_ptr(O)) return SSA_ERR_INVALID_ARG;
+  if (!qkv_args_ok(st, n_q, hidden, X, W)) return SSA_ERR_INVALID_ARG;
+  cudaSetDevice(st->cfg.device);
+  void *q, *k, *v;
+  ssa_status rc = qkv_scratch(st, n_q, &q, &k, &v);
+  if (rc != SSA_OK) return rc;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int64_t pos0 = s->n_tokens + s->n_evicted;   // query tokens follow the cache (R-8)
+  if ((rc = qkv_launch(st, n_q, hidden, pos0, rope_theta, X, W, q, k, v, nullptr, 0, 0, cs)) != SSA_OK) return rc;
+  return ssa_session_query(st, id, layer, n_q, q, k, v, O, stream);
+}

@@ -61,6 +61,7 @@ struct RunOpts {
   const uint64_t* peer_chunk = nullptr;   // device: combine pushes fp32 O / lse to these peer chunks
   int32_t n_peers = 0;
   int64_t lse_off = 0;
+  bool skip_scatter = false;   // K/V of the appended segments are already in their pages
 };
 
 // tcgen05 path (kernels_tc.cu)
@@ -100,6 +101,8 @@ struct ssa_store {
   float* part_lse = nullptr;
   size_t part_lse_cap = 0;
   void* stage = nullptr;
+  void* qkv_scratch = nullptr;   // fused projection: dense Q/K/V of the current call
+  size_t qkv_scratch_cap = 0;
   size_t stage_cap = 0;
   int32_t* counters = nullptr;   // fused-merge group counters (zero between launches)
   void* sample_part = nullptr;   // greedy sampling: per-(row, split) partials

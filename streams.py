@@ -261,3 +261,41 @@ def _shape_stream_torch(spec, x, domain, layer, tensor, tok0, ntok, heads, d):
     if name in ("market", "needle"):
         return _shape_stream(spec, x, domain, layer, tensor, tok0, ntok, heads, d)
     raise ValueError(name)
+
+
+# ----------------------------------------------------------------------------
+# fused projection inputs: hidden states X and the q/k/v weight
+# ----------------------------------------------------------------------------
+TENSOR_X, TENSOR_W = 3, 4
+
+
+def gen_hidden(seed: int, session: int, domain: int, layer: int, tok0: int, n: int, hidden: int, device=None):
+    """Hidden-state rows X [n][hidden], bf16, i.i.d. N(0,1) per (token, dim); a pure
+    function of the global token index (chunking-invariant).  numpy uint16 bits when
+    ``device`` is None, else a torch bfloat16 tensor on ``device`` (same bits)."""
+    spec = StreamSpec("flat", seed=seed)
+    if device is None:
+        return gen_tensor_np(spec, session, domain, layer, TENSOR_X, tok0, n, 1, hidden).reshape(n, hidden)
+    return gen_tensor_torch(spec, session, domain, layer, TENSOR_X, tok0, n, 1, hidden, device=device).reshape(n, hidden)
+
+
+def gen_qkv_weight(seed: int, layer: int, n_out: int, hidden: int, device=None):
+    """q/k/v projection weight W [n_out][hidden] (nn.Linear layout), bf16, N(0, 1/hidden)
+    so that X W^T has unit variance (random init; no trained weights)."""
+    spec = StreamSpec("flat", seed=seed)
+    scale = np.float32(1.0 / math.sqrt(hidden))
+    if device is None:
+        x = gen_f32(spec, 0, 0xFFFD, layer, TENSOR_W, 0, n_out, 1, hidden) * scale
+        return bf16_bits_np(x).reshape(n_out, hidden)
+    import torch
+    base = _base_key(spec.seed, spec.stream_id, 0, 0xFFFD, layer, TENSOR_W)
+    out = torch.empty(n_out, hidden, dtype=torch.bfloat16, device=device)
+    step = max(1, (1 << 24) // hidden)
+    for r0 in range(0, n_out, step):   # bounded temporaries
+        r1 = min(n_out, r0 + step)
+        idx = torch.arange(r0 * hidden, r1 * hidden, dtype=torch.int64, device=device)
+        x = _normal_torch(base, idx) * float(scale)
+        b = x.contiguous().view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        b = (b + 0x7FFF + ((b >> 16) & 1)) >> 16
+        out[r0:r1] = _i64_to_bf16(b).view(r1 - r0, hidden)
+    return out
