@@ -387,6 +387,56 @@ def leg_greedy_sample(torch, dev, stream, peaks, steps, warmup):
     return out
 
 
+def leg_qkv_rope(torch, dev, stream, peaks, steps, warmup):
+    """the fused data-plane projection [Q|K|V] = X W^T + RoPE (+ K/V
+    into pages on the append path), Llama-3-8B shapes (hidden 4096, 32/8 heads, d=128),
+    32 layers with distinct weights (1.6 GB: every launch streams W from HBM), for the
+    256-token append and the 32-token query of BJ.configs[1].  Roofline: the larger of the
+    HBM time of the algorithmic bytes (W + X + Q/K/V out) and the tensor time of the
+    FLOPs; cuBLAS (torch.matmul, GEMM only, no RoPE / scatter) on the same shapes is
+    reported beside it as a library reference."""
+    import paper_2605_13784_b200 as ssa
+    import streams
+    L, hq, hkv, d, hidden = 32, 32, 8, 128, 4096
+    n_out = (hq + 2 * hkv) * d
+    st = ssa.Store(1, hq, hkv, d, page_size=64, num_pages=4, dtype="bf16")
+    W = [streams.gen_qkv_weight(9, l, n_out, hidden, device=dev) for l in range(L)]
+    out = {"workload": "Llama-3-8B qkv projection + RoPE, hidden 4096 -> 6144, 32 layers (distinct W)"}
+    gs = torch.cuda.Stream(device=dev)
+    for m, pos0 in ((256, 32512), (32, 32768)):
+        X = [streams.gen_hidden(9, 0, 0, l, pos0, m, hidden, device=dev) for l in range(L)]
+        Q = torch.empty(m, hq, d, dtype=torch.bfloat16, device=dev)
+        K = torch.empty(m, hkv, d, dtype=torch.bfloat16, device=dev)
+        V = torch.empty_like(K)
+        st.qkv_rope(X[0], W[0], Q, K, V, pos0=pos0, stream=gs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for l in range(L):
+                st.qkv_rope(X[l], W[l], Q, K, V, pos0=pos0, stream=gs)
+        ms = _timed(torch, stream, graph.replay, steps, warmup) / L
+        nb = n_out * hidden * 2 + m * hidden * 2 + m * n_out * 2
+        fl = 2.0 * m * hidden * n_out
+        t_hbm = nb / (peaks["hbm_gbs"] * 1e9)
+        t_tc = fl / (peaks["bf16_tflops"] * 1e12)
+        Y = torch.empty(m, n_out, dtype=torch.bfloat16, device=dev)
+        with torch.cuda.stream(gs):
+            torch.matmul(X[0], W[0].t(), out=Y)   # cuBLAS handle / workspace before capture
+        torch.cuda.synchronize()
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=gs):
+            for l in range(L):
+                torch.matmul(X[l], W[l].t(), out=Y)
+        ms_cublas = _timed(torch, stream, g2.replay, steps, warmup) / L
+        out[f"m{m}"] = {"us_per_layer": ms * 1e3, "gbs": nb / (ms * 1e-3) / 1e9, "tflops": fl / (ms * 1e-3) / 1e12,
+                        "bound": "hbm" if t_hbm >= t_tc else "tensor",
+                        "roofline_us": max(t_hbm, t_tc) * 1e6, "frac": max(t_hbm, t_tc) / (ms * 1e-3),
+                        "bytes": nb, "flops": fl, "cublas_gemm_only_us_per_layer": ms_cublas * 1e3}
+        del X, Q, K, V, Y, graph, g2
+    st.close()
+    return out
+
+
 def leg_split128k(torch, dev, stream, peaks, steps, warmup):
     """BJ.configs[4] at N=1: one 131,072-token session, 1-token and 32-token queries over 32 layers."""
     import streams
@@ -581,6 +631,9 @@ def run_ours(args):
     if world == 1 and "argmax" in want:
         guarded("greedy_sample", lambda: leg_greedy_sample(torch, dev, stream, peaks_l, 3, 1))
         torch.cuda.empty_cache()
+    if world == 1 and "qkv" in want:
+        guarded("qkv_rope", lambda: leg_qkv_rope(torch, dev, stream, peaks_l, 5, 2))
+        torch.cuda.empty_cache()
     if world == 1 and "speedup" in want:
         guarded("stateful_vs_recompute", lambda: leg_stateful_vs_recompute(torch, dev, stream, peaks_l, 3, 1))
         torch.cuda.empty_cache()
@@ -664,7 +717,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--legs", default="flash,tenant,speedup,argmax,split",
+    ap.add_argument("--legs", default="flash,tenant,speedup,argmax,qkv,split",
                     help="extra single-GPU legs (configs 3-5) reported in the same JSON line; '' to skip")
     args = ap.parse_args()
     if args.warmup < 3:

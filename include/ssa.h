@@ -395,6 +395,16 @@ ssa_status ssa_store_timing(ssa_store_t store, double ms[SSA_TIMING_KINDS],
  * build, -1 if `bytes` is too small or the copy fails.  Synchronous. */
 int32_t ssa_debug_trace(void *host, size_t bytes);
 
+/* Occupancy probe of the fused-projection kernel (a tuning aid): the number of
+ * thread-block clusters of `splits` CTAs that can be co-resident on the current
+ * device (cudaOccupancyMaxActiveClusters), or -1 on error. */
+int32_t ssa_debug_qkv_clusters(int32_t splits);
+/* Tuning aid: when `device_buf` is non-NULL the following fused-projection
+ * launches write per-CTA %globaltimer stamps (uint64 [grid][8]: start, after
+ * setup, accumulator ready, partial dumped, cluster synced, epilogue done,
+ * exit) into it; NULL turns it off.  Returns 0. */
+int32_t ssa_debug_qkv_trace(void *device_buf);
+
 /* ----------------------------------------------------------------------------
  * Multi-GPU split-KV for one long session (R-12)
  * -------------------------------------------------------------------------- */

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sm100.cuh"
 #include "store.h"
@@ -41,15 +42,18 @@ constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;         // 16 KB
 constexpr int kBBytes = kBN * kBK * 2;         // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kPitch = kBN + 4;                // fp32 dump row pitch (floats): conflict-free float4 rows
+constexpr int kRowBytes = kBN * 4;             // one fp32 partial row (swizzled, no padding)
 constexpr int kThreads = 256;
 constexpr int kMaxSplits = 8;                  // portable cluster size
-static_assert(kBM * kPitch * 4 <= kStages * kStageBytes, "fp32 dump must fit in the stage buffers");
+constexpr int kTableRows = 64;                 // RoPE (cos, sin) table rows (used when S >= 2)
+constexpr int kTableBytes = kTableRows * 64 * 8;
+constexpr int kExchangeRows = kStages * kStageBytes / kRowBytes;   // part + recv rows that fit (192)
 
 struct QkvBars {
   uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t acc;
+  uint64_t recv;   // peers' partial rows landed (bulk-copy complete_tx)
   uint32_t tmem_base;
 };
 
@@ -67,6 +71,41 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
   return v;
 }
 
+// cos / sin of pos * inv_freq, inv_freq = theta^(-2j/D) (R-19): the angle is formed and reduced mod
+// 2 pi in double, so the fp32 sincos sees |a| <= pi at any position.
+__device__ __forceinline__ void rope_cs(int64_t pos, double inv_freq, float* c, float* s) {
+  const double ang = (double)pos * inv_freq;
+  const double k = rint(ang * 0.15915494309189535);   // 1 / (2 pi)
+  double red = fma(-k, 6.283185307179586, ang);
+  red = fma(-k, 2.4492935982947064e-16, red);          // 2 pi - double(2 pi)
+  sincosf((float)red, s, c);
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define QKV_TRACE(i) do { if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 10 + (i)] = gtimer(); } while (0)
+#define QKV_TRACE_T(i) do { if (p.trace) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 10 + (i)] = gtimer(); } while (0)
+
+// shared::cta -> shared::cluster bulk copy (TMA engine), completing bytes on
+// the destination CTA's mbarrier.
+__device__ __forceinline__ void bulk_copy_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_group_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
   __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
   __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
@@ -76,9 +115,15 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
 __global__ void __launch_bounds__(kThreads, 1)
 qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  QKV_TRACE(0);
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  QkvBars& bar = *reinterpret_cast<QkvBars*>(tiles + kStages * kStageBytes);
-  float* dump = reinterpret_cast<float*>(tiles);
+  float* table = reinterpret_cast<float*>(tiles + kStages * kStageBytes);   // [rows][64] (cos, sin)
+  double* inv_freq = reinterpret_cast<double*>(tiles + kStages * kStageBytes + kTableBytes);   // [64]
+  QkvBars& bar = *reinterpret_cast<QkvBars*>(tiles + kStages * kStageBytes + kTableBytes + 64 * 8);
+  // after the mainloop: part = this CTA's partial rows [valid][256] (swizzled,
+  // rows grouped by owner), recv = the peers' partials of this CTA's own rows
+  // [S-1][rows_max][256]
+  float* part = reinterpret_cast<float*>(tiles);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -90,6 +135,13 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
   const int kb_lo = rank * nkb / S;
   const int kb_hi = (rank + 1) * nkb / S;
   const int n_kb = kb_hi - kb_lo;
+  // token rows of this tile split evenly over the cluster (only the valid ones)
+  const int valid = min(kBM, p.m - tm * kBM);
+  auto row_lo = [&](int o) { return o * valid / S; };
+  const int rows_max = (valid + S - 1) / S;
+  const int own_lo = row_lo(rank);
+  const int own_rows = row_lo(rank + 1) - own_lo;
+  float* recv = part + (size_t)valid * 256;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.x);
@@ -99,13 +151,17 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
       mbar_init(&bar.empty[s], 1);
     }
     mbar_init(&bar.acc, 1);
+    mbar_init(&bar.recv, 1);
     fence_mbar_init();
+    // bytes this CTA will receive: its own rows from each of the S-1 peers
+    mbar_arrive_expect_tx(&bar.recv, (uint32_t)((S - 1) * own_rows * kRowBytes));
   }
   if (warp == 2) tmem_alloc<256>(&bar.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
+  QKV_TRACE(1);
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
@@ -114,10 +170,14 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
         const int s = i % kStages;
         if (i >= kStages) mbar_wait(&bar.empty[s], ((i / kStages) - 1) & 1);
         uint8_t* a = tiles + s * kStageBytes;
+        if (p.debug == 5) { mbar_arrive(&bar.full[s]); continue; }   // experiments: no loads
         mbar_arrive_expect_tx(&bar.full[s], kStageBytes);
         const int k0 = (kb_lo + i) * kBK;
         tma_load_2d(a, &maps.x, &bar.full[s], k0, tm * kBM);
-        tma_load_2d(a + kABytes, &maps.w, &bar.full[s], k0, tn * kBN);
+        if (p.debug >= 2)   // experiments: contiguous 32 KB W blocks (wrong values, same bytes)
+          tma_load_2d(a + kABytes, &maps.w, &bar.full[s], 0, (tn * nkb + kb_lo + i) * kBN);
+        else
+          tma_load_2d(a + kABytes, &maps.w, &bar.full[s], k0, tn * kBN);
       }
     }
   } else if (warp == 1) {
@@ -131,6 +191,7 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
         mbar_wait(&bar.full[s], (i / kStages) & 1);
         tc_fence_after();
         const uint64_t st = (uint64_t)((s * kStageBytes) >> 4);
+        if (p.debug != 4)   // experiments: 4 = no MMAs
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk)   // 16 k-elements = 32 B along the swizzled row
           mma_bf16_ss(tmem, ad0 + st + (uint64_t)(kk * 2), bd0 + st + (uint64_t)(kk * 2), idesc,
@@ -139,74 +200,135 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
       }
       mma_commit(&bar.acc);
     }
+  } else if (p.rope_theta > 0.0) {
+    // ------------------------------------------------------------- RoPE table (idle warps 2-7)
+    // inv_freq_j = theta^(-2j/D) once per j in double, then (cos, sin) of this
+    // CTA's rows x 64 frequencies while the mainloop runs.
+    const int t2 = threadIdx.x - 64;
+    if (t2 < 64) inv_freq[t2] = exp2(-(2.0 * t2 / kHeadD) * log2(p.rope_theta));
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads - 64) : "memory");
+    if (own_rows <= kTableRows && t2 < 3 * 64) {
+      // thread (j, chunk c of 3): the first row's angle exactly (double reduction),
+      // later rows by rotating with (cos, sin) of one position step in fp32
+      // (error grows ~1 ulp per row: <= 22 steps, far below bf16)
+      const int j = t2 & 63, c = t2 >> 6;
+      const int r0 = c * own_rows / 3, r1 = (c + 1) * own_rows / 3;
+      if (r0 < r1) {
+        float cs, sn, cd, sd;
+        rope_cs(p.pos0 + tm * kBM + own_lo + r0, inv_freq[j], &cs, &sn);
+        rope_cs(1, inv_freq[j], &cd, &sd);
+        for (int r = r0; r < r1; ++r) {
+          *reinterpret_cast<float2*>(table + (r * 64 + j) * 2) = make_float2(cs, sn);
+          const float cn = fmaf(cs, cd, -sn * sd);
+          sn = fmaf(sn, cd, cs * sd);
+          cs = cn;
+        }
+      }
+    }
+    if (threadIdx.x == 64) QKV_TRACE_T(8);
   }
   __syncwarp();
 
-  // --------------------------------------------------------------- TMEM -> smem
-  // warp w reads TMEM lanes 32*(w%4).. (token rows) and columns 128*(w/4)..
+  // --------------------------------------------------------------- partials -> owners
+  // After every CTA of the cluster has finished its mainloop (the receive
+  // buffers reuse the stage memory), each thread pushes its TMEM row (one token,
+  // 128 of the 256 columns) into the owning CTA's receive buffer
+  // recv[src rank][owner-local row] with distributed-shared-memory stores.
   mbar_wait(&bar.acc, 0);
+  QKV_TRACE(2);
   tc_fence_after();
+  cluster_sync_all();   // all mainloops done: stage memory is free cluster-wide
+  QKV_TRACE(7);
   {
+    // TMEM -> part (local, float4 index XOR (row & 7): conflict-free per-row stores)
     const int q = warp & 3;
     const int ch = warp >> 2;
     const int r = q * 32 + lane;
-    float* row = dump + (size_t)r * kPitch + ch * 128;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * 128 + c * 32), v);
-      tmem_wait_ld();
-      reg_fence32(v);
+    float* d = part + (size_t)r * 256;
 #pragma unroll
-      for (int e = 0; e < 32; e += 4)
-        *reinterpret_cast<float4*>(row + c * 32 + e) =
-            make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                        __uint_as_float(v[e + 3]));
+    for (int h2 = 0; h2 < 2; ++h2) {
+      uint32_t v0[32], v1[32];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * 128 + h2 * 64);
+      tmem_ld32(ta, v0);
+      tmem_ld32(ta + 32, v1);
+      tmem_wait_ld();
+      reg_fence32(v0);
+      reg_fence32(v1);
+      if (r < valid) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int f0 = ch * 32 + h2 * 16 + e, f1 = f0 + 8;
+          *reinterpret_cast<uint4*>(d + 4 * (f0 ^ (r & 7))) =
+              make_uint4(v0[4 * e], v0[4 * e + 1], v0[4 * e + 2], v0[4 * e + 3]);
+          *reinterpret_cast<uint4*>(d + 4 * (f1 ^ (r & 7))) =
+              make_uint4(v1[4 * e], v1[4 * e + 1], v1[4 * e + 2], v1[4 * e + 3]);
+        }
+      }
     }
   }
   tc_fence_before();
-  cluster_sync_all();   // every partial of the cluster is in shared memory
+  fence_proxy_async_smem();   // the bulk copies below read `part` through the async proxy
+  __syncthreads();
+  if (threadIdx.x == 0 && S > 1) {
+    // one bulk DSMEM copy per peer: the owner's rows, into its recv slot for this rank
+    for (int o = 0; o < S; ++o) {
+      if (o == rank) continue;
+      const int lo = row_lo(o), n = row_lo(o + 1) - lo;
+      if (n == 0) continue;
+      const int slot = rank < o ? rank : rank - 1;
+      const uint32_t dst = mapa_shared(smem_u32(recv + (size_t)slot * rows_max * 256), (uint32_t)o);
+      const uint32_t mb = mapa_shared(smem_u32(&bar.recv), (uint32_t)o);
+      bulk_copy_s2cluster(dst, smem_u32(part + (size_t)lo * 256), (uint32_t)(n * kRowBytes), mb);
+    }
+    bulk_commit_group();
+  }
+  QKV_TRACE(3);
+  if (S > 1) mbar_wait_cluster(&bar.recv, 0);   // peers' partials of this CTA's rows are here
+  QKV_TRACE(4);
+  if (p.debug == 1 || p.debug >= 3) {   // experiments: mainloop + exchange only
+    if (threadIdx.x == 0 && S > 1) bulk_wait_group_read0();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<256>(tmem);
+    return;
+  }
 
   // --------------------------------------------------------------- reduce + RoPE + store
   {
-    const int r_lo = rank * kBM / S;
-    const int r_hi = (rank + 1) * kBM / S;
     const int half = lane >> 4;           // 0: dims [0, 64), 1: dims [64, 128)
     const int j0 = 4 * (lane & 15);       // rotary frequency index of this lane's first dim
     const int dcol = 4 * lane;            // this lane's 4 dims within a head
     const int n_heads = p.Hq + 2 * p.Hkv;
     const bool rope = p.rope_theta > 0.0;
-    // inv_freq_j = theta^(-2j/D) in double (R-19); angles are reduced mod 2 pi
-    // in double so fp32 sincos sees |a| <= pi at any position.
-    double inv_freq[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      inv_freq[c] = rope ? exp2(-(2.0 * (j0 + c) / kHeadD) * log2(p.rope_theta)) : 0.0;
-    const uint32_t own = smem_u32(dump);
-#pragma unroll 1
-    for (int r = r_lo + warp; r < r_hi; r += kThreads / 32) {
-      const int t = tm * kBM + r;
-      if (t >= p.m) break;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      const uint32_t off = (uint32_t)((r * kPitch + dcol) * 4);
-      for (int s = 0; s < S; ++s) {
-        const uint32_t src = mapa_shared(own + off, (uint32_t)s);
-        const float4 x = ld_cluster_f4(src);
-        const float4 y = ld_cluster_f4(src + 128 * 4);
+    const bool use_table = rope && own_rows <= kTableRows;
+    auto load_row = [&](int rl, float4& a, float4& b) {
+      const int ra = own_lo + rl;   // tile row (swizzle key)
+      a = make_float4(0.f, 0.f, 0.f, 0.f);
+      b = a;
+      for (int sp = 0; sp < S; ++sp) {   // fixed order of ranks: deterministic sums
+        const float* src = sp == rank ? part + (size_t)ra * 256
+                                      : recv + (size_t)((sp < rank ? sp : sp - 1) * rows_max + rl) * 256;
+        const float4 x = *reinterpret_cast<const float4*>(src + 4 * (lane ^ (ra & 7)));
+        const float4 y = *reinterpret_cast<const float4*>(src + 4 * ((32 + lane) ^ (ra & 7)));
         a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
         b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
       }
+    };
+    float4 na, nb;   // next row, loaded one step ahead (latency overlap)
+    if (warp < own_rows) load_row(warp, na, nb);
+    for (int rl = warp; rl < own_rows; rl += kThreads / 32) {
+      const int t = tm * kBM + own_lo + rl;
+      const float4 a = na, b = nb;
+      if (rl + kThreads / 32 < own_rows) load_row(rl + kThreads / 32, na, nb);
       float cs[4], sn[4];
-      if (rope) {
-        const double pos = (double)(p.pos0 + t);
+      if (use_table) {
+        const float4* e = reinterpret_cast<const float4*>(table + (rl * 64 + j0) * 2);
+        const float4 c01 = e[0], c23 = e[1];
+        cs[0] = c01.x; sn[0] = c01.y; cs[1] = c01.z; sn[1] = c01.w;
+        cs[2] = c23.x; sn[2] = c23.y; cs[3] = c23.z; sn[3] = c23.w;
+      } else if (rope) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double ang = pos * inv_freq[c];
-          const double k = rint(ang * 0.15915494309189535);   // 1 / (2 pi)
-          double red = fma(-k, 6.283185307179586, ang);
-          red = fma(-k, 2.4492935982947064e-16, red);          // 2 pi - double(2 pi)
-          sincosf((float)red, &sn[c], &cs[c]);
-        }
+        for (int c = 0; c < 4; ++c)
+          rope_cs(p.pos0 + t, inv_freq[j0 + c], &cs[c], &sn[c]);
       }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -249,7 +371,10 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
     }
   }
   tc_fence_before();
-  cluster_sync_all();   // peers may still be reading this CTA's partial
+  QKV_TRACE(5);
+  if (threadIdx.x == 0 && S > 1) bulk_wait_group_read0();   // our outgoing copies finished reading
+  __syncthreads();
+  QKV_TRACE(6);
   if (warp == 2) tmem_dealloc<256>(tmem);
 }
 
@@ -257,17 +382,60 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
 
 bool qkv_supported(int D, int hidden) { return D == kHeadD && hidden > 0 && hidden % kBK == 0; }
 
+// part (valid rows) + recv ((S-1) x ceil(valid/S) rows) must fit in the stage memory
+static bool qkv_exchange_fits(int m, int s) {
+  const int v = m < kBM ? m : kBM;
+  return v + (s - 1) * ((v + s - 1) / s) <= kExchangeRows;
+}
+
 int qkv_choose_splits(int m, int n_heads, int hidden, int num_sms) {
+  if (const char* e = getenv("SSA_QKV_SPLITS")) {   // experiments only
+    const int f = atoi(e);
+    if (f >= 1 && f <= kMaxSplits && f <= hidden / kBK && qkv_exchange_fits(m, f)) return f;
+  }
+  // the most CTAs (tiles x S) whose clusters are all co-resident (one wave);
+  // S = 1 when even that does not fit
   const int tiles = ((n_heads * kHeadD + kBN - 1) / kBN) * ((m + kBM - 1) / kBM);
-  int s = num_sms / (tiles > 0 ? tiles : 1);
-  s = s < 1 ? 1 : (s > kMaxSplits ? kMaxSplits : s);
   const int nkb = hidden / kBK;
-  return s > nkb ? nkb : s;
+  static int max_active[kMaxSplits + 1] = {0};
+  int best = 1;
+  for (int s = 2; s <= kMaxSplits && s <= nkb; ++s) {
+    if (!qkv_exchange_fits(m, s)) continue;
+    if (max_active[s] == 0) max_active[s] = qkv_max_active_clusters(s);
+    if (tiles <= max_active[s] && tiles * s <= num_sms) best = s;
+  }
+  return best;
+}
+
+static size_t qkv_smem_bytes() {
+  return (size_t)kStages * kStageBytes + kTableBytes + 64 * 8 + sizeof(QkvBars) + 1024;
+}
+
+// Largest number of co-resident clusters of `splits` CTAs (cudaOccupancyMaxActiveClusters).
+int qkv_max_active_clusters(int splits) {
+  const size_t smem = qkv_smem_bytes();
+  if (cudaFuncSetAttribute(qkv_rope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(splits * 64, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = -1;
+  if (cudaOccupancyMaxActiveClusters(&n, qkv_rope_kernel, &cfg) != cudaSuccess) return -1;
+  return n;
 }
 
 cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s) {
   if (p.m <= 0) return cudaSuccess;
-  if (!qkv_supported(p.D, p.hidden) || p.splits < 1 || p.splits > kMaxSplits || p.splits > p.hidden / kBK)
+  if (!qkv_supported(p.D, p.hidden) || p.splits < 1 || p.splits > kMaxSplits || p.splits > p.hidden / kBK ||
+      !qkv_exchange_fits(p.m, p.splits))
     return cudaErrorNotSupported;
   const int n_heads = p.Hq + 2 * p.Hkv;
   QkvMaps maps;
@@ -280,10 +448,15 @@ cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s) {
   {
     cuuint64_t dims[2] = {(cuuint64_t)p.hidden, (cuuint64_t)n_heads * kHeadD};
     cuuint64_t str[1] = {(cuuint64_t)p.hidden * 2};
+    if (p.debug >= 2) {
+      dims[0] = kBK;
+      dims[1] = (cuuint64_t)n_heads * kHeadD * (p.hidden / kBK);
+      str[0] = kBK * 2;
+    }
     cuuint32_t box[2] = {kBK, kBN};
     if (!encode_bf16_map(&maps.w, p.W, 2, dims, str, box)) return cudaErrorInvalidValue;
   }
-  const size_t smem = (size_t)kStages * kStageBytes + sizeof(QkvBars) + 1024;
+  const size_t smem = qkv_smem_bytes();
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(qkv_rope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

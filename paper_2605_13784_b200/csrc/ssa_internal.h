@@ -184,6 +184,8 @@ struct QkvParams {
   int64_t page_base;      // layer * num_pages
   int32_t slot0, P;       // slot of token row 0
   int32_t splits;         // split-K factor = thread-block cluster size
+  int32_t debug;          // experiments (SSA_QKV_DEBUG): 1 = skip the reduce / RoPE / store epilogue
+  uint64_t* trace;        // experiments: per-CTA %globaltimer stamps [grid][8], or null
 };
 
 cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s);
@@ -193,6 +195,7 @@ cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
 cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s);
 bool qkv_supported(int D, int hidden);
 int qkv_choose_splits(int m, int n_heads, int hidden, int num_sms);
+int qkv_max_active_clusters(int splits);
 cudaError_t launch_greedy(const SampleParams& p, bool bf16, cudaStream_t s);
 size_t sample_partial_bytes();
 // Merge `world` rank partials (packed chunks [O fp32 rows*Hq*D | lse rows*Hq]) into O.

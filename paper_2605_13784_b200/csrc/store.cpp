@@ -1481,12 +1481,24 @@ int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_
 }  // extern "C"
 
 // ---- fused data-plane projection (Alg. 1 L282 `Forward`)
-static bool qkv_args_ok(ssa_store* st, int32_t n, int32_t hidden, const void* X, const void* W) {
+// cudaPointerGetAttributes is not allowed while a stream is being captured into
+// a CUDA graph (it invalidates a global-mode capture); captured calls must pass
+// device pointers anyway.
+static bool capturing(void* stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) != cudaSuccess) { cudaGetLastError(); return false; }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+static bool dev_ok(const void* p, void* stream) { return p && (capturing(stream) || is_device_ptr(p)); }
+
+static uint64_t* g_qkv_trace = nullptr;   // ssa_debug_qkv_trace
+static bool qkv_args_ok(ssa_store* st, int32_t n, int32_t hidden, const void* X, const void* W, void* stream) {
   if (n <= 0 || !X || !W || st->cfg.dtype != SSA_BF16 || !st->sm100 || !qkv_supported(st->cfg.head_dim, hidden)) {
     set_error("qkv: needs bf16, head_dim 128, hidden %% 64 == 0, sm_100 and n > 0");
     return false;
   }
-  if (!is_device_ptr(X) || !is_device_ptr(W)) {
+  if (!dev_ok(X, stream) || !dev_ok(W, stream)) {
     set_error("qkv: X and W must be device pointers");
     return false;
   }
@@ -1518,6 +1530,8 @@ static ssa_status qkv_launch(ssa_store* st, int32_t n, int32_t hidden, int64_t p
     qp.P = st->cfg.page_size;
   }
   qp.splits = qkv_choose_splits(n, qp.Hq + 2 * qp.Hkv, hidden, st->num_sms);
+  if (const char* e = getenv("SSA_QKV_DEBUG")) qp.debug = atoi(e);
+  qp.trace = g_qkv_trace;
   cudaEvent_t t0 = st->tick(cs);
   SSA_CUDA(st, launch_qkv_rope(qp, cs));
   if (t0) st->timed_push(5, t0, st->tick(cs));
@@ -1528,7 +1542,7 @@ static ssa_status qkv_launch(ssa_store* st, int32_t n, int32_t hidden, int64_t p
 ssa_status ssa_qkv_rope(ssa_store_t st, int32_t n, int32_t hidden, int64_t pos0, float rope_theta, const void* X,
                         const void* W, void* Q, void* K, void* V, void* stream) {
   SSA_CHECK_STORE(st);
-  if (!qkv_args_ok(st, n, hidden, X, W) || !Q || !K || !V || pos0 < 0) return SSA_ERR_INVALID_ARG;
+  if (!qkv_args_ok(st, n, hidden, X, W, stream) || !Q || !K || !V || pos0 < 0) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
   return qkv_launch(st, n, hidden, pos0, rope_theta, X, W, Q, K, V, nullptr, 0, 0, (cudaStream_t)stream);
 }
@@ -1556,8 +1570,8 @@ ssa_status ssa_append_layer_fused(ssa_store_t st, ssa_session_t id, int32_t tick
   ssa_status rc = SSA_OK;
   Session* s = check_ticket(st, id, ticket, &rc);
   if (!s) return rc;
-  if (layer < 0 || layer >= st->cfg.num_layers || !O || !is_device_ptr(O)) return SSA_ERR_INVALID_ARG;
-  if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W)) return SSA_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= st->cfg.num_layers || !dev_ok(O, stream)) return SSA_ERR_INVALID_ARG;
+  if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
   const int32_t n_new = s->ticket_n_new;
@@ -1592,8 +1606,8 @@ ssa_status ssa_session_query_fused(ssa_store_t st, ssa_session_t id, int32_t lay
   SSA_CHECK_STORE(st);
   Session* s = st->get(id);
   if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
-  if (layer < 0 || layer >= st->cfg.num_layers || !O || !is_device_ptr(O)) return SSA_ERR_INVALID_ARG;
-  if (!qkv_args_ok(st, n_q, hidden, X, W)) return SSA_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= st->cfg.num_layers || !dev_ok(O, stream)) return SSA_ERR_INVALID_ARG;
+  if (!qkv_args_ok(st, n_q, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
   void *q, *k, *v;
   ssa_status rc = qkv_scratch(st, n_q, &q, &k, &v);
@@ -1602,4 +1616,12 @@ ssa_status ssa_session_query_fused(ssa_store_t st, ssa_session_t id, int32_t lay
   const int64_t pos0 = s->n_tokens + s->n_evicted;   // query tokens follow the cache (R-8)
   if ((rc = qkv_launch(st, n_q, hidden, pos0, rope_theta, X, W, q, k, v, nullptr, 0, 0, cs)) != SSA_OK) return rc;
   return ssa_session_query(st, id, layer, n_q, q, k, v, O, stream);
+}
+
+int32_t ssa_debug_qkv_clusters(int32_t splits) { return qkv_max_active_clusters(splits); }
+
+/* experiments: per-CTA %globaltimer stamps of the next fused-projection launches */
+int32_t ssa_debug_qkv_trace(void* device_buf) {
+  g_qkv_trace = static_cast<uint64_t*>(device_buf);
+  return 0;
 }

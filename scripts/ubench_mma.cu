@@ -11,7 +11,7 @@ using namespace ssa::sm100;
 
 constexpr int kRounds = 512;   // rounds of 8 MMAs (K = 128)
 
-template <bool kPair, bool kTS, int kLdWarps, bool kBulk = false>
+template <bool kPair, bool kTS, int kLdWarps, bool kBulk = false, int kN = 128>
 __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, const uint8_t* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, const uint8_
   long long t0 = 0, t1 = 0;
   if (warp == 1 && rank == 0 && elect_one()) {
     const uint32_t M = kPair ? 256 : 128;
-    const uint32_t idesc = idesc_bf16(M, 128, 0, kTS ? 1 : 0);
+    const uint32_t idesc = idesc_bf16(M, kN, 0, kTS ? 1 : 0);
     const uint64_t ad = sdesc_sw128(smem_u32(a), 16, 1024);
     const uint64_t bd = sdesc_sw128(smem_u32(b), 16, 1024);
     t0 = clock64();
@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, const uint8_
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t off = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+        const uint64_t offb = (uint64_t)(((kk >> 2) * (kN * 128) + (kk & 3) * 32) >> 4);
         if (kTS) {
           if (kPair) mma_pair_ts(tmem + 256, tmem + 8 * kk, bd + (uint64_t)((kk * 2048) >> 4), idesc, 1u);
           else asm volatile(
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, const uint8_
               "r"(tmem + 8 * kk), "l"(bd + (uint64_t)((kk * 2048) >> 4)), "r"(idesc));
         } else {
           if (kPair) mma_pair_ss(tmem, ad + off, bd + off, idesc, 1u);
-          else mma_bf16_ss(tmem, ad + off, bd + off, idesc, 1u);
+          else mma_bf16_ss(tmem, ad + off, bd + offb, idesc, 1u);
         }
       }
     }
@@ -101,9 +102,9 @@ __global__ void __launch_bounds__(256, 1) mma_bench(long long* out, const uint8_
   }
 }
 
-template <bool kPair, bool kTS, int kLd = 0, bool kBulk = false>
+template <bool kPair, bool kTS, int kLd = 0, bool kBulk = false, int kN = 128>
 void run(const char* name, long long* d, const uint8_t* g) {
-  auto k = mma_bench<kPair, kTS, kLd, kBulk>;
+  auto k = mma_bench<kPair, kTS, kLd, kBulk, kN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kPair ? 2 * 74 : 148);
@@ -130,6 +131,8 @@ int main() {
   cudaMalloc(&g, (size_t)4096 * 32768);
   cudaMemset(g, 0, (size_t)4096 * 32768);
   run<false, false>("1-CTA SS M128N128K16", d, g);
+  run<false, false, 0, false, 256>("1-CTA SS M128N256K16 (floor 128)", d, g);
+  run<false, false, 0, false, 64>("1-CTA SS M128N64K16 (floor 32)", d, g);
   run<false, true>("1-CTA TS M128N128K16", d, g);
   run<true, false>("2-CTA SS M256N128K16", d, g);
   run<true, true>("2-CTA TS M256N128K16", d, g);
