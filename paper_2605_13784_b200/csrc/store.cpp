@@ -366,7 +366,28 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// cudaPointerGetAttributes is not allowed while a stream is being captured into
+// a CUDA graph (it invalidates a global-mode capture); captured calls must pass
+// device pointers anyway.
+static bool capturing(void* stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) != cudaSuccess) { cudaGetLastError(); return false; }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
 ssa_status ssa_store::stage_inputs(IoSet* io, cudaStream_t st) {
+  ssa_status rc = stage_plan(io, st);
+  if (rc != SSA_OK) return rc;
+  for (IoBuf* b : {&io->q, &io->k, &io->v}) {
+    if (!b->host) continue;
+    SSA_CUDA(this, cudaMemcpyAsync(b->dev, b->host, b->bytes, cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += (int64_t)b->bytes;
+  }
+  return SSA_OK;
+}
+
+ssa_status ssa_store::stage_plan(IoSet* io, cudaStream_t st) {
+  (void)st;
   // Place every host pointer of the call in one device staging buffer.
   size_t need = 0;
   auto plan_one = [&](IoBuf& b) {
@@ -382,19 +403,69 @@ ssa_status ssa_store::stage_inputs(IoSet* io, cudaStream_t st) {
   if (need > stage_cap) {
     SSA_CUDA(this, cudaDeviceSynchronize());
     if (stage) cudaFree(stage);
-  if (qkv_scratch) cudaFree(qkv_scratch);
     stage = nullptr;
     stage_cap = std::max(need, stage_cap * 2);
     SSA_CUDA(this, cudaMalloc(&stage, stage_cap));
   }
-  for (IoBuf* b : {&io->q, &io->k, &io->v, &io->o}) {
-    if (!b->host) continue;
-    b->dev = static_cast<char*>(stage) + b->stage_off;
-    if (b != &io->o) {
-      SSA_CUDA(this, cudaMemcpyAsync(b->dev, b->host, b->bytes, cudaMemcpyHostToDevice, st));
-      stats.h2d_bytes += (int64_t)b->bytes;
+  for (IoBuf* b : {&io->q, &io->k, &io->v, &io->o})
+    if (b->host) b->dev = static_cast<char*>(stage) + b->stage_off;
+  return SSA_OK;
+}
+
+// All-layer call with host buffers: the layers run in chunks so that the
+// host->device copy of chunk c+1 (h2d_stream) and the device->host copy of
+// chunk c-1's O (d2h_stream) overlap chunk c's kernels on the call's stream.
+// The call's stream waits for the last O copy, so "synchronize `stream`, then
+// read O" still holds.
+ssa_status ssa_store::run_pipelined(std::vector<SegDesc>& segs, IoSet& io, int64_t rows_per_layer, int32_t n_layers,
+                                    bool query_plane, cudaStream_t st) {
+  ssa_status rc = stage_plan(&io, st);
+  if (rc != SSA_OK) return rc;
+  // 2 chunks measured best on the 32-layer 32k query (1.01 vs 1.09 ms unpipelined;
+  // 4 and 8 chunks were slower: smaller launches, more per-chunk overhead)
+  int chunks = std::min(2, n_layers);
+  if (const char* e = getenv("SSA_PIPE_CHUNKS")) chunks = std::max(1, std::min(atoi(e), n_layers));   // experiments
+  if (!h2d_stream) {
+    SSA_CUDA(this, cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
+    SSA_CUDA(this, cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
+  }
+  while ((int)pipe_events.size() < 2 * chunks + 2) {
+    cudaEvent_t e;
+    SSA_CUDA(this, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pipe_events.push_back(e);
+  }
+  cudaEvent_t ev_start = pipe_events[0], ev_end = pipe_events[1];
+  // the staging buffer may still be in use by earlier work on `st`
+  SSA_CUDA(this, cudaEventRecord(ev_start, st));
+  SSA_CUDA(this, cudaStreamWaitEvent(h2d_stream, ev_start, 0));
+  SSA_CUDA(this, cudaStreamWaitEvent(d2h_stream, ev_start, 0));
+  for (int c = 0; c < chunks; ++c) {
+    const int32_t l0 = (int32_t)((int64_t)c * n_layers / chunks), l1 = (int32_t)((int64_t)(c + 1) * n_layers / chunks);
+    IoSet ioc = io;
+    for (IoBuf* b : {&ioc.q, &ioc.k, &ioc.v, &ioc.o}) {
+      if (!b->dev) continue;
+      const size_t per_layer = b->bytes / n_layers;
+      b->dev = static_cast<char*>(b->dev) + per_layer * l0;
+      if (b->host) b->host = static_cast<char*>(b->host) + per_layer * l0;
+      b->bytes = per_layer * (l1 - l0);
+      if (b != &ioc.o && b->host) {
+        SSA_CUDA(this, cudaMemcpyAsync(b->dev, b->host, b->bytes, cudaMemcpyHostToDevice, h2d_stream));
+        stats.h2d_bytes += (int64_t)b->bytes;
+      }
+    }
+    cudaEvent_t ev_in = pipe_events[2 + 2 * c], ev_out = pipe_events[3 + 2 * c];
+    SSA_CUDA(this, cudaEventRecord(ev_in, h2d_stream));
+    SSA_CUDA(this, cudaStreamWaitEvent(st, ev_in, 0));
+    if ((rc = run(segs, ioc, rows_per_layer, l0, l1 - l0, 1, true, query_plane, st)) != SSA_OK) return rc;
+    if (ioc.o.host) {
+      SSA_CUDA(this, cudaEventRecord(ev_out, st));
+      SSA_CUDA(this, cudaStreamWaitEvent(d2h_stream, ev_out, 0));
+      SSA_CUDA(this, cudaMemcpyAsync(ioc.o.host, ioc.o.dev, ioc.o.bytes, cudaMemcpyDeviceToHost, d2h_stream));
+      stats.d2h_bytes += (int64_t)ioc.o.bytes;
     }
   }
+  SSA_CUDA(this, cudaEventRecord(ev_end, d2h_stream));
+  SSA_CUDA(this, cudaStreamWaitEvent(st, ev_end, 0));
   return SSA_OK;
 }
 
@@ -726,6 +797,10 @@ ssa_store::~ssa_store() {
   if (part_o) cudaFree(part_o);
   if (part_lse) cudaFree(part_lse);
   if (stage) cudaFree(stage);
+  if (qkv_scratch) cudaFree(qkv_scratch);
+  for (auto e : pipe_events) cudaEventDestroy(e);
+  if (h2d_stream) cudaStreamDestroy(h2d_stream);
+  if (d2h_stream) cudaStreamDestroy(d2h_stream);
   if (counters) cudaFree(counters);
   if (sample_part) cudaFree(sample_part);
   if (sample_cnt) cudaFree(sample_cnt);
@@ -1123,7 +1198,11 @@ ssa_status ssa_flash_query_batch(ssa_store_t st, ssa_session_t id, int32_t layer
   io.v = {V, tensor_bytes(st, Lin, total, st->cfg.num_kv_heads)};
   io.o = {O, tensor_bytes(st, Lin, total, st->cfg.num_q_heads)};
   cudaStream_t cs = (cudaStream_t)stream;
-  ssa_status rc = st->stage_inputs(&io, cs);
+  // host buffers with all layers: chunked copies overlapped with the kernels
+  const char* pe = getenv("SSA_PIPE_CHUNKS");
+  const bool pipelined = layer < 0 && Lin >= 4 && !(pe && atoi(pe) == 0) && !capturing(stream) &&
+                         (getenv("SSA_PIPE_FORCE") || !is_device_ptr(Q) || !is_device_ptr(K) || !is_device_ptr(V) || !is_device_ptr(O));
+  ssa_status rc = pipelined ? SSA_OK : st->stage_inputs(&io, cs);
   if (rc != SSA_OK) return rc;
   std::vector<SegDesc> segs;
   int64_t row = 0;
@@ -1137,6 +1216,7 @@ ssa_status ssa_flash_query_batch(ssa_store_t st, ssa_session_t id, int32_t layer
     segs.push_back(sg);
     row += q_lens[i];
   }
+  if (pipelined) return st->run_pipelined(segs, io, total, (int32_t)Lin, true, cs);
   if ((rc = st->run(segs, io, total, layer < 0 ? 0 : layer, (int32_t)Lin, 1, true, true, cs)) != SSA_OK) return rc;
   return st->unstage_output(&io, cs);
 }
@@ -1481,14 +1561,6 @@ int32_t ssa_debug_plan(int32_t n_segs, const int32_t* seg_m, const int32_t* seg_
 }  // extern "C"
 
 // ---- fused data-plane projection (Alg. 1 L282 `Forward`)
-// cudaPointerGetAttributes is not allowed while a stream is being captured into
-// a CUDA graph (it invalidates a global-mode capture); captured calls must pass
-// device pointers anyway.
-static bool capturing(void* stream) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) != cudaSuccess) { cudaGetLastError(); return false; }
-  return cs != cudaStreamCaptureStatusNone;
-}
 
 static bool dev_ok(const void* p, void* stream) { return p && (capturing(stream) || is_device_ptr(p)); }
 

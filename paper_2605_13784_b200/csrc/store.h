@@ -101,6 +101,9 @@ struct ssa_store {
   float* part_lse = nullptr;
   size_t part_lse_cap = 0;
   void* stage = nullptr;
+  // pipelined host staging (all-layer calls with host buffers): copy streams and events
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  std::vector<cudaEvent_t> pipe_events;
   void* qkv_scratch = nullptr;   // fused projection: dense Q/K/V of the current call
   size_t qkv_scratch_cap = 0;
   size_t stage_cap = 0;
@@ -153,6 +156,9 @@ struct ssa_store {
   ssa_status query_segments(ssa::Session& s, int32_t layer, int32_t k, const int32_t* q_lens, bool include_tail,
                             std::vector<ssa::SegDesc>* segs, int64_t* total);
   ssa_status unstage_output(ssa::IoSet* io, cudaStream_t st);
+  ssa_status stage_plan(ssa::IoSet* io, cudaStream_t st);   // stage_inputs without the copies
+  ssa_status run_pipelined(std::vector<ssa::SegDesc>& segs, ssa::IoSet& io, int64_t rows_per_layer, int32_t n_layers,
+                           bool query_plane, cudaStream_t st);
   ssa_status run(std::vector<ssa::SegDesc>& segs, const ssa::IoSet& io, int64_t rows_per_layer, int32_t layer0,
                  int32_t n_layers, int32_t in_layer_stride, bool compute_o, bool query_plane, cudaStream_t st,
                  const ssa::RunOpts& opts = ssa::RunOpts());

@@ -309,6 +309,39 @@ def test_host_pointers_equal_device_pointers(cuda):
     del Qp, Op
 
 
+def test_pipelined_host_query_all_layers(cuda):
+    """All-layer query with host buffers runs in layer chunks whose copies overlap the
+    kernels (copy streams + events); O is complete once the CALL's stream is synchronized.
+    Pinned and pageable buffers; results vs the oracle; state unchanged."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 8, 8, 2, 128, 64
+    spec = streams.StreamSpec("peaked", seed=12)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=256)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=256, dtype="bf16")
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 700)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda),
+                            torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda))
+    rsid, _ = ref.session_create(700, Q, K, V)
+    before = (st.digest(sid), st.info(sid))
+    s = torch.cuda.Stream(device=cuda)
+    for i, pinned in enumerate((True, False, True)):
+        Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1 + i, 0, 32)
+        if pinned:
+            hq_, hk_, hv_ = (torch.from_numpy(x.view(np.int16)).pin_memory() for x in (Qq, Kq, Vq))
+            Oh = torch.full(Qq.shape, -1, dtype=torch.int16).pin_memory()
+        else:
+            hq_, hk_, hv_ = (np.ascontiguousarray(x) for x in (Qq, Kq, Vq))
+            Oh = np.full(Qq.shape, 0xFFFF, dtype=np.uint16)
+        st.session_query(sid, hq_, hk_, hv_, Oh, stream=s)
+        s.synchronize()
+        got = Oh.numpy().view(np.uint16) if pinned else Oh
+        mx, mn = errors(got, ref.session_query(rsid, Qq, Kq, Vq))
+        assert mx <= TOL["bf16"][0] and mn <= TOL["bf16"][1], (i, mx, mn)
+    assert (st.digest(sid), st.info(sid)) == before
+    st.close()
+
+
 def test_errors_leave_no_state_change(cuda):
     import torch
     ssa = _ssa()
