@@ -258,7 +258,7 @@ ssa_status ssa_batch_run(ssa_store_t store, int32_t layer, int32_t n_items,
  *     [Q | K | V] = X W^T,   Q, K <- RoPE(., pos),   V unchanged,
  * with X [n][hidden] bf16 token rows and W the nn.Linear weight
  * [(num_q_heads + 2 num_kv_heads) * head_dim][hidden] bf16 (rows: the Q heads,
- * then the K heads, then the V heads).  RoPE is the rotate-half form (R-19):
+ * then the K heads, then the V heads).  RoPE is the rotate-half form (R-21):
  * for pair j < head_dim/2 of a head, angle = pos * rope_theta^(-2j/head_dim),
  *     x'[j]       = x[j] cos - x[j + head_dim/2] sin,
  *     x'[j + d/2] = x[j + d/2] cos + x[j] sin;

@@ -18,7 +18,11 @@ What it computes:
   whole concatenation [S; D_1..D_k; Q_j] from scratch, no session state.
 * ``merge_partials`` — split-KV log-sum-exp merge (reading R-11).
 * ``qkv_projection`` / ``rope`` / ``qkv_rope`` / ``round_bf16`` — the fused
-  data-plane projection before attention (reading R-19).
+  data-plane projection before attention (reading R-21).
+* ``e4m3_decode`` / ``e4m3_encode`` — the FP8 (E4M3) KV-cache variant (SURVEY
+  §8(f) rank 4, reading R-22): codes per the OCP FP8 E4M3 definition, values
+  x / scale rounded once in fp32, then to the nearest E4M3 value (ties to even),
+  saturating at +-448.
 * ``OracleStore`` — the session model: retained tokens, versions ("data
   version t"), the page allocator replica (lowest free id first, R0 padded to a
   page boundary; reading R-9) and the FNV-1a-64 digest.
@@ -88,6 +92,49 @@ def to_f64(x: np.ndarray) -> np.ndarray:
     if x.dtype == np.float64:
         return x
     raise TypeError(f"unsupported storage dtype {x.dtype}")
+
+
+# ----------------------------------------------------------------------------
+# FP8 E4M3 KV storage (P:629 names FP8 KV for the TRT-LLM
+# baseline; reading R-22)
+# ----------------------------------------------------------------------------
+E4M3_MAX = 448.0
+
+
+def e4m3_decode(codes: np.ndarray) -> np.ndarray:
+    """E4M3 code (uint8: sign, 4-bit exponent with bias 7, 3-bit mantissa; no
+    infinities; S.1111.111 is NaN) -> float64, by the format's definition:
+    exponent field 0 -> (-1)^s (m/8) 2^-6, else (-1)^s (1 + m/8) 2^(e-7)."""
+    c = np.asarray(codes, dtype=np.uint8).astype(np.int64)
+    s = (c >> 7) & 1
+    e = (c >> 3) & 15
+    m = c & 7
+    mag = np.where(e == 0, (m / 8.0) * 2.0 ** -6, (1.0 + m / 8.0) * np.exp2(e - 7.0))
+    val = np.where(s == 1, -mag, mag)
+    return np.where((e == 15) & (m == 7), np.nan, val)
+
+
+_E4M3_POS = e4m3_decode(np.arange(127, dtype=np.uint8))   # codes 0..126: the finite values >= 0
+
+
+def e4m3_encode(x, scale: float) -> np.ndarray:
+    """Quantize to E4M3 codes (reading R-22): y = fp32(x) / fp32(scale), one
+    IEEE fp32 division (round to nearest), then y is rounded to the nearest
+    finite E4M3 value with ties to the even code (even mantissa), |y| > 448
+    saturating to 448 (every such y rounds to 448 or overflows); the sign of y
+    is kept (a negative y that rounds to 0 gives -0, code 0x80); NaN -> 0x7F.
+    x: bf16 bit patterns (uint16) or floats exactly representable in fp32."""
+    xf = to_f64(x).astype(np.float32) if np.asarray(x).dtype == np.uint16 else np.asarray(x, dtype=np.float32)
+    y = (xf / np.float32(scale)).astype(np.float64)       # fp32 division, exact widening
+    a = np.minimum(np.abs(y), E4M3_MAX)
+    a = np.where(np.isnan(y), 0.0, a)
+    # spacing of the E4M3 grid around a: 2^-9 below 2^-6 (subnormals), else 2^(floor(log2 a) - 3)
+    _, ex = np.frexp(np.maximum(a, 2.0 ** -6))            # a = f 2^ex, 0.5 <= f < 1
+    ulp = np.exp2(ex - 4.0)
+    q = np.round(a / ulp) * ulp                            # numpy rounds halves to even
+    code = np.searchsorted(_E4M3_POS, q).astype(np.uint8)  # q is on the grid: exact match
+    code = np.where(np.signbit(y), code | np.uint8(0x80), code).astype(np.uint8)
+    return np.where(np.isnan(y), np.uint8(0x7F), code).astype(np.uint8)
 
 
 # ----------------------------------------------------------------------------
@@ -245,9 +292,15 @@ class OracleStore:
     """
 
     def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
-                 dtype="bf16", softmax_scale=0.0, max_sessions=1024):
+                 dtype="bf16", softmax_scale=0.0, max_sessions=1024, kv_format=None,
+                 k_scale=1.0, v_scale=1.0):
         self.L, self.hq, self.hkv, self.d = num_layers, num_q_heads, num_kv_heads, head_dim
         self.P, self.num_pages, self.dtype = page_size, num_pages, dtype
+        # kv_format "e4m3": the cache holds E4M3 codes of K / k_scale and V / v_scale
+        # (reading R-22); every key and value a row attends to -- cached or the
+        # segment's own -- is the dequantized code (code value * scale).
+        self.kv_format = kv_format
+        self.k_scale, self.v_scale = float(np.float32(k_scale)), float(np.float32(v_scale))
         self.scale = softmax_scale if softmax_scale > 0 else default_scale(head_dim)
         self.max_sessions = max_sessions
         self.free = list(range(num_pages))
@@ -303,12 +356,26 @@ class OracleStore:
     def _layers(self, layer):
         return range(self.L) if layer < 0 else [layer]
 
+    def _store_kv(self, K, V):
+        """What the cache stores for input K/V: the input bits, or E4M3 codes (R-22)."""
+        if self.kv_format == "e4m3":
+            return e4m3_encode(K, self.k_scale), e4m3_encode(V, self.v_scale)
+        return K, V
+
+    def _kv_values(self, K, V):
+        """Stored K/V -> the fp64 values attention uses."""
+        if self.kv_format == "e4m3":
+            return e4m3_decode(K) * self.k_scale, e4m3_decode(V) * self.v_scale
+        return to_f64(K), to_f64(V)
+
     def _rows(self, s: _Session, layer: int, Q, K, V, tokens=None, heads=None):
         d = self.d
+        K, V = self._store_kv(K, V)
         kc = s.k[layer] if s.n_tokens else np.zeros((0, self.hkv, d), dtype=K.dtype)
         vc = s.v[layer] if s.n_tokens else np.zeros((0, self.hkv, d), dtype=V.dtype)
-        return segment_rows(kc[:s.n_tokens], vc[:s.n_tokens], Q, K, V, self.hkv, self.scale,
-                            tokens, heads)
+        kc, vc = self._kv_values(kc[:s.n_tokens], vc[:s.n_tokens])
+        K, V = self._kv_values(K, V)
+        return segment_rows(kc, vc, Q, K, V, self.hkv, self.scale, tokens, heads)
 
     # -- API -------------------------------------------------------------------
     def session_create(self, n_prefix, Q, K, V, compute=True):
@@ -324,8 +391,9 @@ class OracleStore:
         sid = self.next_id
         self.next_id += 1
         O = self._compute(s, Q, K, V, -1) if compute else None
-        s.k = [np.array(K[l]) for l in range(self.L)]
-        s.v = [np.array(V[l]) for l in range(self.L)]
+        Ks, Vs = self._store_kv(K, V)
+        s.k = [np.array(Ks[l]) for l in range(self.L)]
+        s.v = [np.array(Vs[l]) for l in range(self.L)]
         s.n_tokens = n_prefix
         s.version = 1
         self.sessions[sid] = s
@@ -349,6 +417,7 @@ class OracleStore:
 
     def _commit_append(self, s: _Session, new_pages, K, V) -> None:
         m = K.shape[1]
+        K, V = self._store_kv(K, V)
         p0 = self._next_position(s)
         s.pages.extend(new_pages)
         for l in range(self.L):
@@ -617,7 +686,7 @@ def qkv_projection(x: np.ndarray, w: np.ndarray) -> np.ndarray:
 
 
 def rope(x: np.ndarray, positions, theta: float) -> np.ndarray:
-    """Rotary position embedding, rotate-half form (reading R-19; the paper's model
+    """Rotary position embedding, rotate-half form (reading R-21; the paper's model
     uses RoPE, SURVEY A-6): for x [n][H][d] and pair j < d/2 of every head,
         angle = positions[i] * theta^(-2j/d)
         x'[j]       = x[j] cos(angle) - x[j + d/2] sin(angle)

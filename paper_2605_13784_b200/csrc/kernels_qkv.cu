@@ -1,7 +1,7 @@
 // kernels_qkv.cu — fused data-plane projection before attention (SURVEY §8(f)
 // NEXT-2): the `Forward` of Alg. 1 L282 up to the attention inputs,
 //     [Q | K | V] = X W_qkv^T          (tcgen05 GEMM, bf16 in, fp32 accumulate)
-//     Q, K <- RoPE(Q, K; pos)          (rotate-half convention, reading R-19)
+//     Q, K <- RoPE(Q, K; pos)          (rotate-half convention, reading R-21)
 //     K, V -> the append's page slots  (replaces the KA scatter, A2)
 // in one launch.  X is [m][hidden] (token rows), W_qkv is the nn.Linear weight
 // [(Hq + 2 Hkv) D][hidden] (rows: Q heads, then K heads, then V heads).
@@ -71,7 +71,7 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
   return v;
 }
 
-// cos / sin of pos * inv_freq, inv_freq = theta^(-2j/D) (R-19): the angle is formed and reduced mod
+// cos / sin of pos * inv_freq, inv_freq = theta^(-2j/D) (R-21): the angle is formed and reduced mod
 // 2 pi in double, so the fp32 sincos sees |a| <= pi at any position.
 __device__ __forceinline__ void rope_cs(int64_t pos, double inv_freq, float* c, float* s) {
   const double ang = (double)pos * inv_freq;

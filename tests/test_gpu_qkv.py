@@ -1,5 +1,5 @@
 """GPU parity of the fused data-plane projection (kernels_qkv.cu)
-against the fp64 oracle (oracle.qkv_rope, reading R-19).
+against the fp64 oracle (oracle.qkv_rope, reading R-21).
 
 Tolerance (derived): the kernel accumulates in fp32 and rounds once to
 bf16, so each output is within half a bf16 ulp of the exact value plus the fp32

@@ -1,5 +1,5 @@
 """Pins for the oracle's fused-projection functions (reading
-R-19): brute force, closed forms, the RoPE invariants, and an independent library
+R-21): brute force, closed forms, the RoPE invariants, and an independent library
 implementation (transformers' Llama rotary embedding).  CPU only."""
 import math
 
