@@ -507,6 +507,57 @@ def leg_split128k_sharded(torch, dev, stream, peaks, steps, warmup, world, rank)
     return out
 
 
+def leg_fp8(torch, dev, stream, peaks, steps, warmup):
+    """the BJ.configs[1] step on an E4M3 KV store (reading R-22) -- the same
+    32k session, 256-token append and 32-token query over 32 layers; the cached K/V bytes halve."""
+    import streams
+    import paper_2605_13784_b200 as ssa
+    L, hq, hkv, d, P = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"], CFG["P"]
+    n_ctx, m_app, q_len = CFG["n_ctx"], CFG["m_append"], CFG["q_len"]
+    n0 = n_ctx - m_app
+    ks = vs = 1 / 32
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=n_ctx // P + 16, max_sessions=4, dtype="bf16",
+                   kv_format="e4m3", k_scale=ks, v_scale=vs)
+    spec = streams.StreamSpec("market", seed=2)
+    sid = build_session(st, torch, dev, spec, n0)
+    Qa, Ka, Va = gen_new(torch, dev, spec, 0, n0, m_app)
+    Oa = torch.empty_like(Qa)
+    Qq, Kq, Vq = gen_new(torch, dev, spec, 1, 0, q_len)
+    Oq = torch.empty_like(Qq)
+
+    def step():
+        st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)
+        st.session_query(sid, Qq, Kq, Vq, Oq, stream=stream)
+        st.session_truncate(sid, n0)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    st.set_option(ssa.OPT_TIMING, 1)
+    st.timing(reset=True)
+    ms = _timed(torch, stream, step, steps, 0)
+    tm = st.timing(reset=True)
+    st.set_option(ssa.OPT_TIMING, 0)
+    attn_q = tm["attn_query"][0] / max(1, tm["attn_query"][1])
+    attn_a = tm["attn_data"][0] / max(1, tm["attn_data"][1])
+    comb_q = tm["combine_query"][0] / steps
+    quant = tm["quant_e4m3"][0] / max(1, tm["quant_e4m3"][1])     # one per call: append, query
+    # algorithmic bytes: cached K+V at 1 byte per element, Q / own K/V / O at bf16
+    nb = (n_ctx * 2 * hkv * d + q_len * hq * d * 2 * 2 + q_len * 2 * hkv * d * 2) * L
+    fl = append_flops_per_layer(n0, m_app, hq, d) * L
+    q_call = attn_q + comb_q + quant
+    st.close()
+    return {"workload": "BJ.configs[1] on an E4M3 KV store (k_scale = v_scale = 1/32): n=32,512 -> 256-token "
+                        "append -> 32-token query at n=32,768, 32 layers per call",
+            "ms_per_step": ms, "query_latency_us_32_layers": q_call * 1e3,
+            "query_latency_us_per_layer": q_call * 1e3 / L, "query_bytes_32_layers": nb,
+            "query_attn_gbs": nb / (attn_q * 1e-3) / 1e9, "query_attn_hbm_frac": nb / (attn_q * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "query_call_gbs": nb / (q_call * 1e-3) / 1e9,
+            "append_attn_ms": attn_a, "append_tflops": fl / (attn_a * 1e-3) / 1e12,
+            "append_tc_frac": fl / (attn_a * 1e-3) / 1e12 / peaks["bf16_tflops"],
+            "kernel_ms": {k: v[0] / max(1, v[1]) for k, v in tm.items()}}
+
+
 def run_ours(args):
     import torch
     import streams
@@ -634,6 +685,9 @@ def run_ours(args):
     if world == 1 and "qkv" in want:
         guarded("qkv_rope", lambda: leg_qkv_rope(torch, dev, stream, peaks_l, 5, 2))
         torch.cuda.empty_cache()
+    if world == 1 and "fp8" in want:
+        guarded("fp8_kv", lambda: leg_fp8(torch, dev, stream, peaks_l, 5, 3))
+        torch.cuda.empty_cache()
     if world == 1 and "speedup" in want:
         guarded("stateful_vs_recompute", lambda: leg_stateful_vs_recompute(torch, dev, stream, peaks_l, 3, 1))
         torch.cuda.empty_cache()
@@ -717,7 +771,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--legs", default="flash,tenant,speedup,argmax,qkv,split",
+    ap.add_argument("--legs", default="flash,tenant,speedup,argmax,qkv,fp8,split",
                     help="extra single-GPU legs (configs 3-5) reported in the same JSON line; '' to skip")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -90,13 +90,26 @@ typedef struct {
     int32_t device;         /* CUDA device ordinal */
     ssa_dtype dtype;
     float softmax_scale;
+    /* KV-cache storage format (FP8 KV is what the paper's
+     * TRT-LLM baseline runs).  SSA_KV_E4M3 stores every cached K / V
+     * element as the E4M3 code of x / k_scale (x / v_scale), the quotient rounded
+     * once in fp32, then to nearest-even E4M3, saturating at +-448 (reading R-22);
+     * attention uses code * scale for every key and value, the segment's own
+     * tokens included.  Requires dtype SSA_BF16 (Q/K/V/O stay bf16 at the ABI),
+     * head_dim 128, an sm_100 GPU, finite scales > 0.  Halves the pool and the
+     * query plane's HBM bytes.  0 = SSA_KV_SAME (K/V stored in `dtype`). */
+    int32_t kv_format;
+    float k_scale;
+    float v_scale;
 } ssa_store_config;
+
+enum { SSA_KV_SAME = 0, SSA_KV_E4M3 = 1 };
 
 typedef struct ssa_store *ssa_store_t;
 typedef int32_t ssa_session_t;
 
 /* Bytes of the K+V pools for `cfg`: 2 * L * num_pages * Hkv * page_size * d *
- * sizeof(dtype) — the paged form of Eq. (memory), with the GQA
+ * sizeof(dtype) (1 byte per element for SSA_KV_E4M3) — the paged form of Eq. (memory), with the GQA
  * KV width Hkv*d in place of the model dimension (R-13). 0 on bad config. */
 size_t ssa_store_pool_bytes(const ssa_store_config *cfg);
 
@@ -328,7 +341,8 @@ ssa_status ssa_session_page_table(ssa_store_t store, ssa_session_t session, int3
                                   int64_t cap, int64_t *n_out);
 
 /* Gather tokens [start, start+count) of `layer` from the pages into
- * K_out/V_out [count][Hkv][d] (host or device), bit-exact; synchronous. */
+ * K_out/V_out [count][Hkv][d] (host or device), bit-exact; synchronous.
+ * SSA_KV_E4M3 stores return the E4M3 codes (1 byte per element). */
 ssa_status ssa_session_read_kv(ssa_store_t store, ssa_session_t session, int32_t layer,
                                int64_t start, int64_t count, void *K_out, void *V_out);
 
@@ -340,7 +354,8 @@ ssa_status ssa_session_load_kv(ssa_store_t store, ssa_session_t session, int64_t
 
 /* FNV-1a-64 digest of the retained K/V: over layers, then tokens, the
  * records int32 LE layer || int64 LE token || K bytes || V bytes (SPEC
- * S:158-166).  Reads the pages back; synchronous. */
+ * S:158-166) -- the stored bytes, i.e. E4M3 codes for an
+ * SSA_KV_E4M3 store.  Reads the pages back; synchronous. */
 ssa_status ssa_session_digest(ssa_store_t store, ssa_session_t session, uint64_t *out);
 
 /* Counters since store creation (or the last reset). */
@@ -380,10 +395,11 @@ ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value
  * (SSA_TIMING_KINDS entries): [0] data-plane attention (create/append/batch),
  * [1] query-plane attention (query/flash/sharded), [2] data-plane split-KV
  * combine, [3] query-plane combine, [4] KV append scatter, [5] fused QKV
- * projection + RoPE (ssa_qkv_rope and the *_fused calls).
+ * projection + RoPE (ssa_qkv_rope and the *_fused calls), [6] E4M3
+ * quantization of a call's K/V (SSA_KV_E4M3 stores).
  * ms[i] = summed device time of launches of class i, count[i] = launches.
  * Synchronizes the recorded events; reset != 0 clears the record. */
-#define SSA_TIMING_KINDS 6
+#define SSA_TIMING_KINDS 7
 ssa_status ssa_store_timing(ssa_store_t store, double ms[SSA_TIMING_KINDS],
                             int64_t count[SSA_TIMING_KINDS], int32_t reset);
 

@@ -18,7 +18,7 @@ __all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", 
            "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING", "OPT_FUSED_MERGE",
            "OPT_CTA_PAIR",
            "debug_plan", "TIMING_KINDS"]
-TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter", "qkv_rope")
+TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter", "qkv_rope", "quant_e4m3")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libssa.so")
@@ -45,7 +45,11 @@ class StoreConfig(ctypes.Structure):
                 ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
                 ("page_size", ctypes.c_int32), ("num_pages", ctypes.c_int64),
                 ("max_sessions", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("dtype", ctypes.c_int32), ("softmax_scale", ctypes.c_float)]
+                ("dtype", ctypes.c_int32), ("softmax_scale", ctypes.c_float),
+                ("kv_format", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float)]
+
+
+KV_SAME, KV_E4M3 = 0, 1
 
 
 class SessionInfo(ctypes.Structure):
@@ -171,10 +175,15 @@ class Store:
     """A KV pool on one GPU plus its sessions (see include/ssa.h)."""
 
     def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, page_size=64, num_pages=1024,
-                 max_sessions=64, device=0, dtype="bf16", softmax_scale=0.0):
+                 max_sessions=64, device=0, dtype="bf16", softmax_scale=0.0, kv_format=None,
+                 k_scale=1.0, v_scale=1.0):
+        """kv_format None: K/V stored in `dtype`; "e4m3": E4M3 codes of K/k_scale, V/v_scale
+        (include/ssa.h, reading R-22)."""
         self.cfg = StoreConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
-                               max_sessions, device, BF16 if dtype == "bf16" else FP32, softmax_scale)
+                               max_sessions, device, BF16 if dtype == "bf16" else FP32, softmax_scale,
+                               KV_E4M3 if kv_format == "e4m3" else KV_SAME, k_scale, v_scale)
         self.dtype = dtype
+        self.kv_format = kv_format
         self.L, self.hq, self.hkv, self.d, self.P = num_layers, num_q_heads, num_kv_heads, head_dim, page_size
         self.device = device
         h = ctypes.c_void_p()
@@ -182,9 +191,11 @@ class Store:
         self._h = h
 
     @staticmethod
-    def pool_bytes(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages, dtype="bf16"):
+    def pool_bytes(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages, dtype="bf16",
+                   kv_format=None, k_scale=1.0, v_scale=1.0):
         c = StoreConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages, 1, 0,
-                        BF16 if dtype == "bf16" else FP32, 0.0)
+                        BF16 if dtype == "bf16" else FP32, 0.0, KV_E4M3 if kv_format == "e4m3" else KV_SAME,
+                        k_scale, v_scale)
         return int(lib.ssa_store_pool_bytes(ctypes.byref(c)))
 
     def close(self):
@@ -324,7 +335,7 @@ class Store:
 
     def read_kv(self, sid, layer, start, count):
         import numpy as np
-        dt = np.uint16 if self.dtype == "bf16" else np.float32
+        dt = np.uint8 if self.kv_format == "e4m3" else np.uint16 if self.dtype == "bf16" else np.float32
         K = np.zeros((count, self.hkv, self.d), dtype=dt)
         V = np.zeros_like(K)
         _check(lib.ssa_session_read_kv(self._h, sid, layer, start, count, _ptr(K), _ptr(V)), "session_read_kv")

@@ -345,6 +345,38 @@ __global__ void __launch_bounds__(256) scatter_kernel(const ScatterParams p) {
   }
 }
 
+// FP8 KV variant (reading R-22): code = E4M3(x / scale), the quotient rounded
+// once in fp32 (IEEE division), then one round-to-nearest-even to E4M3 with
+// saturation at +-448 (cvt.rn.satfinite); 16 elements per thread and tensor.
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
+  uint32_t lo, hi;
+  asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %1;\n\tcvt.u32.u16 %0, t;\n\t}"
+      : "=r"(lo) : "f"(a), "f"(b));
+  asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %1;\n\tcvt.u32.u16 %0, t;\n\t}"
+      : "=r"(hi) : "f"(c), "f"(d));
+  return lo | (hi << 16);
+}
+__device__ __forceinline__ uint4 quant16(const uint4 a, const uint4 b, float s) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  float f[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    f[2 * i] = __fdiv_rn(__uint_as_float(w[i] << 16), s);
+    f[2 * i + 1] = __fdiv_rn(__uint_as_float(w[i] & 0xFFFF0000u), s);
+  }
+  return make_uint4(e4m3x4(f[0], f[1], f[2], f[3]), e4m3x4(f[4], f[5], f[6], f[7]),
+                    e4m3x4(f[8], f[9], f[10], f[11]), e4m3x4(f[12], f[13], f[14], f[15]));
+}
+__global__ void __launch_bounds__(256) quant_e4m3_kernel(const QuantParams p) {
+  const int64_t n16 = p.n / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4* k = reinterpret_cast<const uint4*>(p.K) + 2 * i;
+    const uint4* v = reinterpret_cast<const uint4*>(p.V) + 2 * i;
+    reinterpret_cast<uint4*>(p.K8)[i] = quant16(k[0], k[1], p.k_scale);
+    reinterpret_cast<uint4*>(p.V8)[i] = quant16(v[0], v[1], p.v_scale);
+  }
+}
+
 __global__ void __launch_bounds__(256) gather_kernel(const GatherParams p) {
   const int chunks = p.D * p.elem_bytes / 16;
   const int64_t total = p.count * p.Hkv * chunks;
@@ -445,6 +477,15 @@ cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s)
   if (blocks > 148 * 16) blocks = 148 * 16;
   dim3 grid(blocks, n_layers);
   scatter_kernel<<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_e4m3(const QuantParams& p, cudaStream_t s) {
+  if (p.n == 0) return cudaSuccess;
+  const int64_t work = p.n / 16;
+  int blocks = (int)((work + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  quant_e4m3_kernel<<<blocks, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

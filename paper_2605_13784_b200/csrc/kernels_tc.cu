@@ -17,6 +17,14 @@
 // grows by more than 8 in log2 units), so O is rarely rescaled.
 // Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM
 // allocator, warps 4-7 softmax slot 0, warps 8-11 softmax slot 1.
+//
+// FP8 KV variant (template F8, reading R-22): the pools and
+// the call's own K/V hold E4M3 codes.  Warp 0 loads every K and V tile (16 KB of
+// codes) into the upper half of its 32 KB ring slot; warp 2 (K) and warp 3 (V)
+// convert the codes in place to fp16 in the same 128-byte-swizzled layout the
+// bf16 tiles use (cvt.rn.f16x2.e4m3x2 is exact), and the MMAs run kind::f16 with
+// fp16 operands: Q is converted bf16 -> fp16 in smem once per CTA, P is packed
+// as fp16.  The K scale folds into the softmax constant, the V scale into 1/l.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -57,6 +65,9 @@ static_assert(kRegsWG0 % 8 == 0 && kRegsSoftmax % 8 == 0, "setmaxnreg needs mult
 
 struct Bars {
   uint64_t q_full;
+  uint64_t q_ready;               // F8: Q converted to fp16 (both converter warps)
+  uint64_t k_raw[kMaxStages];     // F8: E4M3 codes of a K stage landed (TMA)
+  uint64_t v_raw[kMaxStages];
   uint64_t k_full[kMaxStages];
   uint64_t v_full[kMaxStages];
   uint64_t k_empty[kMaxStages];   // K stage consumed by the S MMA(s) of its event
@@ -80,6 +91,69 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+template <bool F8>
+__device__ __forceinline__ uint32_t pack_p(float a, float b) {
+  return F8 ? pack_f16(a, b) : pack_bf16(a, b);
+}
+// four E4M3 codes (bytes, lowest first) -> two fp16 pairs, exactly
+__device__ __forceinline__ uint2 e4m3x4_to_f16x4(uint32_t w) {
+  uint2 r;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+      "cvt.rn.f16x2.e4m3x2 %0, lo;\n\tcvt.rn.f16x2.e4m3x2 %1, hi;\n\t}"
+      : "=r"(r.x), "=r"(r.y) : "r"(w));
+  return r;
+}
+// bf16 pair -> fp16 pair (Q of the FP8 variant; |q| well inside fp16's range)
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
+  return pack_f16(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
+// In-place conversion of one ring slot: codes in [kChunkBytes, 2 kChunkBytes)
+// (128 rows x 128 B, 128-byte swizzle) -> fp16 tile [128 rows][128 d] as two
+// 64-column swizzled chunks; chunk 1 of row r overwrites code row r, so each
+// row's codes are read by its 4 lanes before any lane stores.
+__device__ __forceinline__ void convert_kv_slot(uint8_t* slot, int lane) {
+  const int j = lane & 3;             // d range [32 j, 32 j + 32) of the row
+  const int h = j >> 1;               // output 64-column chunk
+#pragma unroll 2
+  for (int it = 0; it < 16; ++it) {
+    const int r = it * 8 + (lane >> 2);
+    const int sw = r & 7;
+    const uint8_t* in = slot + kChunkBytes + r * 128;
+    const uint4 a = *reinterpret_cast<const uint4*>(in + (((2 * j) ^ sw) << 4));
+    const uint4 b = *reinterpret_cast<const uint4*>(in + (((2 * j + 1) ^ sw) << 4));
+    __syncwarp();
+    uint8_t* out = slot + h * kChunkBytes + r * 128;
+    const int cc = (2 * j & 3) * 2;     // first 16-byte output chunk within the 64 columns
+    const uint2 a0 = e4m3x4_to_f16x4(a.x), a1 = e4m3x4_to_f16x4(a.y), a2 = e4m3x4_to_f16x4(a.z),
+                a3 = e4m3x4_to_f16x4(a.w);
+    const uint2 b0 = e4m3x4_to_f16x4(b.x), b1 = e4m3x4_to_f16x4(b.y), b2 = e4m3x4_to_f16x4(b.z),
+                b3 = e4m3x4_to_f16x4(b.w);
+    *reinterpret_cast<uint4*>(out + (((cc + 0) ^ sw) << 4)) = make_uint4(a0.x, a0.y, a1.x, a1.y);
+    *reinterpret_cast<uint4*>(out + (((cc + 1) ^ sw) << 4)) = make_uint4(a2.x, a2.y, a3.x, a3.y);
+    *reinterpret_cast<uint4*>(out + (((cc + 2) ^ sw) << 4)) = make_uint4(b0.x, b0.y, b1.x, b1.y);
+    *reinterpret_cast<uint4*>(out + (((cc + 3) ^ sw) << 4)) = make_uint4(b2.x, b2.y, b3.x, b3.y);
+    __syncwarp();
+  }
+}
+// In-place bf16 -> fp16 of a 32 KB Q tile (same element positions).
+__device__ __forceinline__ void convert_q_tile(uint8_t* q, int lane) {
+#pragma unroll 4
+  for (int i = lane; i < kSlotBytes / 16; i += 32) {
+    uint4 v = reinterpret_cast<uint4*>(q)[i];
+    v.x = bf16x2_to_f16x2(v.x);
+    v.y = bf16x2_to_f16x2(v.y);
+    v.z = bf16x2_to_f16x2(v.z);
+    v.w = bf16x2_to_f16x2(v.w);
+    reinterpret_cast<uint4*>(q)[i] = v;
+  }
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -131,6 +205,7 @@ __device__ __forceinline__ int event_of(int k, int j, int nsh, int nt0, int nt1)
   return nsh + (jj < m ? 2 * jj + k : 2 * m + (jj - m));
 }
 
+template <bool F8>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const int box_rows) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -168,7 +243,10 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     tma_prefetch_desc(&maps.pk);
     tma_prefetch_desc(&maps.pv);
     mbar_init(&bar.q_full, 1);
+    mbar_init(&bar.q_ready, 2);
     for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&bar.k_raw[s], 1);
+      mbar_init(&bar.v_raw[s], 1);
       mbar_init(&bar.k_full[s], 1);
       mbar_init(&bar.v_full[s], 1);
       mbar_init(&bar.k_empty[s], 1);
@@ -189,9 +267,31 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsWG0));
-    if (warp == 0 || warp == 3) {
+    if (F8 && (warp == 2 || warp == 3)) {
+      // ----------------------------------------------------------- F8 converters
+      // warp 2: Q tile 0 then the K ring; warp 3: Q tile 1 (two q tiles) then the V ring
+      const bool is_k = warp == 2;
+      mbar_wait(&bar.q_full, 0);
+      if (is_k || two_q) convert_q_tile(is_k ? q_buf[0] : q_buf[1], lane);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar.q_ready);
+      const int NR = is_k ? NK : NV;
+      uint8_t* ring = is_k ? k_base : v_base;
+      uint64_t* raw = is_k ? bar.k_raw : bar.v_raw;
+      uint64_t* full = is_k ? bar.k_full : bar.v_full;
+      const int E = nt0 + nt1 - nsh;
+      for (int e = 0; e < E; ++e) {
+        const int s = e % NR;
+        mbar_wait(&raw[s], (e / NR) & 1);
+        convert_kv_slot(ring + s * kSlotBytes, lane);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+      }
+    } else if (warp == 0 || (!F8 && warp == 3)) {
       // ----------------------------------------------------------- TMA producers
-      // warp 0: Q and the K ring; warp 3: the V ring
+      // warp 0: Q and the K ring; warp 3: the V ring (F8: warp 0 loads both rings)
       if (elect_one()) {
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
@@ -206,14 +306,10 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
           }
         }
-        const int NR = is_k ? NK : NV;
-        uint8_t* ring = is_k ? k_base : v_base;
-        uint64_t* full = is_k ? bar.k_full : bar.v_full;
-        uint64_t* empty = is_k ? bar.k_empty : bar.v_empty;
-        const CUtensorMap* pool_map = is_k ? &maps.pk : &maps.pv;
-        const CUtensorMap* tail_map = is_k ? &maps.kt : &maps.vt;
         const int E = nt0 + nt1 - nsh;
         const int m01 = min(nt0, nt1) - nsh;
+        // F8: each event loads K then V (codes: one 128-byte chunk per row, into the
+        // slot's upper half; the converter warps signal k_full / v_full)
         for (int e = 0; e < E; ++e) {
           int k, j;
           if (e < nsh) { k = 0; j = e; }
@@ -221,44 +317,55 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           else { k = nt0 > nt1 ? 0 : 1; j = nsh + m01 + (e - nsh - 2 * m01); }
           const WorkUnit& w = k ? w1 : w0;
           const SegDesc sg = p.segs[w.seg];
-          const int s = e % NR;
-          if (e >= NR) mbar_wait(&empty[s], ((e / NR) - 1) & 1);
-          uint8_t* dst = ring + s * kSlotBytes;
           const int tile = w.tile_lo + j;
           const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
-          mbar_arrive_expect_tx(&full[s], kSlotBytes);
-          if (tile < n_pool_tiles) {
-            const int key0 = tile * kBN;
-            const int nb = kBN / box_rows;
-            for (int b = 0; b < nb; ++b) {
-              const int slot = key0 + b * box_rows;
-              int32_t row = 0x7FFFFFF0;   // past the tensor -> TMA zero fill
-              if (slot < sg.n_slots) {
-                const int64_t page = __ldg(sg.pages + slot / p.P);
-                row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
+#pragma unroll 1
+          for (int kv = 0; kv < (F8 ? 2 : 1); ++kv) {
+            const bool ik = F8 ? kv == 0 : is_k;
+            const int NR = ik ? NK : NV;
+            uint8_t* ring = ik ? k_base : v_base;
+            uint64_t* full = F8 ? (ik ? bar.k_raw : bar.v_raw) : (ik ? bar.k_full : bar.v_full);
+            uint64_t* empty = ik ? bar.k_empty : bar.v_empty;
+            const CUtensorMap* pool_map = ik ? &maps.pk : &maps.pv;
+            const CUtensorMap* tail_map = ik ? &maps.kt : &maps.vt;
+            const int s = e % NR;
+            if (e >= NR) mbar_wait(&empty[s], ((e / NR) - 1) & 1);
+            uint8_t* dst = ring + s * kSlotBytes + (F8 ? kChunkBytes : 0);
+            constexpr int nchunk = F8 ? 1 : 2;
+            mbar_arrive_expect_tx(&full[s], nchunk * kChunkBytes);
+            if (tile < n_pool_tiles) {
+              const int key0 = tile * kBN;
+              const int nb = kBN / box_rows;
+              for (int b = 0; b < nb; ++b) {
+                const int slot = key0 + b * box_rows;
+                int32_t row = 0x7FFFFFF0;   // past the tensor -> TMA zero fill
+                if (slot < sg.n_slots) {
+                  const int64_t page = __ldg(sg.pages + slot / p.P);
+                  row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
+                }
+                for (int c = 0; c < nchunk; ++c)
+                  tma_load_2d(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row);
               }
-              for (int c = 0; c < 2; ++c)
-                tma_load_2d(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row);
+            } else {
+              const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
+              for (int c = 0; c < nchunk; ++c)
+                tma_load_3d(dst + c * kChunkBytes, tail_map, &full[s], c * 64, w.kv_head, krow);
             }
-          } else {
-            const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
-            for (int c = 0; c < 2; ++c)
-              tma_load_3d(dst + c * kChunkBytes, tail_map, &full[s], c * 64, w.kv_head, krow);
           }
         }
       }
     } else if (warp == 1) {
       // ----------------------------------------------------------- MMA issuer
       if (elect_one()) {
-        constexpr uint32_t idesc_s = idesc_bf16(kM, kBN, 0, 0);   // Q, K both K-major
-        constexpr uint32_t idesc_o = idesc_bf16(kM, kD, 0, 1);    // P K-major (TMEM), V MN-major
+        constexpr uint32_t idesc_s = F8 ? idesc_f16(kM, kBN, 0, 0) : idesc_bf16(kM, kBN, 0, 0);   // Q, K K-major
+        constexpr uint32_t idesc_o = F8 ? idesc_f16(kM, kD, 0, 1) : idesc_bf16(kM, kD, 0, 1);    // P (TMEM), V MN-major
         // descriptor bases; per-step offsets are compile-time adds on the 16-byte address field
         const uint64_t qd0 = sdesc_sw128(smem_u32(q_buf[0]), 16, 1024);
         const uint64_t qd1 = sdesc_sw128(smem_u32(q_buf[1]), 16, 1024);
         const uint64_t kd0 = sdesc_sw128(smem_u32(k_base), 16, 1024);
         const uint64_t vd0 = sdesc_sw128(smem_u32(v_base), kChunkBytes, 1024);
         constexpr uint64_t kStageStep = kSlotBytes >> 4;
-        mbar_wait(&bar.q_full, 0);
+        mbar_wait(F8 ? &bar.q_ready : &bar.q_full, 0);
         tc_fence_after();
         const int jmax = max(nt0, nt1);
         // prologue: S(k, 0); then per j: PV(k, j) and S(k, j+1) for k = 0, 1
@@ -398,7 +505,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), c2, nmc2);
           const float2 e = ((i & 7) >= 8 - kPolyPairsOf8) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           sum4[i & 3] = __fadd2_rn(sum4[i & 3], e);
-          pk[i] = pack_bf16(e.x, e.y);
+          pk[i] = pack_p<F8>(e.x, e.y);
         }
         const float2 s01 = __fadd2_rn(sum4[0], sum4[1]), s23 = __fadd2_rn(sum4[2], sum4[3]);
         const float2 sum2 = __fadd2_rn(s01, s23);
@@ -444,7 +551,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         tc_fence_after();
       }
       const int rows = w.q_ntok * G;
-      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+      const float inv_l = (l_run > 0.f ? 1.f / l_run : 0.f) * (F8 ? p.o_scale : 1.f);   // F8: V scale
       const int h = w.kv_head * G + r % G;
       const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
       const int64_t orow = in_l + sg.row0 + tok;
@@ -588,6 +695,17 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
             const cuuint32_t* box) {
   return encode_bf16_map(m, base, rank, dims, strides_bytes, box);
 }
+// bf16, or uint8 (E4M3 codes) when u8; 128-byte swizzle either way
+bool encode_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+                const cuuint32_t* box, bool u8) {
+  if (!u8) return encode_bf16_map(m, base, rank, dims, strides_bytes, box);
+  EncodeTiledFn fn = get_encode();
+  if (!fn) return false;
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void*>(base), dims, strides_bytes, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace
 
 int tc_key_tile() { return kBN; }
@@ -620,31 +738,35 @@ cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, c
     cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)(kM / G)};
     if (!encode(&maps.q, p.Q, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
+  // K/V element bytes: 2 (bf16) or 1 (E4M3 codes: a row of d = 128 codes is one 128-byte swizzle chunk)
+  const int kvb = p.kv_fp8 ? 1 : 2;
+  const bool u8 = p.kv_fp8 != 0;
   {
     cuuint64_t dims[3] = {(cuuint64_t)kD, (cuuint64_t)p.Hkv, rows};
-    cuuint64_t str[2] = {(cuuint64_t)kD * 2, (cuuint64_t)p.Hkv * kD * 2};
-    cuuint32_t box[3] = {64, 1, (cuuint32_t)kBN};
-    if (!encode(&maps.kt, p.Kt, 3, dims, str, box)) return cudaErrorInvalidValue;
-    if (!encode(&maps.vt, p.Vt, 3, dims, str, box)) return cudaErrorInvalidValue;
+    cuuint64_t str[2] = {(cuuint64_t)kD * kvb, (cuuint64_t)p.Hkv * kD * kvb};
+    cuuint32_t box[3] = {(cuuint32_t)(128 / kvb), 1, (cuuint32_t)kBN};
+    if (!encode_map(&maps.kt, p.Kt, 3, dims, str, box, u8)) return cudaErrorInvalidValue;
+    if (!encode_map(&maps.vt, p.Vt, 3, dims, str, box, u8)) return cudaErrorInvalidValue;
   }
   const int box_rows = p.P < kBN ? p.P : kBN;
   {
     const cuuint64_t prow = (cuuint64_t)(p.layer0 + n_layers) * p.num_pages * p.Hkv * p.P;
     cuuint64_t dims[2] = {(cuuint64_t)kD, prow};
-    cuuint64_t str[1] = {(cuuint64_t)kD * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-    if (!encode(&maps.pk, p.poolK, 2, dims, str, box)) return cudaErrorInvalidValue;
-    if (!encode(&maps.pv, p.poolV, 2, dims, str, box)) return cudaErrorInvalidValue;
+    cuuint64_t str[1] = {(cuuint64_t)kD * kvb};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / kvb), (cuuint32_t)box_rows};
+    if (!encode_map(&maps.pk, p.poolK, 2, dims, str, box, u8)) return cudaErrorInvalidValue;
+    if (!encode_map(&maps.pv, p.poolV, 2, dims, str, box, u8)) return cudaErrorInvalidValue;
   }
   const size_t smem = (size_t)kNumSlots * kSlotBytes + sizeof(Bars) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool configured[2] = {false, false};
+  auto kern = p.kv_fp8 ? attn_tc_kernel<true> : attn_tc_kernel<false>;
+  if (!configured[p.kv_fp8 ? 1 : 0]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[p.kv_fp8 ? 1 : 0] = true;
   }
   dim3 grid(p.n_pairs, n_layers);
-  attn_tc_kernel<<<grid, kThreads, smem, s>>>(p, maps, box_rows);
+  kern<<<grid, kThreads, smem, s>>>(p, maps, box_rows);
   return cudaGetLastError();
 }
 

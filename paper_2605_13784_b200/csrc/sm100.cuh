@@ -173,6 +173,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32
          | (a_mn_major << 15) | (b_mn_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// A and B in fp16 (the FP8 KV variant converts E4M3 codes to fp16 in smem).
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, uint32_t a_mn_major, uint32_t b_mn_major) {
+  return (1u << 4)                 // D format F32; A, B format F16 (0)
+         | (a_mn_major << 15) | (b_mn_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
 
 // 2^x for a pair on the FMA pipe (no MUFU): x = j + f with j = rint(x) from the
 // 1.5*2^23 magic add, f in [-0.5, 0.5]; 2^f by a degree-3 minimax polynomial

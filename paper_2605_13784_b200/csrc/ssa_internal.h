@@ -94,6 +94,19 @@ struct AttnParams {
   int32_t* group_counters;   // [layers][n_groups], or null: separate combine kernel
   float* o_f32;              // optional fp32 O output (O layout) instead of O
   float* lse_out;            // optional lse output (log2, [rows][Hq])
+  // FP8 KV variant (reading R-22): pools and Kt/Vt hold E4M3 codes; scale_log2
+  // already includes k_scale, o_scale = v_scale multiplies 1/l
+  int32_t kv_fp8;
+  float o_scale;
+};
+
+struct QuantParams {
+  const void* K;         // bf16 [n] (flattened [layers][rows][Hkv][D])
+  const void* V;
+  uint8_t* K8;           // E4M3 codes [n]
+  uint8_t* V8;
+  int64_t n;             // elements per tensor (multiple of 16)
+  float k_scale, v_scale;
 };
 
 // Append scatter (KA): copy new K/V rows into pages, bit-exact.
@@ -191,6 +204,7 @@ struct QkvParams {
 cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaStream_t s);
 cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits);
 cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
+cudaError_t launch_quant_e4m3(const QuantParams& p, cudaStream_t s);
 cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
 cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s);
 bool qkv_supported(int D, int hidden);

@@ -489,6 +489,10 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   Plan plan;
   PlanConfig pc;
   const bool use_tc = compute_o && tc_eligible(segs);
+  if (kv_fp8 && compute_o && !use_tc) {
+    ssa::set_error("E4M3 KV cache: attention needs the tcgen05 path (sm_100, default backend)");
+    return SSA_ERR_UNSUPPORTED;
+  }
   if (compute_o) {
     pc.Hkv = cfg.num_kv_heads;
     pc.key_tile = use_tc ? tc_key_tile() : simt_key_tile();
@@ -511,7 +515,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   const bool fused_req = use_tc && opt_fused_merge;
   if (use_tc) {
     std::vector<char> in_pair2;
-    if (opt_cta_pair && !fused_req) pair_units_cta2(segs, plan, pc.key_tile, &pairs2, &in_pair2);
+    if (opt_cta_pair && !fused_req && !kv_fp8) pair_units_cta2(segs, plan, pc.key_tile, &pairs2, &in_pair2);
     pair_units(segs, plan, pc.key_tile, &pairs, pairs2.empty() ? nullptr : &in_pair2);
   }
   // ---- append segments for the scatter
@@ -552,11 +556,39 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   auto d_pairs2 = reinterpret_cast<const TcPair*>(put(pairs2.data(), b_pairs2));
   SSA_CUDA(this, ring.to_device(off, total, st));
 
+  // ---- E4M3 KV (R-22): codes of the call's K/V, the tails' and the scatter's source
+  const void* k_src = io.k.dev;
+  const void* v_src = io.v.dev;
+  if (kv_fp8 && io.k.dev && (compute_o || (!app_segs.empty() && !opts.skip_scatter))) {
+    QuantParams qp{};
+    qp.n = (int64_t)(in_layer_stride ? n_layers : 1) * rows_per_layer * cfg.num_kv_heads * D;
+    if ((size_t)(2 * qp.n) > kv8_cap) {
+      SSA_CUDA(this, cudaStreamSynchronize(st));
+      SSA_CUDA(this, cudaDeviceSynchronize());
+      if (kv8) cudaFree(kv8);
+      kv8 = nullptr;
+      kv8_cap = std::max((size_t)(2 * qp.n), 2 * kv8_cap);
+      SSA_CUDA(this, cudaMalloc(&kv8, kv8_cap));
+    }
+    qp.K = io.k.dev;
+    qp.V = io.v.dev;
+    qp.K8 = kv8;
+    qp.V8 = kv8 + qp.n;
+    qp.k_scale = cfg.k_scale;
+    qp.v_scale = cfg.v_scale;
+    cudaEvent_t t0 = tick(st);
+    SSA_CUDA(this, launch_quant_e4m3(qp, st));
+    if (t0) timed_push(6, t0, tick(st));
+    stats.kernel_launches++;
+    k_src = qp.K8;
+    v_src = qp.V8;
+  }
+
   // ---- KA: scatter new K/V into pages
   if (!app_segs.empty() && !opts.skip_scatter) {
     ScatterParams sp{};
-    sp.K = io.k.dev;
-    sp.V = io.v.dev;
+    sp.K = k_src;
+    sp.V = v_src;
     sp.rows_per_layer = rows_per_layer;
     sp.layer0 = layer0;
     sp.in_layer_stride = in_layer_stride;
@@ -566,7 +598,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     sp.Hkv = cfg.num_kv_heads;
     sp.D = D;
     sp.P = cfg.page_size;
-    sp.elem_bytes = elem;
+    sp.elem_bytes = pelem;
     sp.segs = d_app;
     sp.tok_prefix = d_pre;
     sp.n_segs = (int32_t)app_segs.size();
@@ -587,8 +619,8 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     }
     AttnParams ap{};
     ap.Q = io.q.dev;
-    ap.Kt = io.k.dev;
-    ap.Vt = io.v.dev;
+    ap.Kt = k_src;
+    ap.Vt = v_src;
     ap.O = io.o.dev;
     ap.rows_per_layer = rows_per_layer;
     ap.layer0 = layer0;
@@ -601,7 +633,9 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.D = D;
     ap.P = cfg.page_size;
     ap.G = G;
-    ap.scale_log2 = scale * 1.4426950408889634f;
+    ap.scale_log2 = scale * 1.4426950408889634f * (kv_fp8 ? cfg.k_scale : 1.f);
+    ap.kv_fp8 = kv_fp8 ? 1 : 0;
+    ap.o_scale = kv_fp8 ? cfg.v_scale : 1.f;
     ap.segs = d_segs;
     ap.units = d_units;
     ap.n_units = (int32_t)plan.units.size();
@@ -738,12 +772,17 @@ static bool valid_config(const ssa_store_config* c) {
   const int d = c->head_dim;
   if (d != 16 && d != 32 && d != 64 && d != 128) return false;
   if ((int64_t)c->num_pages * c->num_kv_heads * c->page_size >= (1LL << 31)) return false;
+  if (c->kv_format != SSA_KV_SAME && c->kv_format != SSA_KV_E4M3) return false;
+  if (c->kv_format == SSA_KV_E4M3 &&
+      (c->dtype != SSA_BF16 || d != 128 || !(c->k_scale > 0.f) || !(c->v_scale > 0.f) ||
+       !std::isfinite(c->k_scale) || !std::isfinite(c->v_scale)))
+    return false;
   return true;
 }
 
 size_t ssa_store_pool_bytes(const ssa_store_config* c) {
   if (!valid_config(c)) return 0;
-  const size_t elem = c->dtype == SSA_BF16 ? 2 : 4;
+  const size_t elem = c->kv_format == SSA_KV_E4M3 ? 1 : c->dtype == SSA_BF16 ? 2 : 4;
   return 2 * (size_t)c->num_layers * c->num_pages * c->num_kv_heads * c->page_size * c->head_dim * elem;
 }
 
@@ -764,6 +803,8 @@ ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
   ssa_store* st = new ssa_store();
   st->cfg = *cfg;
   st->elem = cfg->dtype == SSA_BF16 ? 2 : 4;
+  st->kv_fp8 = cfg->kv_format == SSA_KV_E4M3;
+  st->pelem = st->kv_fp8 ? 1 : st->elem;
   st->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : (float)(1.0 / std::sqrt((double)cfg->head_dim));
   cudaDeviceGetAttribute(&st->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   int major = 0, minor = 0;
@@ -798,6 +839,7 @@ ssa_store::~ssa_store() {
   if (part_lse) cudaFree(part_lse);
   if (stage) cudaFree(stage);
   if (qkv_scratch) cudaFree(qkv_scratch);
+  if (kv8) cudaFree(kv8);
   for (auto e : pipe_events) cudaEventDestroy(e);
   if (h2d_stream) cudaStreamDestroy(h2d_stream);
   if (d2h_stream) cudaStreamDestroy(d2h_stream);
@@ -1140,7 +1182,7 @@ ssa_status ssa_session_alias_prefix(ssa_store_t st, ssa_session_t donor_id, int6
     st->stats.pages_reserved += 1;
     const int32_t src = d->pages[full];
     // one page = [Hkv][P][d] contiguous per layer; layers are num_pages pages apart
-    const size_t blk = (size_t)st->cfg.num_kv_heads * P * st->cfg.head_dim * st->elem;
+    const size_t blk = (size_t)st->cfg.num_kv_heads * P * st->cfg.head_dim * st->pelem;
     const size_t pitch = blk * (size_t)st->cfg.num_pages;
     for (void* pool : {st->poolK, st->poolV}) {
       char* b = static_cast<char*>(pool);
@@ -1385,7 +1427,7 @@ ssa_status ssa_session_read_kv(ssa_store_t st, ssa_session_t id, int32_t layer, 
     return SSA_ERR_INVALID_ARG;
   if (count == 0) return SSA_OK;
   cudaSetDevice(st->cfg.device);
-  const size_t bytes = (size_t)count * st->cfg.num_kv_heads * st->cfg.head_dim * st->elem;
+  const size_t bytes = (size_t)count * st->cfg.num_kv_heads * st->cfg.head_dim * st->pelem;
   const bool kdev = is_device_ptr(K_out), vdev = is_device_ptr(V_out);
   void* dk = K_out;
   void* dv = V_out;
@@ -1405,7 +1447,7 @@ ssa_status ssa_session_read_kv(ssa_store_t st, ssa_session_t id, int32_t layer, 
   gp.Hkv = st->cfg.num_kv_heads;
   gp.D = st->cfg.head_dim;
   gp.P = st->cfg.page_size;
-  gp.elem_bytes = st->elem;
+  gp.elem_bytes = st->pelem;
   gp.start = start;
   gp.count = count;
   gp.n_prefix = s->n_prefix;
@@ -1497,7 +1539,7 @@ ssa_status ssa_session_digest(ssa_store_t st, ssa_session_t id, uint64_t* out) {
   if (!out) return SSA_ERR_INVALID_ARG;
   uint64_t h = 0xcbf29ce484222325ULL;
   const int64_t n = s->n_tokens;
-  const size_t row = (size_t)st->cfg.num_kv_heads * st->cfg.head_dim * st->elem;
+  const size_t row = (size_t)st->cfg.num_kv_heads * st->cfg.head_dim * st->pelem;
   std::vector<uint8_t> k(n * row), v(n * row);
   for (int32_t l = 0; l < st->cfg.num_layers; ++l) {
     if (n) {
@@ -1644,6 +1686,10 @@ ssa_status ssa_append_layer_fused(ssa_store_t st, ssa_session_t id, int32_t tick
   if (!s) return rc;
   if (layer < 0 || layer >= st->cfg.num_layers || !dev_ok(O, stream)) return SSA_ERR_INVALID_ARG;
   if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
+  if (st->kv_fp8) {   // the projection epilogue stores bf16 K/V into the pages
+    set_error("ssa_append_layer_fused: not available for an E4M3 KV store (use ssa_qkv_rope + ssa_append_layer)");
+    return SSA_ERR_UNSUPPORTED;
+  }
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
   const int32_t n_new = s->ticket_n_new;

@@ -83,7 +83,11 @@ struct CommState;
 
 struct ssa_store {
   ssa_store_config cfg{};
-  int elem = 2;
+  int elem = 2;            // bytes per Q/K/V/O element at the ABI
+  int pelem = 2;           // bytes per pool element (1: E4M3 codes)
+  bool kv_fp8 = false;     // SSA_KV_E4M3 (reading R-22)
+  uint8_t* kv8 = nullptr;  // E4M3 codes of the current call's K and V (tails + scatter source)
+  size_t kv8_cap = 0;
   float scale = 1.f;
   int num_sms = 148;
   bool sm100 = false;

@@ -47,6 +47,13 @@ def test_pool_bytes_matches_memory_model():
     assert ssa.Store.pool_bytes(1, 4, 4, 64, 16, 40, "fp32") == 2 * 1 * 4 * 64 * 640 * 4
     assert ssa.Store.pool_bytes(32, 32, 7, 128, 64, 512, "bf16") == 0      # Hkv must divide Hq
     assert ssa.Store.pool_bytes(32, 32, 8, 128, 48, 512, "bf16") == 0      # page size power of two
+    # E4M3 KV (reading R-22): one byte per element -> 2 GiB at 32k; needs bf16, d=128, scales > 0
+    e4 = dict(kv_format="e4m3", k_scale=1 / 16, v_scale=1 / 32)
+    assert ssa.Store.pool_bytes(32, 32, 8, 128, 64, 512, "bf16", **e4) == 2147483648
+    assert ssa.Store.pool_bytes(32, 32, 8, 64, 64, 512, "bf16", **e4) == 0
+    assert ssa.Store.pool_bytes(32, 32, 8, 128, 64, 512, "fp32", **e4) == 0
+    assert ssa.Store.pool_bytes(32, 32, 8, 128, 64, 512, "bf16", kv_format="e4m3", k_scale=0.0) == 0
+    assert ssa.Store.pool_bytes(32, 32, 8, 128, 64, 512, "bf16", kv_format="e4m3", v_scale=float("inf")) == 0
 
 
 def test_store_create_fails_loudly_without_gpu():
