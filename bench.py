@@ -547,8 +547,24 @@ def leg_fp8(torch, dev, stream, peaks, steps, warmup):
     fl = append_flops_per_layer(n0, m_app, hq, d) * L
     q_call = attn_q + comb_q + quant
     st.close()
+    # BJ.configs[4] at N=1 on the E4M3 store: 131,072 cached tokens, 1- and 32-token queries
+    n = 131072
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=n // P + 8, max_sessions=2, dtype="bf16",
+                   kv_format="e4m3", k_scale=ks, v_scale=vs)
+    spec5 = streams.StreamSpec("market", seed=5)
+    sid = build_session_n(st, torch, dev, spec5, n)
+    long = {}
+    for qn in (1, 32):
+        q, k, v = gen_new(torch, dev, spec5, 1, 0, qn)
+        o = torch.empty_like(q)
+        qms = _timed(torch, stream, lambda: st.session_query(sid, q, k, v, o, stream=stream), steps, warmup)
+        b = (n * 2 * hkv * d + qn * hq * d * 2 * 2 + qn * 2 * hkv * d * 2) * L
+        long[f"q{qn}_n131072"] = {"ms_32_layers": qms, "us_per_layer": qms * 1e3 / L, "gbs": b / (qms * 1e-3) / 1e9,
+                                  "hbm_frac": b / (qms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+    st.close()
     return {"workload": "BJ.configs[1] on an E4M3 KV store (k_scale = v_scale = 1/32): n=32,512 -> 256-token "
                         "append -> 32-token query at n=32,768, 32 layers per call",
+            "split_kv_128k": long,
             "ms_per_step": ms, "query_latency_us_32_layers": q_call * 1e3,
             "query_latency_us_per_layer": q_call * 1e3 / L, "query_bytes_32_layers": nb,
             "query_attn_gbs": nb / (attn_q * 1e-3) / 1e9, "query_attn_hbm_frac": nb / (attn_q * 1e-3) / 1e9 / peaks["hbm_gbs"],

@@ -113,44 +113,66 @@ __device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
   return pack_f16(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
 }
 
+// 16-byte shared-memory accesses by 32-bit shared address (LDS / STS: the
+// aligned generic pointer of the dynamic smem would compile to generic LD / ST)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
 // In-place conversion of one ring slot: codes in [kChunkBytes, 2 kChunkBytes)
 // (128 rows x 128 B, 128-byte swizzle) -> fp16 tile [128 rows][128 d] as two
-// 64-column swizzled chunks; chunk 1 of row r overwrites code row r, so each
-// row's codes are read by its 4 lanes before any lane stores.
-__device__ __forceinline__ void convert_kv_slot(uint8_t* slot, int lane) {
-  const int j = lane & 3;             // d range [32 j, 32 j + 32) of the row
-  const int h = j >> 1;               // output 64-column chunk
-#pragma unroll 2
+// 64-column swizzled chunks.  Quarter-warp j (lanes 8j..8j+7) handles d range
+// [32 j, 32 j + 32) of 8 consecutive rows, so the row's swizzle phase r & 7 =
+// lane & 7 is fixed per lane, every address is a per-lane base plus a
+// compile-time offset, and the 8 lanes of a quarter-warp touch 8 distinct
+// 16-byte bank groups on every load and store (conflict free).  Output chunk 1
+// of row r overwrites code row r: the loads of a row group precede its stores
+// (warp barrier); different row groups never overlap, so the loads of group
+// it+1 are issued before the stores of group it.
+__device__ __forceinline__ void convert_kv_slot(uint32_t slot, int lane) {
+  const int j = lane >> 3;            // d range [32 j, 32 j + 32)
+  const int sw = lane & 7;            // row r = 8 it + sw
+  const uint32_t in0 = slot + kChunkBytes + sw * 128 + (((2 * j) ^ sw) << 4);
+  const uint32_t in1 = slot + kChunkBytes + sw * 128 + (((2 * j + 1) ^ sw) << 4);
+  const uint32_t ob = slot + (j >> 1) * kChunkBytes + sw * 128;
+  const int cc = (j & 1) * 4;
+  const uint32_t o0 = ob + (((cc + 0) ^ sw) << 4), o1 = ob + (((cc + 1) ^ sw) << 4),
+                 o2 = ob + (((cc + 2) ^ sw) << 4), o3 = ob + (((cc + 3) ^ sw) << 4);
+  uint4 a = lds128(in0), b = lds128(in1);
+#pragma unroll
   for (int it = 0; it < 16; ++it) {
-    const int r = it * 8 + (lane >> 2);
-    const int sw = r & 7;
-    const uint8_t* in = slot + kChunkBytes + r * 128;
-    const uint4 a = *reinterpret_cast<const uint4*>(in + (((2 * j) ^ sw) << 4));
-    const uint4 b = *reinterpret_cast<const uint4*>(in + (((2 * j + 1) ^ sw) << 4));
-    __syncwarp();
-    uint8_t* out = slot + h * kChunkBytes + r * 128;
-    const int cc = (2 * j & 3) * 2;     // first 16-byte output chunk within the 64 columns
+    asm volatile("bar.warp.sync -1;" ::: "memory");   // group it: all loads before any store
+    uint4 na, nb;
+    if (it < 15) {
+      na = lds128(in0 + (it + 1) * 1024);
+      nb = lds128(in1 + (it + 1) * 1024);
+    }
     const uint2 a0 = e4m3x4_to_f16x4(a.x), a1 = e4m3x4_to_f16x4(a.y), a2 = e4m3x4_to_f16x4(a.z),
                 a3 = e4m3x4_to_f16x4(a.w);
     const uint2 b0 = e4m3x4_to_f16x4(b.x), b1 = e4m3x4_to_f16x4(b.y), b2 = e4m3x4_to_f16x4(b.z),
                 b3 = e4m3x4_to_f16x4(b.w);
-    *reinterpret_cast<uint4*>(out + (((cc + 0) ^ sw) << 4)) = make_uint4(a0.x, a0.y, a1.x, a1.y);
-    *reinterpret_cast<uint4*>(out + (((cc + 1) ^ sw) << 4)) = make_uint4(a2.x, a2.y, a3.x, a3.y);
-    *reinterpret_cast<uint4*>(out + (((cc + 2) ^ sw) << 4)) = make_uint4(b0.x, b0.y, b1.x, b1.y);
-    *reinterpret_cast<uint4*>(out + (((cc + 3) ^ sw) << 4)) = make_uint4(b2.x, b2.y, b3.x, b3.y);
-    __syncwarp();
+    sts128(o0 + it * 1024, make_uint4(a0.x, a0.y, a1.x, a1.y));
+    sts128(o1 + it * 1024, make_uint4(a2.x, a2.y, a3.x, a3.y));
+    sts128(o2 + it * 1024, make_uint4(b0.x, b0.y, b1.x, b1.y));
+    sts128(o3 + it * 1024, make_uint4(b2.x, b2.y, b3.x, b3.y));
+    if (it < 15) { a = na; b = nb; }
   }
 }
 // In-place bf16 -> fp16 of a 32 KB Q tile (same element positions).
-__device__ __forceinline__ void convert_q_tile(uint8_t* q, int lane) {
+__device__ __forceinline__ void convert_q_tile(uint32_t q, int lane) {
 #pragma unroll 4
   for (int i = lane; i < kSlotBytes / 16; i += 32) {
-    uint4 v = reinterpret_cast<uint4*>(q)[i];
+    uint4 v = lds128(q + i * 16);
     v.x = bf16x2_to_f16x2(v.x);
     v.y = bf16x2_to_f16x2(v.y);
     v.z = bf16x2_to_f16x2(v.z);
     v.w = bf16x2_to_f16x2(v.w);
-    reinterpret_cast<uint4*>(q)[i] = v;
+    sts128(q + i * 16, v);
   }
 }
 
@@ -272,7 +294,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       // warp 2: Q tile 0 then the K ring; warp 3: Q tile 1 (two q tiles) then the V ring
       const bool is_k = warp == 2;
       mbar_wait(&bar.q_full, 0);
-      if (is_k || two_q) convert_q_tile(is_k ? q_buf[0] : q_buf[1], lane);
+      if (is_k || two_q) convert_q_tile(smem_u32(is_k ? q_buf[0] : q_buf[1]), lane);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar.q_ready);
@@ -284,18 +306,20 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       for (int e = 0; e < E; ++e) {
         const int s = e % NR;
         mbar_wait(&raw[s], (e / NR) & 1);
-        convert_kv_slot(ring + s * kSlotBytes, lane);
+        convert_kv_slot(smem_u32(ring + s * kSlotBytes), lane);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[s]);
       }
     } else if (warp == 0 || (!F8 && warp == 3)) {
       // ----------------------------------------------------------- TMA producers
-      // warp 0: Q and the K ring; warp 3: the V ring (F8: warp 0 loads both rings)
-      if (elect_one()) {
+      // warp 0: Q and the K ring; warp 3: the V ring.  F8: warps 2-3 convert, so
+      // lane 0 of warp 0 loads Q and the K ring and lane 1 the V ring (two
+      // independent loops in one warp, so K loads run ahead of V as in bf16).
+      if (F8 ? lane < 2 : elect_one()) {
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
-        const bool is_k = warp == 0;
+        const bool is_k = F8 ? lane == 0 : warp == 0;
         if (is_k) {
           const int nq = two_q ? 2 : 1;
           mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
@@ -308,8 +332,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         }
         const int E = nt0 + nt1 - nsh;
         const int m01 = min(nt0, nt1) - nsh;
-        // F8: each event loads K then V (codes: one 128-byte chunk per row, into the
-        // slot's upper half; the converter warps signal k_full / v_full)
+        // F8: codes, one 128-byte chunk per row, into the slot's upper half; the
+        // converter warps signal k_full / v_full
         for (int e = 0; e < E; ++e) {
           int k, j;
           if (e < nsh) { k = 0; j = e; }
@@ -319,9 +343,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           const SegDesc sg = p.segs[w.seg];
           const int tile = w.tile_lo + j;
           const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
-#pragma unroll 1
-          for (int kv = 0; kv < (F8 ? 2 : 1); ++kv) {
-            const bool ik = F8 ? kv == 0 : is_k;
+          {
+            const bool ik = is_k;
             const int NR = ik ? NK : NV;
             uint8_t* ring = ik ? k_base : v_base;
             uint64_t* full = F8 ? (ik ? bar.k_raw : bar.v_raw) : (ik ? bar.k_full : bar.v_full);
