@@ -168,6 +168,14 @@ def oracle_query_sample(n=CFG["n_ctx"], kv_heads=1, q_len=CFG["q_len"]):
     return dt, nbytes
 
 
+def arm_config():
+    """The workload both arms report (BJ.configs[1])."""
+    return {"workload": "BJ.configs[1]: Llama-3-8B-shaped GQA 32/8 d=128 x 32 layers, one session at "
+                        "n=32,512 -> 256-token append -> 32-token query at n=32,768",
+            "page_size": CFG["P"], "l2": "inputs larger than L2 (4.3 GB of KV read per step)",
+            "sessions_per_gpu": 1}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -185,7 +193,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (streams.py market stream)",
-            "config": {"workload": "llama3-8b-shape GQA 32/8 d128, 32-token query at n=32768 (1 layer, 1 KV head sample)"},
+            "config": arm_config(),
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": "fp64 C oracle: one layer, one KV head (4 q heads), 32-token query over 32,768 cached tokens, per step"},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -744,10 +752,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic market-feed stream (streams.py), random K/V/Q of Llama-3-8B attention shapes",
-            "config": {"workload": "BJ.configs[1]: Llama-3-8B-shaped GQA 32/8 d=128 x 32 layers, one session at "
-                                   "n=32,512 -> 256-token append -> 32-token query at n=32,768",
-                       "page_size": P, "l2": "inputs larger than L2 (4.3 GB of KV read per step)",
-                       "sessions_per_gpu": 1},
+            "config": arm_config(),
             "query_latency_us_32_layers": query_call_ms * 1e3,
             "query_latency_us_per_layer": query_call_ms * 1e3 / L,
             "query_hbm_gbs": q_gbs,

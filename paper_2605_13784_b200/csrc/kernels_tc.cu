@@ -126,41 +126,31 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 
 // In-place conversion of one ring slot: codes in [kChunkBytes, 2 kChunkBytes)
 // (128 rows x 128 B, 128-byte swizzle) -> fp16 tile [128 rows][128 d] as two
-// 64-column swizzled chunks.  Quarter-warp j (lanes 8j..8j+7) handles d range
-// [32 j, 32 j + 32) of 8 consecutive rows, so the row's swizzle phase r & 7 =
-// lane & 7 is fixed per lane, every address is a per-lane base plus a
-// compile-time offset, and the 8 lanes of a quarter-warp touch 8 distinct
-// 16-byte bank groups on every load and store (conflict free).  Output chunk 1
-// of row r overwrites code row r: the loads of a row group precede its stores
-// (warp barrier); different row groups never overlap, so the loads of group
-// it+1 are issued before the stores of group it.
+// 64-column swizzled chunks.  Each lane converts whole rows (row 32 it + lane):
+// it loads the row's 128 codes into registers before storing its 256 bytes of
+// fp16, so the in-place overlap (output chunk 1 of row r is code row r) needs no
+// cross-lane ordering and no barrier.  The 8 lanes of a quarter-warp are 8 rows
+// with distinct swizzle phases, so every LDS / STS is bank-conflict free.
+// (Measured alternatives: 4 lanes per row with a warp barrier per
+// row group, half rows per step -- both slower.)
 __device__ __forceinline__ void convert_kv_slot(uint32_t slot, int lane) {
-  const int j = lane >> 3;            // d range [32 j, 32 j + 32)
-  const int sw = lane & 7;            // row r = 8 it + sw
-  const uint32_t in0 = slot + kChunkBytes + sw * 128 + (((2 * j) ^ sw) << 4);
-  const uint32_t in1 = slot + kChunkBytes + sw * 128 + (((2 * j + 1) ^ sw) << 4);
-  const uint32_t ob = slot + (j >> 1) * kChunkBytes + sw * 128;
-  const int cc = (j & 1) * 4;
-  const uint32_t o0 = ob + (((cc + 0) ^ sw) << 4), o1 = ob + (((cc + 1) ^ sw) << 4),
-                 o2 = ob + (((cc + 2) ^ sw) << 4), o3 = ob + (((cc + 3) ^ sw) << 4);
-  uint4 a = lds128(in0), b = lds128(in1);
+  const int sw = lane & 7;
+#pragma unroll 1
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 32 + lane;
+    const uint32_t in = slot + kChunkBytes + r * 128;
+    uint4 x[8];
 #pragma unroll
-  for (int it = 0; it < 16; ++it) {
-    asm volatile("bar.warp.sync -1;" ::: "memory");   // group it: all loads before any store
-    uint4 na, nb;
-    if (it < 15) {
-      na = lds128(in0 + (it + 1) * 1024);
-      nb = lds128(in1 + (it + 1) * 1024);
+    for (int c = 0; c < 8; ++c) x[c] = lds128(in + ((c ^ sw) << 4));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t out = slot + (c >> 2) * kChunkBytes + r * 128;
+      const int cc = 2 * (c & 3);
+      const uint2 a0 = e4m3x4_to_f16x4(x[c].x), a1 = e4m3x4_to_f16x4(x[c].y);
+      const uint2 a2 = e4m3x4_to_f16x4(x[c].z), a3 = e4m3x4_to_f16x4(x[c].w);
+      sts128(out + ((cc ^ sw) << 4), make_uint4(a0.x, a0.y, a1.x, a1.y));
+      sts128(out + (((cc + 1) ^ sw) << 4), make_uint4(a2.x, a2.y, a3.x, a3.y));
     }
-    const uint2 a0 = e4m3x4_to_f16x4(a.x), a1 = e4m3x4_to_f16x4(a.y), a2 = e4m3x4_to_f16x4(a.z),
-                a3 = e4m3x4_to_f16x4(a.w);
-    const uint2 b0 = e4m3x4_to_f16x4(b.x), b1 = e4m3x4_to_f16x4(b.y), b2 = e4m3x4_to_f16x4(b.z),
-                b3 = e4m3x4_to_f16x4(b.w);
-    sts128(o0 + it * 1024, make_uint4(a0.x, a0.y, a1.x, a1.y));
-    sts128(o1 + it * 1024, make_uint4(a2.x, a2.y, a3.x, a3.y));
-    sts128(o2 + it * 1024, make_uint4(b0.x, b0.y, b1.x, b1.y));
-    sts128(o3 + it * 1024, make_uint4(b2.x, b2.y, b3.x, b3.y));
-    if (it < 15) { a = na; b = nb; }
   }
 }
 // In-place bf16 -> fp16 of a 32 KB Q tile (same element positions).
