@@ -240,3 +240,111 @@ def test_fp8_unsupported_paths_fail_loudly(cuda):
         ssa.Store(1, 32, 8, 64, kv_format="e4m3", k_scale=1.0, v_scale=1.0)      # head_dim 64
     with pytest.raises(ssa.SsaError):
         ssa.Store(1, 32, 8, 128, kv_format="e4m3", k_scale=0.0, v_scale=1.0)     # scale must be > 0
+
+
+def test_fp8_retention_alias_and_read_back(cuda):
+    """Store paths that move pages on an E4M3 pool (1-byte elements): retention eviction,
+    prefix aliasing with the one-page copy, destroy / reuse -- codes, page tables and digests
+    bit-exact, attention within tolerance."""
+    import torch
+    spec = streams.StreamSpec("peaked", seed=38)
+    L, P = 2, 64
+    st, ref = _pair(L, P, 128)
+    Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 0, 0, 100)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    rsid, _ = ref.session_create(100, Q, K, V)
+    st.set_retention(sid, 700)
+    ref.set_retention(rsid, 700)
+    tok = 100
+    for m in (300, 256, 200, 37):
+        Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 0, tok, m)
+        O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+        Oref, _ = ref.session_append(rsid, Q, K, V)
+        ok, e = within(from_dev(O), Oref, "bf16")
+        assert ok, (m, e)
+        assert st.page_table(sid) == ref.page_table(rsid) and st.info(sid) == ref.info(rsid)
+        tok += m
+    assert st.info(sid)["n_evicted"] > 0
+    n_keep = ref.info(rsid)["n_tokens"]
+    Kb, Vb = st.read_kv(sid, 1, 0, n_keep)
+    assert np.array_equal(Kb, ref.sessions[rsid].k[1][:n_keep]) and np.array_equal(Vb, ref.sessions[rsid].v[1][:n_keep])
+    # aliasing on a fresh donor (no eviction): shared pages + copied partial page
+    Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 0, 0, 500, session=1)
+    d0 = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    r0, _ = ref.session_create(500, Q, K, V, compute=False)
+    g, r = st.alias_prefix(d0, 333), ref.alias_prefix(r0, 333)
+    assert st.page_table(g) == ref.page_table(r) and st.digest(g) == ref.digest(r)
+    Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 7, 0, 45, session=1)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_append(g, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    Oref, _ = ref.session_append(r, Q, K, V)
+    ok, e = within(from_dev(O), Oref, "bf16")
+    assert ok, e
+    st.session_destroy(d0)
+    ref.session_destroy(r0)
+    assert st.digest(g) == ref.digest(r) and st.occupancy() == ref.occupancy()
+    st.close()
+
+
+def test_fp8_per_layer_and_host_buffers(cuda):
+    """Per-layer tickets == one all-layer append; pageable host buffers (the pipelined
+    all-layer path) == device buffers, on an E4M3 store."""
+    import torch
+    spec = streams.StreamSpec("market", seed=39)
+    L = 3
+    a, _ = _pair(L, 64, 64)
+    b, _ = _pair(L, 64, 64)
+    Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 0, 0, 200)
+    sa = a.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    sb = b.session_create(None, K, V)                   # host inputs
+    Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 0, 200, 90)
+    Oa = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    a.session_append(sa, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), Oa)
+    t = b.append_begin(sb, 90)
+    Ob = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    for l in range(L):
+        b.append_layer(sb, t, l, to_dev(Q[l:l + 1], cuda), to_dev(K[l:l + 1], cuda), to_dev(V[l:l + 1], cuda),
+                       Ob[l:l + 1])
+    b.append_commit(sb, t)
+    assert torch.equal(Oa.view(torch.int16), Ob.view(torch.int16))
+    assert a.digest(sa) == b.digest(sb)
+    Qq, Kq, Vq = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
+    Od = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    a.session_query(sa, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Od)
+    Oh = np.zeros(Qq.shape, dtype=np.uint16)
+    b.session_query(sb, Qq, Kq, Vq, Oh)
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(Od), Oh)
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fp8_sharded_partials_merge(cuda, world):
+    """A9 on E4M3 shards: rank partials + log-sum-exp merge == the unsharded e4m3 oracle."""
+    import torch
+    from paper_2605_13784_b200.sharding import shard_range
+    spec = streams.StreamSpec("market", seed=40)
+    L, n, nq = 2, 3001, 32
+    Q, K, V = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 0, 0, n)
+    _, ref = _pair(L, 64, 64)
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    Qq, Kq, Vq = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 1, 0, nq)
+    rows = L * nq
+    parts = torch.empty((world, rows * LL["hq"] * (LL["d"] + 1)), dtype=torch.float32, device=cuda)
+    stores = []
+    for r in range(world):
+        lo, hi = shard_range(n, r, world)
+        st, _ = _pair(L, 64, 64)
+        sid = st.session_create(None, to_dev(K[:, lo:hi], cuda), to_dev(V[:, lo:hi], cuda))
+        st.sharded_partial(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), parts[r],
+                           include_tail=(r == world - 1))
+        stores.append(st)
+    O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    stores[0].merge_rank_partials(world, rows, parts, O)
+    ok, e = within(from_dev(O), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, e
+    for st in stores:
+        st.close()
