@@ -446,6 +446,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       const int G = p.G;
       const int tok = w.q_tok0 + r / G;
       const int last_key = min(sg.tail_m - 1, p.fault == 2 ? tok - 1 : tok);   // own keys 0..tok (R-2)
+      // rows >= q_ntok * G of the 128-row tile are padding (1-token GQA query: 4 live rows); a
+      // warp whose 32 rows are all padding skips S loads, softmax and P stores (MUFU is the
+      // query plane's co-bottleneck), but still waits for each S before arriving on p_full so
+      // the barrier phases stay in order.  Its P columns keep stale values that only reach
+      // the O rows of its own (discarded) lanes.
+      const bool warp_dead = (warp & 3) * 32 >= w.q_ntok * G;
       const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
       float m_run = -CUDART_INF_F;
       float l_run = 0.f;
@@ -456,6 +462,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         mbar_wait(&bar.s_full[k], j & 1);
         TRACE(r == 0, k, j, 0, clock64());
         tc_fence_after();
+        if (!warp_dead) {   // a warp with no live row (|q| * G <= 96) only keeps the handoff order
         float sv[kBN];
         {
           uint32_t ra[32], rb[32], rc[32], rd[32];
@@ -550,6 +557,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           tmem_st32(s_col + 32, hi);
         }
         tmem_wait_st();
+        }
         TRACE(r == 0, 6 + k, j, 1, clock64());
         tc_fence_before();
         __syncwarp();
