@@ -342,7 +342,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
             const CUtensorMap* pool_map = ik ? &maps.pk : &maps.pv;
             const CUtensorMap* tail_map = ik ? &maps.kt : &maps.vt;
             const int s = e % NR;
-            if (e >= NR) mbar_wait(&empty[s], ((e / NR) - 1) & 1);
+            if (e >= NR) mbar_wait_lazy(&empty[s], ((e / NR) - 1) & 1);
             uint8_t* dst = ring + s * kSlotBytes + (F8 ? kChunkBytes : 0);
             constexpr int nchunk = F8 ? 1 : 2;
             mbar_arrive_expect_tx(&full[s], nchunk * kChunkBytes);
