@@ -224,6 +224,20 @@ def build_session_n(st, torch, dev, spec, n, chunk=4096, session=0):
     return sid
 
 
+def extend_session(st, sid, torch, dev, spec, n_from, n_to, chunk=4096, session=0):
+    """Bulk-import the session's tokens [n_from, n_to) again (after a SeqRemove)."""
+    import streams
+    tok = n_from
+    while tok < n_to:
+        m = min(chunk, n_to - tok)
+        K = torch.stack([streams.gen_tensor_torch(spec, session, 0, l, streams.TENSOR_K, tok, m, CFG["hkv"],
+                                                  CFG["d"], device=dev) for l in range(CFG["L"])])
+        V = torch.stack([streams.gen_tensor_torch(spec, session, 0, l, streams.TENSOR_V, tok, m, CFG["hkv"],
+                                                  CFG["d"], device=dev) for l in range(CFG["L"])])
+        st.load_kv(sid, K, V)
+        tok += m
+
+
 def gen_new(torch, dev, spec, domain, tok0, m, session=0):
     import streams
     out = []
@@ -271,6 +285,43 @@ def leg_flash(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_ctx):
             "tc_frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
             "ms_64_separate_queries": sep, "speedup_vs_separate": sep / ms,
             "paper_context": "paper T_f ~30-35 ms per Flash Query on L40S, full 8B forward (P:484)"}
+
+
+def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq):
+    """BJ.configs[1] curves vs context n: the same session truncated (SeqRemove)
+    to n in {4k, 8k, 16k, 32,512}; per n the 32-token query and the 256-token append over
+    32 layers (kernel CUDA events, as the headline), as GB/s and TFLOP/s of their algorithmic
+    bytes / FLOPs.  Runs right after the headline region (before the heavy legs)."""
+    import paper_2605_13784_b200 as ssa
+    L, hq, hkv, d = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"]
+    out = {"workload": "BJ.configs[1] session truncated to n; 32-token query / 256-token append, 32 layers"}
+    for n in (n_top, 16384, 8192, 4096):
+        st.session_truncate(sid, n)
+        st.set_option(ssa.OPT_TIMING, 1)
+        st.timing(reset=True)
+        _timed(torch, stream, lambda: st.session_query(sid, Qq, Kq, Vq, Oq, stream=stream), steps, 0)
+        tq = st.timing(reset=True)
+        st.set_option(ssa.OPT_TIMING, 0)
+        # device time of the query call (attention + combine), as the headline `value`
+        qms = (tq["attn_query"][0] + tq["combine_query"][0]) / max(1, tq["attn_query"][1])
+
+        def app():
+            st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)
+            st.session_truncate(sid, n)
+        st.set_option(ssa.OPT_TIMING, 1)
+        st.timing(reset=True)
+        _timed(torch, stream, app, steps, warmup)
+        tm = st.timing(reset=True)
+        st.set_option(ssa.OPT_TIMING, 0)
+        a_ms = tm["attn_data"][0] / max(1, tm["attn_data"][1])
+        qb = query_bytes_per_layer(n, CFG["q_len"], hq, hkv, d) * L
+        af = append_flops_per_layer(n, CFG["m_append"], hq, d) * L
+        out[f"n{n}"] = {"query_us_32_layers": qms * 1e3, "query_gbs": qb / (qms * 1e-3) / 1e9,
+                        "query_hbm_frac": qb / (qms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                        "append_attn_ms": a_ms, "append_tflops": af / (a_ms * 1e-3) / 1e12,
+                        "append_tc_frac": af / (a_ms * 1e-3) / 1e12 / peaks["bf16_tflops"]}
+    st.session_truncate(sid, 4096)
+    return out
 
 
 def leg_multitenant(torch, dev, stream, peaks, steps, warmup):
@@ -662,6 +713,20 @@ def run_ours(args):
     a_tflops = a_flops / (attn_a_ms * 1e-3) / 1e12
     append_tok_s = m_app / (append_call_ms * 1e-3)
 
+    # ---- host-side cost of a call (planning, descriptor upload, launches): wall time to enqueue
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(20):
+        st.session_query(sid, Qq, Kq, Vq, Oq, stream=stream)
+    host_q_us = (time.perf_counter() - t0) / 20 * 1e6
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)
+        st.session_truncate(sid, n0)
+    host_a_us = (time.perf_counter() - t0) / 10 * 1e6
+    torch.cuda.synchronize()
+
     # ---- end-to-end through the C ABI with host (pinned) buffers
     hQ, hK, hV = (x.cpu().pin_memory() for x in (Qq, Kq, Vq))
     hO = torch.empty(Oq.shape, dtype=Oq.dtype).pin_memory()
@@ -693,10 +758,15 @@ def run_ours(args):
             legs[name] = {"error": f"{type(exc).__name__}: {exc}"}
 
     peaks_l, _ = load_peaks()
+    if world == 1 and "nsweep" in want:   # truncates the session to 4k, then restores it to n0
+        guarded("context_sweep", lambda: leg_nsweep(st, sid, torch, dev, spec, stream, peaks_l, 3, 1, n0,
+                                                    Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq))
+        extend_session(st, sid, torch, dev, spec, st.info(sid)["n_tokens"], n0)
     if world == 1 and "flash" in want:
         st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # the 256-token update, n -> 32,768
         guarded("flash_queries", lambda: leg_flash(st, sid, torch, dev, spec, stream, peaks_l, 3, 1, n_ctx))
         st.session_truncate(sid, n0)
+
     st.close()
     del Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq
     torch.cuda.empty_cache()
@@ -765,6 +835,8 @@ def run_ours(args):
             "roofline_query": roof_query,
             "roofline_append": roof_append,
             "gpu_launches": launches,
+            "host_us_per_call": {"query": host_q_us, "append_and_truncate": host_a_us,
+                                 "what": "CPU wall time to enqueue one 32-layer call (plan, upload, launches)"},
             "clocks": clocks,
             "e2e": {"value": q_bytes / (e2e_ms * 1e-3) / 1e9 * world, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_query": e2e_ms,
@@ -792,7 +864,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--legs", default="flash,tenant,speedup,argmax,qkv,fp8,split",
+    ap.add_argument("--legs", default="flash,nsweep,tenant,speedup,argmax,qkv,fp8,split",
                     help="extra single-GPU legs (configs 3-5) reported in the same JSON line; '' to skip")
     args = ap.parse_args()
     if args.warmup < 3:
