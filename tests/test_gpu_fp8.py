@@ -348,3 +348,35 @@ def test_fp8_sharded_partials_merge(cuda, world):
     assert ok, e
     for st in stores:
         st.close()
+
+
+@pytest.mark.parametrize("opt", ["fused_merge", "max_splits_16", "q_tiles_1"])
+def test_fp8_kernel_options(cuda, opt):
+    """E4M3 store under the kernel options: in-kernel split merge, a high split cap, one q tile
+    per CTA -- append and query parity."""
+    import torch
+    ssa = _ssa()
+    spec = streams.StreamSpec("market", seed=41)
+    st, ref = _pair(2, 64, 256)
+    if opt == "fused_merge":
+        st.set_option(ssa.OPT_FUSED_MERGE, 1)
+    elif opt == "max_splits_16":
+        st.set_option(ssa.OPT_MAX_SPLITS, 16)
+    else:
+        st.set_option(ssa.OPT_TC_Q_TILES, 1)
+    Q, K, V = gen_qkv(spec, 2, LL["hq"], LL["hkv"], LL["d"], 0, 0, 3000)
+    sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    rsid, _ = ref.session_create(3000, Q, K, V, compute=False)
+    Q, K, V = gen_qkv(spec, 2, LL["hq"], LL["hkv"], LL["d"], 0, 3000, 200)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    Oref, _ = ref.session_append(rsid, Q, K, V)
+    ok, e = within(from_dev(O), Oref, "bf16")
+    assert ok, ("append", e)
+    for nq in (1, 32):
+        Qq, Kq, Vq = gen_qkv(spec, 2, LL["hq"], LL["hkv"], LL["d"], 1, 0, nq)
+        Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+        st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+        ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+        assert ok, ("query", nq, e)
+    st.close()
