@@ -15,12 +15,15 @@
 // TMEM (512 columns): slot k uses [256k, 256k+128) for S/P and
 // [256k+128, 256k+256) for O.  The running max is updated lazily (only when it
 // grows by more than 8 in log2 units), so O is rarely rescaled.
-// Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM
-// allocator, warps 4-7 softmax slot 0, warps 8-11 softmax slot 1.
+// Warp roles (384 threads): warp 0 TMA producer of Q and the K ring, warp 3 TMA
+// producer of the V ring, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7
+// softmax slot 0, warps 8-11 softmax slot 1.  A warp whose 32 rows are all
+// padding (a 1-token GQA query fills 4 of 128 rows) skips its softmax.
 //
 // FP8 KV variant (template F8, reading R-22): the pools and
-// the call's own K/V hold E4M3 codes.  Warp 0 loads every K and V tile (16 KB of
-// codes) into the upper half of its 32 KB ring slot; warp 2 (K) and warp 3 (V)
+// the call's own K/V hold E4M3 codes.  Lanes 0 / 1 of warp 0 load the K / V
+// tiles (16 KB of codes) into the upper half of their 32 KB ring slots; warp 2
+// (K) and warp 3 (V)
 // convert the codes in place to fp16 in the same 128-byte-swizzled layout the
 // bf16 tiles use (cvt.rn.f16x2.e4m3x2 is exact), and the MMAs run kind::f16 with
 // fp16 operands: Q is converted bf16 -> fp16 in smem once per CTA, P is packed
