@@ -285,7 +285,8 @@ ssa_status ssa_batch_run(ssa_store_t store, int32_t layer, int32_t n_items,
  * ssa_append_layer_fused: the per-layer append of an open ticket (as
  *   ssa_append_layer) whose Q/K/V come from X: positions continue the session
  *   (n_tokens + evicted tokens, never re-based, R-8); the projection epilogue
- *   writes K and V straight into the ticket's pages (no scatter launch), then
+ *   writes K and V straight into the ticket's pages (no scatter launch; E4M3
+ *   codes of the bf16-rounded values on an SSA_KV_E4M3 store), then
  *   the data-plane attention writes O [n_new][Hq][d].
  * ssa_session_query_fused: ssa_session_query for one layer with Q/K/V from
  *   X [n_q][hidden] at the positions after the cache; no state change.

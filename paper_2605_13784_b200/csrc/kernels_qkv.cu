@@ -62,6 +62,22 @@ struct QkvMaps {
   CUtensorMap w;   // [Nout][hidden]   box {64, 256}
 };
 
+// Four bf16 values (packed pairs) -> four E4M3 codes of value / scale: the quotient
+// rounded once in fp32, then cvt.rn.satfinite (reading R-22; the same arithmetic as
+// quant_e4m3_kernel, so pages written here equal pages the scatter writes).
+__device__ __forceinline__ uint32_t e4m3x4_of_bf16(uint2 v, float scale) {
+  const float a = __fdiv_rn(__uint_as_float(v.x << 16), scale);
+  const float b = __fdiv_rn(__uint_as_float(v.x & 0xFFFF0000u), scale);
+  const float c = __fdiv_rn(__uint_as_float(v.y << 16), scale);
+  const float d = __fdiv_rn(__uint_as_float(v.y & 0xFFFF0000u), scale);
+  uint32_t lo, hi;
+  asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %1;\n\tcvt.u32.u16 %0, t;\n\t}"
+      : "=r"(lo) : "f"(a), "f"(b));
+  asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %1;\n\tcvt.u32.u16 %0, t;\n\t}"
+      : "=r"(hi) : "f"(c), "f"(d));
+  return lo | (hi << 16);
+}
+
 __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -364,7 +380,11 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
             const int64_t slot = (int64_t)p.slot0 + t;
             const int64_t page = __ldg(p.pages + slot / p.P);
             const int64_t prow = ((p.page_base + page) * p.Hkv + kh) * p.P + slot % p.P;
-            *reinterpret_cast<uint2*>(static_cast<uint8_t*>(pool) + (prow * kHeadD + dcol) * 2) = packed;
+            if (p.kv_fp8)   // E4M3 pool (R-22): codes of the bf16-rounded values, as the quantize kernel
+              *reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(pool) + prow * kHeadD + dcol) =
+                  e4m3x4_of_bf16(packed, is_v ? p.v_scale : p.k_scale);
+            else
+              *reinterpret_cast<uint2*>(static_cast<uint8_t*>(pool) + (prow * kHeadD + dcol) * 2) = packed;
           }
         }
       }

@@ -196,6 +196,8 @@ struct QkvParams {
   const int32_t* pages;   // device page table of the session (slot / P -> page)
   int64_t page_base;      // layer * num_pages
   int32_t slot0, P;       // slot of token row 0
+  int32_t kv_fp8;         // paged destination holds E4M3 codes of x / k_scale, x / v_scale (R-22)
+  float k_scale, v_scale;
   int32_t splits;         // split-K factor = thread-block cluster size
   int32_t debug;          // experiments (SSA_QKV_DEBUG): 1 = skip the reduce / RoPE / store epilogue
   uint64_t* trace;        // experiments: per-CTA %globaltimer stamps [grid][8], or null

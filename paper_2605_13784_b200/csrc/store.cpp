@@ -1642,6 +1642,9 @@ static ssa_status qkv_launch(ssa_store* st, int32_t n, int32_t hidden, int64_t p
     qp.page_base = (int64_t)layer * st->cfg.num_pages;
     qp.slot0 = (int32_t)slot0;
     qp.P = st->cfg.page_size;
+    qp.kv_fp8 = st->kv_fp8 ? 1 : 0;
+    qp.k_scale = st->cfg.k_scale;
+    qp.v_scale = st->cfg.v_scale;
   }
   qp.splits = qkv_choose_splits(n, qp.Hq + 2 * qp.Hkv, hidden, st->num_sms);
   if (const char* e = getenv("SSA_QKV_DEBUG")) qp.debug = atoi(e);
@@ -1686,10 +1689,6 @@ ssa_status ssa_append_layer_fused(ssa_store_t st, ssa_session_t id, int32_t tick
   if (!s) return rc;
   if (layer < 0 || layer >= st->cfg.num_layers || !dev_ok(O, stream)) return SSA_ERR_INVALID_ARG;
   if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
-  if (st->kv_fp8) {   // the projection epilogue stores bf16 K/V into the pages
-    set_error("ssa_append_layer_fused: not available for an E4M3 KV store (use ssa_qkv_rope + ssa_append_layer)");
-    return SSA_ERR_UNSUPPORTED;
-  }
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
   const int32_t n_new = s->ticket_n_new;

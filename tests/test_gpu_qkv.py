@@ -168,3 +168,57 @@ def test_fused_rejects_bad_arguments(cuda):
     with pytest.raises(ssa.SsaError):
         st.qkv_rope(Xh, Wd, Q, K, K)
     st.close()
+
+
+def test_fused_append_e4m3_store(cuda):
+    """Fused projection into an E4M3 store (R-22): the epilogue writes codes of the
+    bf16-rounded K/V; they, the digest and the attention output are bit-identical to the
+    unfused path (dense projection -> quantize kernel -> scatter), and O matches the e4m3
+    oracle fed with the projection's bf16 values."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, hidden, theta, P = 2, 8, 2, 128, 512, 500000.0, 64
+    kw = dict(page_size=P, num_pages=128, max_sessions=2, dtype="bf16", kv_format="e4m3",
+              k_scale=1 / 16, v_scale=1 / 16)
+    a = ssa.Store(L, hq, hkv, d, **kw)        # fused
+    b = ssa.Store(L, hq, hkv, d, **kw)        # unfused reference path
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=128, kv_format="e4m3",
+                             k_scale=1 / 16, v_scale=1 / 16)
+    spec = streams.StreamSpec("peaked", seed=12)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 100)
+    sa = a.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    sb = b.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    rs, _ = ref.session_create(100, Q, K, V, compute=False)
+    W = [streams.gen_qkv_weight(6, l, (hq + 2 * hkv) * d, hidden) for l in range(L)]
+    Wd = [to_dev(w, cuda) for w in W]
+    pos, n = 100, 77
+    X = [streams.gen_hidden(6, 0, 0, l, pos, n, hidden) for l in range(L)]
+    ta, tb = a.append_begin(sa, n), b.append_begin(sb, n)
+    Oa, Ob = [], []
+    for l in range(L):
+        o = torch.empty((n, hq, d), dtype=torch.bfloat16, device=cuda)
+        a.append_layer_fused(sa, ta, l, to_dev(X[l], cuda), Wd[l], o, rope_theta=theta)
+        Oa.append(o)
+        Qd = torch.empty((n, hq, d), dtype=torch.bfloat16, device=cuda)
+        Kd = torch.empty((n, hkv, d), dtype=torch.bfloat16, device=cuda)
+        Vd = torch.empty_like(Kd)
+        b.qkv_rope(to_dev(X[l], cuda), Wd[l], Qd, Kd, Vd, pos0=pos, rope_theta=theta)
+        o2 = torch.empty_like(o)
+        b.append_layer(sb, tb, l, Qd[None], Kd[None], Vd[None], o2[None])
+        Ob.append(o2)
+    a.append_commit(sa, ta)
+    b.append_commit(sb, tb)
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert torch.equal(Oa[l].view(torch.int16), Ob[l].view(torch.int16)), l
+        ka, va = a.read_kv(sa, l, 0, 100 + n)
+        kb, vb = b.read_kv(sb, l, 0, 100 + n)
+        assert np.array_equal(ka, kb) and np.array_equal(va, vb), l
+    assert a.digest(sa) == b.digest(sb)
+    Qr, Kr, Vr = _oracle_layers(X, W, hq, hkv, pos, theta)
+    Oref, _ = ref.session_append(rs, Qr, Kr, Vr)
+    mx, mn = errors(np.stack([from_dev(o) for o in Oa]), Oref)
+    assert mx <= TOL["bf16"][0] and mn <= TOL["bf16"][1], (mx, mn)
+    assert a.digest(sa) == ref.digest(rs)
+    a.close()
+    b.close()
