@@ -324,6 +324,30 @@ def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Q
     return out
 
 
+def leg_graph(st, sid, torch, stream, Qq, Kq, Vq, steps, warmup):
+    """SURVEY §8(d) "query latency per layer and for 32 layers (CUDA graph)": the 32-token query
+    as 32 single-layer calls (the form a real model issues, one per layer), eager and captured
+    into one CUDA graph (work lists in the store's graph arena), vs the one all-layer call."""
+    L = CFG["L"]
+    O = torch.empty_like(Qq)
+
+    def per_layer(s):
+        for l in range(L):
+            st.session_query(sid, Qq[l:l + 1], Kq[l:l + 1], Vq[l:l + 1], O[l:l + 1], layer=l, stream=s)
+    per_layer(stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        per_layer(torch.cuda.current_stream())
+    ms_graph = _timed(torch, stream, g.replay, steps, warmup)
+    ms_eager = _timed(torch, stream, lambda: per_layer(stream), steps, warmup)
+    ms_all = _timed(torch, stream, lambda: st.session_query(sid, Qq, Kq, Vq, O, stream=stream), steps, warmup)
+    return {"workload": "BJ.configs[1] 32-token query at n=32,768 as 32 per-layer calls",
+            "graph_ms_32_layers": ms_graph, "graph_us_per_layer": ms_graph * 1e3 / L,
+            "eager_ms_32_layers": ms_eager, "all_layer_call_ms": ms_all,
+            "note": "stream-timed (CUDA events around the replay / the calls), host gaps included"}
+
+
 def leg_multitenant(torch, dev, stream, peaks, steps, warmup):
     """BJ.configs[2]: 48 sessions of 4k-16k context; one launch (all 32 layers) packs 24 appends of 256,
     24 queries of 32 and 4 stateless 1024-token prompts (snapshot semantics, R-7)."""
@@ -762,6 +786,10 @@ def run_ours(args):
         guarded("context_sweep", lambda: leg_nsweep(st, sid, torch, dev, spec, stream, peaks_l, 3, 1, n0,
                                                     Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq))
         extend_session(st, sid, torch, dev, spec, st.info(sid)["n_tokens"], n0)
+    if world == 1 and "graph" in want:
+        st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # n -> 32,768 as in the headline query
+        guarded("query_graph", lambda: leg_graph(st, sid, torch, stream, Qq, Kq, Vq, 10, 3))
+        st.session_truncate(sid, n0)
     if world == 1 and "flash" in want:
         st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # the 256-token update, n -> 32,768
         guarded("flash_queries", lambda: leg_flash(st, sid, torch, dev, spec, stream, peaks_l, 3, 1, n_ctx))
@@ -864,7 +892,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--legs", default="flash,nsweep,tenant,speedup,argmax,qkv,fp8,split",
+    ap.add_argument("--legs", default="graph,flash,nsweep,tenant,speedup,argmax,qkv,fp8,split",
                     help="extra single-GPU legs (configs 3-5) reported in the same JSON line; '' to skip")
     args = ap.parse_args()
     if args.warmup < 3:

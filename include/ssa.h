@@ -45,6 +45,15 @@
  *   NO state change; page reservation is all-or-none.  A CUDA or NCCL failure
  *   marks the store failed (sticky): every later call returns SSA_ERR_STATE.
  *   ssa_last_error() returns a message for the calling thread's last error.
+ * CUDA graphs.  Query-plane calls (ssa_session_query, ssa_flash_query_batch,
+ *   ssa_batch_run without APPEND items, the sharded partial/push/merge) may be
+ *   captured into a CUDA graph on a capturing `stream` with DEVICE pointers: the
+ *   work list goes to a persistent store-owned arena (4 MiB), so a replay repeats
+ *   the call as planned at capture time (cache length and page table of that
+ *   moment; re-capture after the session changes).  Run the call once before
+ *   capturing (scratch buffers are sized on first use).  Calls that change the
+ *   store (create, append, load, evict, alias) return SSA_ERR_STATE while the
+ *   stream is capturing, with no state change.
  * Threading.  One host thread at a time per store (external serialization —
  *   the paper's single dispatch worker).  Distinct stores are
  *   independent.  Sessions never see each other's keys.

@@ -184,16 +184,17 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
 // w_s = 2^(lse_s - L) / sum_s 2^(lse_s - L) are computed once into smem, then
 // the 128-bit-vectorized weighted sum runs over all (row, 4-column) pairs.
 // Partials carry normalized o_s and lse_s in log2 units (reading R-11).
-constexpr int kCombineRows = 32;   // rows of a group per combine CTA
+constexpr int kCombineRows = 32;   // rows of a group per combine CTA (max; fewer for small launches)
 
 template <typename T>
 __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
-  extern __shared__ float wsm[];                       // [n_splits][kCombineRows]
-  const int g = blockIdx.x, ly = blockIdx.y, r0 = blockIdx.z * kCombineRows;
+  extern __shared__ float wsm[];                       // [n_splits][CR]
+  const int CR = p.combine_rows;
+  const int g = blockIdx.x, ly = blockIdx.y, r0 = blockIdx.z * CR;
   const Group gr = p.groups[g];
   const int rows = gr.q_ntok * p.G;
   if (r0 >= rows) return;
-  const int nr = min(kCombineRows, rows - r0);
+  const int nr = min(CR, rows - r0);
   const SegDesc sg = p.segs[gr.seg];
   const int RT = p.rows_tile;
   const int64_t slot0 = (int64_t)ly * p.n_units + gr.unit0;
@@ -206,11 +207,11 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
     for (int s = 0; s < NS; ++s) {
       const float ls = p.part_lse[(slot0 + s) * RT + r];
       const float w = ls == -CUDART_INF_F ? 0.f : exp2f(ls - L);
-      wsm[s * kCombineRows + rr] = w;
+      wsm[s * CR + rr] = w;
       wsum += w;
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-    for (int s = 0; s < NS; ++s) wsm[s * kCombineRows + rr] *= inv;
+    for (int s = 0; s < NS; ++s) wsm[s * CR + rr] *= inv;
     if (p.lse_out || p.n_peers > 0) {
       const int64_t row = (p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0) + sg.row0 + gr.q_tok0 + r / p.G;
       const float lse = wsum > 0.f ? L + log2f(wsum) : -CUDART_INF_F;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
       for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (s + u) * split_stride4);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float w = wsm[(s + u) * kCombineRows + rr];
+        const float w = wsm[(s + u) * CR + rr];
         acc.x = fmaf(w, v[u].x, acc.x);
         acc.y = fmaf(w, v[u].y, acc.y);
         acc.z = fmaf(w, v[u].z, acc.z);
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
       }
     }
     for (; s < NS; ++s) {
-      const float w = wsm[s * kCombineRows + rr];
+      const float w = wsm[s * CR + rr];
       const float4 v = __ldcs(src + s * split_stride4);
       acc.x = fmaf(w, v.x, acc.x);
       acc.y = fmaf(w, v.y, acc.y);
@@ -458,15 +459,21 @@ cudaError_t launch_attn_simt(const AttnParams& p, int n_layers, bool bf16, cudaS
 
 cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cudaStream_t s, int max_splits) {
   if (p.n_groups == 0 || n_layers == 0) return cudaSuccess;
-  dim3 grid(p.n_groups, n_layers, (p.rows_tile + kCombineRows - 1) / kCombineRows);
-  const size_t smem = sizeof(float) * (size_t)max_splits * kCombineRows;
+  // rows per CTA: 32, or down to 8 when the launch would not fill the SMs (a single-layer
+  // query: 8 groups x 4 row blocks = 32 CTAs at 32 rows, 128 at 8)
+  CombineParams q = p;
+  q.combine_rows = kCombineRows;
+  while (q.combine_rows > 8 && (int64_t)p.n_groups * n_layers * ((p.rows_tile + q.combine_rows - 1) / q.combine_rows) < 2 * 148)
+    q.combine_rows /= 2;
+  dim3 grid(p.n_groups, n_layers, (p.rows_tile + q.combine_rows - 1) / q.combine_rows);
+  const size_t smem = sizeof(float) * (size_t)max_splits * q.combine_rows;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(bf16 ? (const void*)combine_kernel<__nv_bfloat16> : (const void*)combine_kernel<float>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  if (bf16) combine_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(p);
-  else combine_kernel<float><<<grid, 256, smem, s>>>(p);
+  if (bf16) combine_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(q);
+  else combine_kernel<float><<<grid, 256, smem, s>>>(q);
   return cudaGetLastError();
 }
 

@@ -142,6 +142,7 @@ struct GatherParams {
 
 // Merge of split partials into O.
 struct CombineParams {
+  int32_t combine_rows;  // rows of a group per CTA (set by launch_combine)
   const float* part_o;
   const float* part_lse;
   void* O;

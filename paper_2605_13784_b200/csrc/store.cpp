@@ -339,8 +339,14 @@ void ssa_store::fill_cached(const Session& s, SegDesc* sg) const {
   sg->n_pages = (int32_t)s.pages.size();
 }
 
+static bool capturing(void* stream);
+
 ssa_status ssa_store::ensure_scratch(size_t part_o_floats, size_t part_lse_floats, cudaStream_t st) {
   if (part_o_floats > part_o_cap || part_lse_floats > part_lse_cap) {
+    if (capturing(st)) {
+      ssa::set_error("CUDA-graph capture: warm up the call once before capturing (split-KV scratch)");
+      return SSA_ERR_STATE;
+    }
     SSA_CUDA(this, cudaStreamSynchronize(st));
     SSA_CUDA(this, cudaDeviceSynchronize());
     if (part_o) cudaFree(part_o);
@@ -387,14 +393,16 @@ ssa_status ssa_store::stage_inputs(IoSet* io, cudaStream_t st) {
 }
 
 ssa_status ssa_store::stage_plan(IoSet* io, cudaStream_t st) {
-  (void)st;
-  // Place every host pointer of the call in one device staging buffer.
+  // Place every host pointer of the call in one device staging buffer.  A call
+  // being captured into a CUDA graph must pass device pointers (pointer queries
+  // would invalidate a global-mode capture), so they are taken as such.
+  const bool cap = capturing(st);
   size_t need = 0;
   auto plan_one = [&](IoBuf& b) {
     b.dev = nullptr;
     b.host = nullptr;
     if (!b.user || b.bytes == 0) return;
-    if (is_device_ptr(b.user)) { b.dev = const_cast<void*>(b.user); return; }
+    if (cap || is_device_ptr(b.user)) { b.dev = const_cast<void*>(b.user); return; }
     b.host = const_cast<void*>(b.user);
     b.stage_off = need;
     need += (b.bytes + 255) & ~size_t(255);
@@ -528,7 +536,13 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     app_segs.push_back(segs[i]);
     prefix.push_back(prefix.back() + segs[i].m);
   }
-  // ---- upload descriptors through the ring (one span)
+  // ---- upload descriptors through the ring (one span); a call being captured
+  // into a CUDA graph takes a persistent span of the graph arena instead
+  const bool cap = capturing(st);
+  if (cap && ((!app_segs.empty() && !opts.skip_scatter) || opt_timing)) {
+    ssa::set_error("CUDA-graph capture: only query-plane calls can be captured (and not with SSA_OPT_TIMING)");
+    return SSA_ERR_STATE;
+  }
   const size_t b_segs = segs.size() * sizeof(SegDesc);
   const size_t b_units = plan.units.size() * sizeof(WorkUnit);
   const size_t b_groups = plan.groups.size() * sizeof(Group);
@@ -538,14 +552,26 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   const size_t b_pairs2 = pairs2.size() * sizeof(TcPair);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre) + al(b_pairs) + al(b_pairs2);
-  const size_t off = ring.alloc(total);
-  if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
+  size_t off = 0;
+  if (cap) {
+    if (arena_used + total > arena_cap) {
+      ssa::set_error("CUDA-graph capture: graph arena exhausted (%zu of %zu bytes used)", arena_used, arena_cap);
+      return SSA_ERR_STATE;
+    }
+    off = arena_used;
+    arena_used += total;
+  } else {
+    off = ring.alloc(total);
+    if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
+  }
+  char* const host_base = cap ? arena_h : ring.host(0);
+  char* const dev_base = cap ? arena_d : ring.dev(0);
   size_t o = off;
   auto put = [&](const void* src, size_t b) {
     const size_t here = o;
-    if (b) memcpy(ring.host(here), src, b);
+    if (b) memcpy(host_base + here, src, b);
     o += al(b);
-    return ring.dev(here);
+    return dev_base + here;
   };
   auto d_segs = reinterpret_cast<const SegDesc*>(put(segs.data(), b_segs));
   auto d_units = reinterpret_cast<const WorkUnit*>(put(plan.units.data(), b_units));
@@ -554,7 +580,10 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   auto d_pre = reinterpret_cast<const int32_t*>(put(prefix.data(), b_pre));
   auto d_pairs = reinterpret_cast<const TcPair*>(put(pairs.data(), b_pairs));
   auto d_pairs2 = reinterpret_cast<const TcPair*>(put(pairs2.data(), b_pairs2));
-  SSA_CUDA(this, ring.to_device(off, total, st));
+  if (cap)
+    SSA_CUDA(this, cudaMemcpyAsync(arena_d + off, arena_h + off, total, cudaMemcpyHostToDevice, st));
+  else
+    SSA_CUDA(this, ring.to_device(off, total, st));
 
   // ---- E4M3 KV (R-22): codes of the call's K/V, the tails' and the scatter's source
   const void* k_src = io.k.dev;
@@ -563,6 +592,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     QuantParams qp{};
     qp.n = (int64_t)(in_layer_stride ? n_layers : 1) * rows_per_layer * cfg.num_kv_heads * D;
     if ((size_t)(2 * qp.n) > kv8_cap) {
+      if (cap) { ssa::set_error("CUDA-graph capture: warm up the call once before capturing (E4M3 scratch)"); return SSA_ERR_STATE; }
       SSA_CUDA(this, cudaStreamSynchronize(st));
       SSA_CUDA(this, cudaDeviceSynchronize());
       if (kv8) cudaFree(kv8);
@@ -713,7 +743,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     stats.rows_computed += rows;
     if (query_plane) stats.query_rows += rows;
   }
-  SSA_CUDA(this, ring.fence(off, off + total, st));
+  if (!cap) SSA_CUDA(this, ring.fence(off, off + total, st));
   last_plan_units = (int64_t)plan.units.size();
   last_plan_groups = (int64_t)plan.groups.size();
   last_used_tc = use_tc;
@@ -813,9 +843,13 @@ ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
   st->sm100 = (major == 10 && minor == 0);
   const size_t half = ssa_store_pool_bytes(cfg) / 2;
   st->pool_half_bytes = half;
+  st->arena_cap = 4u << 20;
   if ((e = cudaMalloc(&st->poolK, half)) != cudaSuccess || (e = cudaMalloc(&st->poolV, half)) != cudaSuccess ||
       (e = cudaMemset(st->poolK, 0, half)) != cudaSuccess || (e = cudaMemset(st->poolV, 0, half)) != cudaSuccess ||
-      (e = st->ring.init(8u << 20)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+      (e = st->ring.init(8u << 20)) != cudaSuccess ||
+      (e = cudaMallocHost(reinterpret_cast<void**>(&st->arena_h), 4u << 20)) != cudaSuccess ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&st->arena_d), 4u << 20)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess) {
     set_error("store allocation failed: %s", cudaGetErrorString(e));
     delete st;
     return SSA_ERR_CUDA;
@@ -840,6 +874,8 @@ ssa_store::~ssa_store() {
   if (stage) cudaFree(stage);
   if (qkv_scratch) cudaFree(qkv_scratch);
   if (kv8) cudaFree(kv8);
+  if (arena_h) cudaFreeHost(arena_h);
+  if (arena_d) cudaFree(arena_d);
   for (auto e : pipe_events) cudaEventDestroy(e);
   if (h2d_stream) cudaStreamDestroy(h2d_stream);
   if (d2h_stream) cudaStreamDestroy(d2h_stream);
@@ -903,8 +939,19 @@ static size_t tensor_bytes(const ssa_store* st, int64_t layers, int64_t rows, in
 }
 
 // Create / append share this path: reserve, upload pages, scatter + attention, commit.
+// Calls that change the store cannot be captured into a CUDA graph (their page
+// reservation and version bump happen at call time, once): rejected up front.
+#define SSA_NO_CAPTURE(stream)                                                              \
+  do {                                                                                      \
+    if (capturing(stream)) {                                                                \
+      set_error("CUDA-graph capture: only query-plane calls can be captured");              \
+      return SSA_ERR_STATE;                                                                 \
+    }                                                                                       \
+  } while (0)
+
 static ssa_status do_append(ssa_store* st, Session& s, int32_t n_new, const void* Q, const void* K,
                             const void* V, void* O, cudaStream_t stream) {
+  SSA_NO_CAPTURE(stream);
   const int L = st->cfg.num_layers;
   std::vector<int32_t> got;
   ssa_status rc = st->evict_for_append(s, n_new, stream);
@@ -940,6 +987,7 @@ ssa_status ssa_session_create(ssa_store_t st, int32_t n_prefix, const void* Q, c
     set_error("session_create: invalid arguments");
     return SSA_ERR_INVALID_ARG;
   }
+  SSA_NO_CAPTURE(stream);
   cudaSetDevice(st->cfg.device);
   int live = 0;
   int32_t id = -1;
@@ -1025,6 +1073,7 @@ ssa_status ssa_append_layer(ssa_store_t st, ssa_session_t id, int32_t ticket, in
   ssa_status rc = SSA_OK;
   Session* s = check_ticket(st, id, ticket, &rc);
   if (!s) return rc;
+  SSA_NO_CAPTURE(stream);
   if (layer < 0 || layer >= st->cfg.num_layers || !K || !V || (O && !Q)) return SSA_ERR_INVALID_ARG;
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
@@ -1106,6 +1155,7 @@ ssa_status ssa_session_evict_oldest(ssa_store_t st, ssa_session_t id, int64_t n,
   Session* s = st->get(id);
   if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
   if (s->ticket_open) return SSA_ERR_STATE;
+  SSA_NO_CAPTURE(stream);
   if (n < 0 || n > s->n_tokens - s->n_prefix) {
     set_error("evict_oldest: n=%lld but %lld Region-1 tokens retained", (long long)n,
               (long long)(s->n_tokens - s->n_prefix));
@@ -1131,6 +1181,7 @@ ssa_status ssa_session_alias_prefix(ssa_store_t st, ssa_session_t donor_id, int6
   SSA_CHECK_STORE(st);
   Session* d = st->get(donor_id);
   if (!d) { set_error("unknown session %d", donor_id); return SSA_ERR_UNKNOWN_SESSION; }
+  SSA_NO_CAPTURE(stream);
   if (!out || len < 0 || len > d->n_tokens || (len > d->n_prefix && d->n_evicted > 0)) {
     set_error("alias_prefix: len=%lld invalid for a donor of %lld tokens (%lld evicted)", (long long)len,
               (long long)d->n_tokens, (long long)d->n_evicted);
@@ -1272,6 +1323,8 @@ ssa_status ssa_batch_run(ssa_store_t st, int32_t layer, int32_t n_items, const s
     set_error("batch_run: invalid arguments");
     return SSA_ERR_INVALID_ARG;
   }
+  for (int32_t i = 0; i < n_items; ++i)
+    if (items[i].kind == SSA_WORK_APPEND) { SSA_NO_CAPTURE(stream); break; }
   int64_t n_rows = 0;
   std::vector<int32_t> app_sessions;
   for (int i = 0; i < n_items; ++i) {
@@ -1687,6 +1740,7 @@ ssa_status ssa_append_layer_fused(ssa_store_t st, ssa_session_t id, int32_t tick
   ssa_status rc = SSA_OK;
   Session* s = check_ticket(st, id, ticket, &rc);
   if (!s) return rc;
+  SSA_NO_CAPTURE(stream);
   if (layer < 0 || layer >= st->cfg.num_layers || !dev_ok(O, stream)) return SSA_ERR_INVALID_ARG;
   if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }

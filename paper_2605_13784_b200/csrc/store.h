@@ -100,6 +100,12 @@ struct ssa_store {
   bool failed = false;
   std::string fail_msg;
   ssa::UploadRing ring;
+  // CUDA-graph capture (query plane): work lists of captured calls live in this
+  // arena (pinned host + device, bump-allocated, never recycled while the store
+  // lives) so the captured H2D copy node reads the same bytes at every replay.
+  char* arena_h = nullptr;
+  char* arena_d = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
   float* part_o = nullptr;
   size_t part_o_cap = 0;
   float* part_lse = nullptr;

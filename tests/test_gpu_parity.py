@@ -819,3 +819,49 @@ def test_sharded_peer_push_two_processes(cuda):
             ok, e = within(results[r][i], want, "bf16")
             assert ok, (r, i, e)
     assert all(int(f[r].item()) == 3 for f in flags for r in range(world))
+
+
+@pytest.mark.parametrize("kv", [None, "e4m3"])
+def test_query_plane_cuda_graph_capture(cuda, kv):
+    """Query-plane calls captured into a CUDA graph (work lists in the store's graph arena)
+    replay bit-identically to direct calls, repeatedly; per-layer and all-layer forms.  An
+    append cannot be captured (it changes the store at call time)."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d = LL["L"], LL["hq"], LL["hkv"], LL["d"]
+    kw = dict(kv_format="e4m3", k_scale=1 / 16, v_scale=1 / 32) if kv else {}
+    st = ssa.Store(L, hq, hkv, d, page_size=64, num_pages=128, dtype="bf16", **kw)
+    spec = streams.StreamSpec("market", seed=42)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 3000)
+    sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
+    Qq, Kq, Vq = (to_dev(x, cuda) for x in gen_qkv(spec, L, hq, hkv, d, 1, 0, 32))
+    want = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    for l in range(L):                     # direct calls (also the warm-up: scratch sized)
+        st.session_query(sid, Qq[l:l + 1], Kq[l:l + 1], Vq[l:l + 1], want[l:l + 1], layer=l)
+    want_all = torch.empty_like(want)
+    st.session_query(sid, Qq, Kq, Vq, want_all)
+    torch.cuda.synchronize()
+    O = torch.zeros_like(want)
+    O_all = torch.zeros_like(want)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        s = torch.cuda.current_stream()
+        for l in range(L):
+            st.session_query(sid, Qq[l:l + 1], Kq[l:l + 1], Vq[l:l + 1], O[l:l + 1], layer=l, stream=s)
+        st.session_query(sid, Qq, Kq, Vq, O_all, stream=s)
+    for _ in range(2):
+        O.zero_()
+        O_all.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(O.view(torch.int16), want.view(torch.int16))
+        assert torch.equal(O_all.view(torch.int16), want_all.view(torch.int16))
+    Qa, Ka, Va = (to_dev(x, cuda) for x in gen_qkv(spec, L, hq, hkv, d, 0, 3000, 64))
+    occ = st.occupancy()
+    with pytest.raises(ssa.SsaError):
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            st.session_append(sid, Qa, Ka, Va, torch.empty_like(Qa), stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert st.info(sid)["n_tokens"] == 3000 and st.occupancy() == occ
+    st.close()
