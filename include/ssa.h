@@ -50,7 +50,8 @@
  *   captured into a CUDA graph on a capturing `stream` with DEVICE pointers: the
  *   work list goes to a persistent store-owned arena (4 MiB), so a replay repeats
  *   the call as planned at capture time (cache length and page table of that
- *   moment; re-capture after the session changes).  Run the call once before
+ *   moment; re-capture after the session changes; SSA_OPT_GRAPH_ARENA_RESET
+ *   recycles the arena once old graphs are dropped).  Run the call once before
  *   capturing (scratch buffers are sized on first use).  Calls that change the
  *   store (create, append, load, evict, alias) return SSA_ERR_STATE while the
  *   stream is capturing, with no state change.
@@ -395,9 +396,11 @@ typedef enum {
     SSA_OPT_FUSED_MERGE = 6,    /* 1: the last tcgen05 CTA of a split group merges the
                                    group in-kernel (no combine launch); 0 (default):
                                    separate combine kernel */
-    SSA_OPT_CTA_PAIR = 7        /* 1: work units whose key tiles are the same keys (q tiles
+    SSA_OPT_CTA_PAIR = 7,       /* 1: work units whose key tiles are the same keys (q tiles
                                    of one append / prompt) run on cta_group::2 CTA pairs
                                    with double-buffered S; 0: two-slot CTAs only */
+    SSA_OPT_GRAPH_ARENA_RESET = 8  /* value 1: recycle the CUDA-graph arena (the caller no
+                                   longer replays graphs captured before this call) */
 } ssa_option;
 ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
 

@@ -26,6 +26,7 @@ LIB_PATH = os.path.join(_HERE, "libssa.so")
 WORK_APPEND, WORK_QUERY, WORK_STATELESS = 0, 1, 2
 OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES, OPT_TIMING, OPT_FUSED_MERGE = 1, 2, 3, 4, 5, 6
 OPT_CTA_PAIR = 7
+OPT_GRAPH_ARENA_RESET = 8
 BF16, FP32 = 0, 1
 
 _STATUS = {0: "SSA_OK", -1: "SSA_ERR_INVALID_ARG", -2: "SSA_ERR_UNKNOWN_SESSION", -3: "SSA_ERR_POOL_EXHAUSTED",

@@ -916,6 +916,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
     case SSA_OPT_TIMING: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_timing = value; break;
     case SSA_OPT_FUSED_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_fused_merge = value; break;
     case SSA_OPT_CTA_PAIR: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_cta_pair = value; break;
+    case SSA_OPT_GRAPH_ARENA_RESET: if (value != 1) return SSA_ERR_INVALID_ARG; st->arena_used = 0; break;
     default: return SSA_ERR_INVALID_ARG;
   }
   return SSA_OK;

@@ -864,4 +864,19 @@ def test_query_plane_cuda_graph_capture(cuda, kv):
             st.session_append(sid, Qa, Ka, Va, torch.empty_like(Qa), stream=torch.cuda.current_stream())
     torch.cuda.synchronize()
     assert st.info(sid)["n_tokens"] == 3000 and st.occupancy() == occ
+    # the arena is exhausted by enough captures and recycled on request
+    with pytest.raises(ssa.SsaError):
+        for _ in range(100000):
+            g3 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g3):
+                st.session_query(sid, Qq, Kq, Vq, O_all, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    st.set_option(ssa.OPT_GRAPH_ARENA_RESET, 1)
+    g4 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g4):
+        st.session_query(sid, Qq, Kq, Vq, O_all, stream=torch.cuda.current_stream())
+    O_all.zero_()
+    g4.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(O_all.view(torch.int16), want_all.view(torch.int16))
     st.close()
