@@ -515,16 +515,46 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     pc.fault = (int)opt_fault;
     pc.force_groups = opts.force_groups;
     pc.pair_slots = use_tc;
-    plan_units(segs, pc, &plan);
   }
   // tcgen05: units with identical key tiles run as cta_group::2 CTA pairs
   // (kernels_tc2.cu), the rest as two-slot CTAs (kernels_tc.cu).
   std::vector<TcPair> pairs, pairs2;
   const bool fused_req = use_tc && opt_fused_merge;
-  if (use_tc) {
-    std::vector<char> in_pair2;
-    if (opt_cta_pair && !fused_req && !kv_fp8) pair_units_cta2(segs, plan, pc.key_tile, &pairs2, &in_pair2);
-    pair_units(segs, plan, pc.key_tile, &pairs, pairs2.empty() ? nullptr : &in_pair2);
+  const bool want_pairs2 = use_tc && opt_cta_pair && !fused_req && !kv_fp8;
+  if (compute_o) {
+    // plan cache key: options + per segment (m, own keys, cached slots, R0 hole, pool class)
+    std::vector<int64_t> key = {use_tc, want_pairs2, pc.Hkv, pc.key_tile, pc.q_tile_tokens, pc.n_layers, pc.num_sms,
+                                pc.max_splits, pc.fault, pc.force_groups, (int64_t)segs.size()};
+    for (size_t i = 0; i < segs.size(); ++i) {
+      size_t cls = i;   // first segment reading the same page table
+      for (size_t j = 0; j < i; ++j)
+        if (segs[j].pages == segs[i].pages) { cls = j; break; }
+      key.insert(key.end(), {segs[i].m, segs[i].tail_m, segs[i].n_slots, segs[i].hole_lo, segs[i].hole_hi,
+                             (int64_t)cls});
+    }
+    bool hit = false;
+    for (size_t e = 0; e < plan_cache.size(); ++e)
+      if (plan_cache[e].key == key) {
+        PlanCacheEntry ent = std::move(plan_cache[e]);
+        plan_cache.erase(plan_cache.begin() + e);
+        plan = ent.plan;
+        pairs = ent.pairs;
+        pairs2 = ent.pairs2;
+        plan_cache.push_back(std::move(ent));
+        ++plan_cache_hits;
+        hit = true;
+        break;
+      }
+    if (!hit) {
+      plan_units(segs, pc, &plan);
+      if (use_tc) {
+        std::vector<char> in_pair2;
+        if (want_pairs2) pair_units_cta2(segs, plan, pc.key_tile, &pairs2, &in_pair2);
+        pair_units(segs, plan, pc.key_tile, &pairs, pairs2.empty() ? nullptr : &in_pair2);
+      }
+      if (plan_cache.size() >= 8) plan_cache.erase(plan_cache.begin());
+      plan_cache.push_back({std::move(key), plan, pairs, pairs2});
+    }
   }
   // ---- append segments for the scatter
   std::vector<int32_t> app_idx;

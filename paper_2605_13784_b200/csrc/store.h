@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "ssa.h"
+#include "plan.h"
 #include "ssa_internal.h"
 
 namespace ssa {
@@ -100,6 +101,16 @@ struct ssa_store {
   bool failed = false;
   std::string fail_msg;
   ssa::UploadRing ring;
+  // Plans of recent calls (planner + CTA pairing are pure functions of the segment
+  // shapes and options): per-layer calls of one step, repeated queries between
+  // appends and Flash Query cycles skip the LPT search.
+  struct PlanCacheEntry {
+    std::vector<int64_t> key;
+    ssa::Plan plan;
+    std::vector<ssa::TcPair> pairs, pairs2;
+  };
+  std::vector<PlanCacheEntry> plan_cache;   // most recent last, at most 8
+  int64_t plan_cache_hits = 0;
   // CUDA-graph capture (query plane): work lists of captured calls live in this
   // arena (pinned host + device, bump-allocated, never recycled while the store
   // lives) so the captured H2D copy node reads the same bytes at every replay.
