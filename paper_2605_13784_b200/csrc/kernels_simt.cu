@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
         alpha = exp2f(m_old - m_new);
       }
       const float sum = warp_sum(p0 + p1);
+      __syncwarp();   // every lane's reads of this row (S, mrow) before the writes below
       Ss[r * kBK + lane] = p0;
       Ss[r * kBK + lane + 32] = p1;
       if (lane == 0) {
