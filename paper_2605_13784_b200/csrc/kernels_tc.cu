@@ -84,6 +84,7 @@ struct Bars {
 
 struct TcMaps {
   CUtensorMap q;       // [rows][Hq][D]   box {64, G, 128/G}
+  CUtensorMap q32;     // [rows][Hq][D]   box {64, G, 32/G}  (duplicated small q tiles)
   CUtensorMap kt;      // [rows][Hkv][D]  box {64, 1, 128}
   CUtensorMap vt;
   CUtensorMap pk;      // [L*num_pages*Hkv*P][D] box {64, BR}
@@ -241,6 +242,11 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   const int nt0 = w0.tile_hi - w0.tile_lo;
   const int nsh = pr.ub >= 0 ? pr.n_shared : 0;
   const bool two_q = pr.ub >= 0 && !pr.same_q;
+  // A split pair of a q tile with <= 32 live rows (e.g. a 1-token GQA query: 4 rows) loads
+  // those rows twice, at rows 0.. and 32.., so slot 1 reads its live S rows from TMEM lane
+  // quadrant 1 (warp 9, SM sub-partition 1) instead of sharing sub-partition 0's MUFU with
+  // slot 0.  Rows 64-127 of the tile are padding.
+  const bool dup = pr.ub >= 0 && pr.same_q && w0.q_ntok * p.G <= 32;
   // smem tile slots (7 x 32 KB): Q (1 or 2), a K ring of NK and a V ring of NV
   // stages.  K(e) is released by its S MMA, V(e) by its PV MMA, which run
   // about a tile later, so the rings and their producer warps progress
@@ -253,6 +259,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.q);
+    tma_prefetch_desc(&maps.q32);
     tma_prefetch_desc(&maps.kt);
     tma_prefetch_desc(&maps.vt);
     tma_prefetch_desc(&maps.pk);
@@ -313,7 +320,14 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
         const bool is_k = F8 ? lane == 0 : warp == 0;
-        if (is_k) {
+        if (is_k && dup) {
+          mbar_arrive_expect_tx(&bar.q_full, 2 * 2 * 32 * 128);
+          const int32_t qrow = (int32_t)(in_l + p.segs[w0.seg].row0 + w0.q_tok0);
+          for (int c = 0; c < 2; ++c)
+            for (int rb = 0; rb < 2; ++rb)
+              tma_load_3d(q_buf[0] + c * kChunkBytes + rb * 32 * 128, &maps.q32, &bar.q_full, c * 64,
+                          w0.kv_head * p.G, qrow);
+        } else if (is_k) {
           const int nq = two_q ? 2 : 1;
           mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
           for (int k = 0; k < nq; ++k) {
@@ -441,20 +455,22 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     const int nt = k ? nt1 : nt0;
     if (active) {
       const SegDesc sg = p.segs[w.seg];
-      const int r = threadIdx.x - 128 - 128 * k;   // row == TMEM lane
+      const int r = threadIdx.x - 128 - 128 * k;   // TMEM lane
+      const int roff = (dup && k == 1) ? 32 : 0;    // tile row of this slot's first live row
+      const int rr = r - roff;                      // row of the unit's q tile
       const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
       const uint32_t s_col = tmem + lane_base + 256u * k;
       const uint32_t o_col = s_col + 128u;
       const float c = p.scale_log2;
       const int G = p.G;
-      const int tok = w.q_tok0 + r / G;
+      const int tok = w.q_tok0 + (rr >= 0 ? rr : 0) / G;
       const int last_key = min(sg.tail_m - 1, p.fault == 2 ? tok - 1 : tok);   // own keys 0..tok (R-2)
       // rows >= q_ntok * G of the 128-row tile are padding (1-token GQA query: 4 live rows); a
       // warp whose 32 rows are all padding skips S loads, softmax and P stores (MUFU is the
       // query plane's co-bottleneck), but still waits for each S before arriving on p_full so
       // the barrier phases stay in order.  Its P columns keep stale values that only reach
       // the O rows of its own (discarded) lanes.
-      const bool warp_dead = (warp & 3) * 32 >= w.q_ntok * G;
+      const bool warp_dead = !(roff < (warp & 3) * 32 + 32 && roff + w.q_ntok * G > (warp & 3) * 32);
       const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
       float m_run = -CUDART_INF_F;
       float l_run = 0.f;
@@ -576,7 +592,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       }
       const int rows = w.q_ntok * G;
       const float inv_l = (l_run > 0.f ? 1.f / l_run : 0.f) * (F8 ? p.o_scale : 1.f);   // F8: V scale
-      const int h = w.kv_head * G + r % G;
+      const int h = w.kv_head * G + (rr >= 0 ? rr : 0) % G;
+      const bool live = rr >= 0 && rr < w.q_ntok * G;
       const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
       const int64_t orow = in_l + sg.row0 + tok;
       const int unit = k ? pr.ub : pr.ua;
@@ -586,7 +603,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         uint32_t ro[32];
         tmem_ld32(o_col + q4 * 32, ro);
         tmem_wait_ld();
-        if (r < rows) {
+        if (live) {
           if (w.group < 0) {
             __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32;
 #pragma unroll
@@ -599,7 +616,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               *reinterpret_cast<uint4*>(out + i) = v;
             }
           } else {
-            float* out = p.part_o + (pslot * kM + r) * kD + q4 * 32;
+            float* out = p.part_o + (pslot * kM + rr) * kD + q4 * 32;
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               *reinterpret_cast<float4*>(out + i) =
@@ -609,8 +626,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           }
         }
       }
-      if (w.group >= 0 && r < rows)
-        p.part_lse[pslot * kM + r] = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
+      if (w.group >= 0 && live)
+        p.part_lse[pslot * kM + rr] = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
       // ------------------------------------------------- fused split-KV merge (R-11)
       if (w.group >= 0 && p.group_counters) {
         const Group gr = p.groups[w.group];
@@ -625,13 +642,13 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
         if (bar.merge_flag[k]) {
           __threadfence();
-          if (r < rows) {
+          if (live) {
             const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
             float L = -CUDART_INF_F;
-            for (int s = 0; s < gr.n_splits; ++s) L = fmaxf(L, __ldcg(p.part_lse + (s0 + s) * kM + r));
+            for (int s = 0; s < gr.n_splits; ++s) L = fmaxf(L, __ldcg(p.part_lse + (s0 + s) * kM + rr));
             float wsum = 0.f;
             for (int s = 0; s < gr.n_splits; ++s) {
-              const float ls = __ldcg(p.part_lse + (s0 + s) * kM + r);
+              const float ls = __ldcg(p.part_lse + (s0 + s) * kM + rr);
               if (ls != -CUDART_INF_F) wsum += exp2f(ls - L);
             }
             const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
@@ -641,10 +658,10 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
 #pragma unroll
               for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
               for (int s = 0; s < gr.n_splits; ++s) {
-                const float ls = __ldcg(p.part_lse + (s0 + s) * kM + r);
+                const float ls = __ldcg(p.part_lse + (s0 + s) * kM + rr);
                 if (ls == -CUDART_INF_F) continue;
                 const float wt = exp2f(ls - L) * inv;
-                const float4* src = reinterpret_cast<const float4*>(p.part_o + ((s0 + s) * kM + r) * kD + q4 * 32);
+                const float4* src = reinterpret_cast<const float4*>(p.part_o + ((s0 + s) * kM + rr) * kD + q4 * 32);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                   const float4 v = __ldcg(src + i);
@@ -761,6 +778,8 @@ cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, c
     cuuint64_t str[2] = {(cuuint64_t)kD * 2, (cuuint64_t)p.Hq * kD * 2};
     cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)(kM / G)};
     if (!encode(&maps.q, p.Q, 3, dims, str, box)) return cudaErrorInvalidValue;
+    cuuint32_t box32[3] = {64, (cuuint32_t)G, (cuuint32_t)(32 / G)};
+    if (!encode(&maps.q32, p.Q, 3, dims, str, box32)) return cudaErrorInvalidValue;
   }
   // K/V element bytes: 2 (bf16) or 1 (E4M3 codes: a row of d = 128 codes is one 128-byte swizzle chunk)
   const int kvb = p.kv_fp8 ? 1 : 2;
