@@ -2,7 +2,7 @@
 SIMT fp32 (toy config), tcgen05 bf16 append / query / flash / batch, E4M3 store, scatter /
 gather / digest, retention + alias page copy, split-KV partials + merge, greedy sampling,
 fused projection.  Exits non-zero on a parity failure against the fp64 oracle.
-    compute-sanitizer --tool memcheck python scripts/sanitize_run.py"""
+    compute-sanitizer --tool memcheck python tests/sanitize_run.py"""
 import os
 import sys
 
