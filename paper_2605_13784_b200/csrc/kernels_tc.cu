@@ -276,7 +276,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&bar.s_full[k], 1);
-      mbar_init(&bar.p_full[k], 4);
+      // one arrival per softmax warp that owns a live row of slot k (padding warps skip)
+      const int rows_k = (k ? w1 : w0).q_ntok * p.G;
+      const int roff_k = (dup && k == 1) ? 32 : 0;
+      int live_warps = 0;
+      for (int q = 0; q < 4; ++q) live_warps += (roff_k < 32 * q + 32 && roff_k + rows_k > 32 * q) ? 1 : 0;
+      mbar_init(&bar.p_full[k], live_warps);
       mbar_init(&bar.o_final[k], 1);
     }
     fence_mbar_init();
@@ -466,22 +471,21 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       const int tok = w.q_tok0 + (rr >= 0 ? rr : 0) / G;
       const int last_key = min(sg.tail_m - 1, p.fault == 2 ? tok - 1 : tok);   // own keys 0..tok (R-2)
       // rows >= q_ntok * G of the 128-row tile are padding (1-token GQA query: 4 live rows); a
-      // warp whose 32 rows are all padding skips S loads, softmax and P stores (MUFU is the
-      // query plane's co-bottleneck), but still waits for each S before arriving on p_full so
-      // the barrier phases stay in order.  Its P columns keep stale values that only reach
-      // the O rows of its own (discarded) lanes.
+      // warp whose 32 rows are all padding takes no part in the tile loop (p_full counts only
+      // the live warps): no S loads, softmax, P stores or barrier polling.  Its P columns keep
+      // stale values that only reach the O rows of its own (discarded) lanes.
       const bool warp_dead = !(roff < (warp & 3) * 32 + 32 && roff + w.q_ntok * G > (warp & 3) * 32);
       const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
       float m_run = -CUDART_INF_F;
       float l_run = 0.f;
-      for (int j = 0; j < nt; ++j) {
+      for (int j = 0; j < (warp_dead ? 0 : nt); ++j) {
         const int tile = w.tile_lo + j;
         const bool is_pool = tile < n_pool_tiles;
         const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBN;
         mbar_wait(&bar.s_full[k], j & 1);
         TRACE(r == 0, k, j, 0, clock64());
         tc_fence_after();
-        if (!warp_dead) {   // a warp with no live row (|q| * G <= 96) only keeps the handoff order
+        {
         float sv[kBN];
         {
           uint32_t ra[32], rb[32], rc[32], rd[32];
