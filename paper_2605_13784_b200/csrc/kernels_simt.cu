@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
   const int CR = p.combine_rows;
   const int g = blockIdx.x, ly = blockIdx.y, r0 = blockIdx.z * CR;
   const Group gr = p.groups[g];
+  if (gr.n_splits == 0) return;   // merged inside its attention CTA
   const int rows = gr.q_ntok * p.G;
   if (r0 >= rows) return;
   const int nr = min(CR, rows - r0);

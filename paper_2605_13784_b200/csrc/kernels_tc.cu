@@ -602,6 +602,64 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       const int64_t orow = in_l + sg.row0 + tok;
       const int unit = k ? pr.ub : pr.ua;
       const int64_t pslot = (int64_t)ly * p.n_units + unit;
+      if (pr.merge) {
+        // The two slots are the two key ranges of one q tile and the whole split group:
+        // log-sum-exp merge (R-11) in the CTA.  Slot 1 leaves its normalized O and lse in
+        // the (now idle) ring shared memory, slot 0 merges and writes O -- no partials in
+        // HBM, no combine launch for the group.
+        float* xo = reinterpret_cast<float*>(k_base);   // [128][129] fp32 (padded rows)
+        float* xl = xo + 128 * 129;                      // [128]
+        const float lse = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
+        if (k == 1) {
+          // the ring may still feed slot 0's last MMAs: wait until they have completed
+          if (nt0 > 0) mbar_wait(&bar.o_final[0], 0);
+#pragma unroll 1
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t ro[32];
+            tmem_ld32(o_col + q4 * 32, ro);
+            tmem_wait_ld();
+            if (live)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) xo[rr * 129 + q4 * 32 + i] = __uint_as_float(ro[i]) * inv_l;
+          }
+          if (live) xl[rr] = lse;
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (k == 0) {
+          float w0 = 0.f, w1 = 0.f;
+          if (live) {
+            const float l1 = xl[rr];
+            const float L = fmaxf(lse, l1);
+            w0 = lse == -CUDART_INF_F ? 0.f : exp2f(lse - L);
+            w1 = l1 == -CUDART_INF_F ? 0.f : exp2f(l1 - L);
+            const float inv = (w0 + w1) > 0.f ? 1.f / (w0 + w1) : 0.f;
+            w0 *= inv * inv_l;
+            w1 *= inv;
+          }
+#pragma unroll 1
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t ro[32];
+            tmem_ld32(o_col + q4 * 32, ro);
+            tmem_wait_ld();
+            if (live) {
+              const float* x1 = xo + rr * 129 + q4 * 32;
+              __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32;
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = fmaf(w0, __uint_as_float(ro[i + u]), w1 * x1[i + u]);
+                uint4 pk4;
+                pk4.x = pack_bf16(v[0], v[1]);
+                pk4.y = pack_bf16(v[2], v[3]);
+                pk4.z = pack_bf16(v[4], v[5]);
+                pk4.w = pack_bf16(v[6], v[7]);
+                *reinterpret_cast<uint4*>(out + i) = pk4;
+              }
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         uint32_t ro[32];
@@ -632,6 +690,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       }
       if (w.group >= 0 && live)
         p.part_lse[pslot * kM + rr] = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
+      }   // !pr.merge
       // ------------------------------------------------- fused split-KV merge (R-11)
       if (w.group >= 0 && p.group_counters) {
         const Group gr = p.groups[w.group];

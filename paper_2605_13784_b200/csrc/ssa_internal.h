@@ -62,6 +62,7 @@ struct TcPair {
   int32_t ua, ub;     // unit indices (ub = -1: single slot)
   int32_t n_shared;   // leading tiles shared by both slots
   int32_t same_q;
+  int32_t merge;      // the two units are the whole split group: merged in the CTA's epilogue
 };
 
 struct AttnParams {

@@ -556,6 +556,21 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       plan_cache.push_back({std::move(key), plan, pairs, pairs2});
     }
   }
+  // ---- split groups that are exactly one SPLIT pair are merged inside that CTA
+  // (kernels_tc.cu epilogue): no partial traffic and no combine work for them
+  bool any_combine = !plan.groups.empty();
+  if (use_tc && !plan.groups.empty() && !opt_fused_merge && !opts.force_groups && opts.n_peers == 0 &&
+      !opts.o_f32 && !opts.lse_out && !getenv("SSA_NO_CTA_MERGE")) {
+    for (auto& pr : pairs) {
+      if (pr.ub < 0 || !pr.same_q) continue;
+      const int g = plan.units[pr.ua].group;
+      if (g < 0 || g != plan.units[pr.ub].group || plan.groups[g].n_splits != 2) continue;
+      pr.merge = 1;
+      plan.groups[g].n_splits = 0;
+    }
+    any_combine = false;
+    for (auto& g : plan.groups) any_combine = any_combine || g.n_splits > 0;
+  }
   // ---- append segments for the scatter
   std::vector<int32_t> app_idx;
   for (int i = 0; i < (int)segs.size(); ++i)
@@ -740,7 +755,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     if (t0) timed_push(query_plane ? 1 : 0, t0, tick(st));
     stats.kernel_launches++;
     if (use_tc) stats.tc_launches++;
-    if (!plan.groups.empty() && !fused) {
+    if (!plan.groups.empty() && !fused && any_combine) {
       CombineParams cp{};
       cp.part_o = part_o;
       cp.part_lse = part_lse;
