@@ -34,7 +34,12 @@
  *   store-owned staging buffers on `stream`; a host O is copied back on
  *   `stream` — synchronize `stream` before reading it.
  * Streams.  `stream` is a cudaStream_t passed as void* (NULL = legacy default
- *   stream).  All device work of a call is enqueued on it, in call order.
+ *   stream).  All device work of a call is enqueued on it, in call order.  The
+ *   store orders its calls across streams: a call on another stream than the
+ *   previous call first waits (cudaStreamWaitEvent, no host sync) for the
+ *   previous call's work, so pages released by truncate / destroy / evict,
+ *   scratch and staging buffers are never reused while an earlier call on
+ *   another stream may still read them (one dispatch order).
  * Ownership.  The caller owns Q/K/V/O and `stream` and keeps device buffers
  *   alive until the stream has passed the call.  The store owns the KV pool,
  *   page tables, staging and scratch memory, and its NCCL communicator.
@@ -46,15 +51,21 @@
  *   marks the store failed (sticky): every later call returns SSA_ERR_STATE.
  *   ssa_last_error() returns a message for the calling thread's last error.
  * CUDA graphs.  Query-plane calls (ssa_session_query, ssa_flash_query_batch,
- *   ssa_batch_run without APPEND items, the sharded partial/push/merge) may be
- *   captured into a CUDA graph on a capturing `stream` with DEVICE pointers: the
- *   work list goes to a persistent store-owned arena (4 MiB), so a replay repeats
- *   the call as planned at capture time (cache length and page table of that
- *   moment; re-capture after the session changes; SSA_OPT_GRAPH_ARENA_RESET
- *   recycles the arena once old graphs are dropped).  Run the call once before
- *   capturing (scratch buffers are sized on first use).  Calls that change the
- *   store (create, append, load, evict, alias) return SSA_ERR_STATE while the
- *   stream is capturing, with no state change.
+ *   ssa_batch_run without APPEND items, the sharded partial/push/merge) and the
+ *   per-layer data-plane step ssa_append_layer may be captured into a CUDA graph
+ *   on a capturing `stream` with DEVICE pointers.  A replay repeats the call as
+ *   planned at capture time (cache length, page table and, for
+ *   ssa_append_layer, the ticket's destination slots of that moment): replay a
+ *   captured ssa_append_layer only inside a ticket of the same session state
+ *   (e.g. after truncating back to the captured length, ssa_append_begin
+ *   reserves the same pages, lowest id first, R-9); a capture marks the layer
+ *   appended for the ticket open at capture time.  Work lists come from the
+ *   store's cache of call shapes (entries read by a graph are kept) or, for a
+ *   shape never run eagerly, from a persistent 4 MiB arena written by a captured
+ *   copy (SSA_OPT_GRAPH_ARENA_RESET recycles it once old graphs are dropped).
+ *   Run the call once before capturing (scratch buffers are sized on first
+ *   use).  Calls that change host state (create, append, begin, load, evict,
+ *   alias) return SSA_ERR_STATE while the stream is capturing, no state change.
  * Threading.  One host thread at a time per store (external serialization —
  *   the paper's single dispatch worker).  Distinct stores are
  *   independent.  Sessions never see each other's keys.
@@ -69,7 +80,7 @@
 extern "C" {
 #endif
 
-#define SSA_ABI_VERSION 1
+#define SSA_ABI_VERSION 2
 
 typedef enum {
     SSA_OK = 0,
@@ -378,8 +389,12 @@ typedef struct {
     int64_t pages_reserved;
     int64_t h2d_bytes;           /* host staging copies */
     int64_t d2h_bytes;
-    int64_t tc_launches;         /* attention launches on the tcgen05 kernels */
-    int64_t tc_pair_launches;    /* of which on the cta_group::2 CTA-pair kernel */
+    int64_t tc_launches;         /* attention launches on the tcgen05 kernel */
+    int64_t cm_launches;         /* of which cluster-merge launches (split-KV merged
+                                    in the kernel: no partials in HBM unless a group
+                                    spans several clusters, no combine launch) */
+    int64_t plan_uploads;        /* work lists planned and copied to the device (a
+                                    repeated call shape reuses the device copy) */
 } ssa_stats;
 
 ssa_status ssa_store_stats(ssa_store_t store, ssa_stats *out, int32_t reset);
@@ -390,19 +405,36 @@ typedef enum {
     SSA_OPT_MAX_SPLITS = 2,     /* cap on split-KV factor (0 = auto) */
     SSA_OPT_FAULT_INJECT = 3,   /* negative controls: 0 none, 1 drop last key tile,
                                    2 causal off-by-one (row t misses its own key) */
-    SSA_OPT_TC_Q_TILES = 4,     /* tcgen05 Q tiles per CTA (1 or 2; 0 = auto) */
+    SSA_OPT_TC_Q_TILES = 4,     /* accepted for compatibility; no effect */
     SSA_OPT_TIMING = 5,         /* 1: record CUDA events around every kernel launch
                                    (on the call's stream) for ssa_store_timing */
-    SSA_OPT_FUSED_MERGE = 6,    /* 1: the last tcgen05 CTA of a split group merges the
-                                   group in-kernel (no combine launch); 0 (default):
-                                   separate combine kernel */
-    SSA_OPT_CTA_PAIR = 7,       /* 1: work units whose key tiles are the same keys (q tiles
-                                   of one append / prompt) run on cta_group::2 CTA pairs
-                                   with double-buffered S; 0: two-slot CTAs only */
-    SSA_OPT_GRAPH_ARENA_RESET = 8  /* value 1: recycle the CUDA-graph arena (the caller no
-                                   longer replays graphs captured before this call) */
+    /* 6, 7: removed in ABI 2 (in-kernel merge is now the cluster merge below;
+       the cta_group::2 kernel was slower than the two-slot kernel) */
+    SSA_OPT_GRAPH_ARENA_RESET = 8, /* value 1: recycle the CUDA-graph arena and unpin the
+                                   cached work lists (the caller no longer replays
+                                   graphs captured before this call) */
+    SSA_OPT_CLUSTER = 9,        /* split-KV merge of single-layer tcgen05 calls: 0 (default)
+                                   cluster size from the planner's cost model over
+                                   C in 1..8 and 16; 1..8 or 16 force C; -1 no cluster
+                                   plan (LPT plan, split groups merged across CTAs) */
+    SSA_OPT_PDL = 10,           /* 1 (default): tcgen05 attention launches allow
+                                   programmatic dependent launch (prologue overlaps
+                                   the previous kernel); 0: plain stream order */
+    SSA_OPT_PIPE_CHUNKS = 11,   /* all-layer calls with host buffers: -1 no copy/compute
+                                   pipelining, 0 default (2 layer chunks), n chunks */
+    SSA_OPT_QKV_DEBUG = 12,     /* fused projection experiments: 0 off, 1 skip the epilogue */
+    SSA_OPT_CM_MERGE = 13       /* cluster-merge groups over several clusters: 1 (default)
+                                   a separate merge kernel (programmatic launch right
+                                   behind the attention kernel), 0 the last arriving CTA
+                                   merges inside the attention kernel */
 } ssa_option;
 ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
+
+/* Shape of the store's last attention launch (a test / tuning aid):
+ * out[0] work units, [1] split groups, [2] CTAs per layer, [3] cluster size of a
+ * cluster-merge launch (0: combine kernel or SIMT), [4] largest split count
+ * (clusters per group for a cluster-merge launch). */
+ssa_status ssa_debug_last_plan(ssa_store_t store, int64_t out[5]);
 
 /* Kernel timing recorded while SSA_OPT_TIMING is on, per kernel class
  * (SSA_TIMING_KINDS entries): [0] data-plane attention (create/append/batch),
@@ -428,6 +460,11 @@ int32_t ssa_debug_trace(void *host, size_t bytes);
  * thread-block clusters of `splits` CTAs that can be co-resident on the current
  * device (cudaOccupancyMaxActiveClusters), or -1 on error. */
 int32_t ssa_debug_qkv_clusters(int32_t splits);
+
+/* Occupancy probe of the tcgen05 attention kernel: co-resident thread-block
+ * clusters of `size` CTAs (one CTA per SM) on the current device, for the bf16
+ * (e4m3 = 0) or E4M3 variant; what the cluster-merge planner sizes plans by. */
+int32_t ssa_debug_tc_clusters(int32_t size, int32_t e4m3);
 /* Tuning aid: when `device_buf` is non-NULL the following fused-projection
  * launches write per-CTA %globaltimer stamps (uint64 [grid][8]: start, after
  * setup, accumulator ready, partial dumped, cluster synced, epilogue done,

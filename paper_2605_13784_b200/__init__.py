@@ -15,8 +15,8 @@ import ctypes
 import os
 
 __all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", "WORK_STATELESS",
-           "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING", "OPT_FUSED_MERGE",
-           "OPT_CTA_PAIR",
+           "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING",
+           "OPT_GRAPH_ARENA_RESET", "OPT_CLUSTER", "OPT_PDL", "OPT_PIPE_CHUNKS", "OPT_QKV_DEBUG", "OPT_CM_MERGE",
            "debug_plan", "TIMING_KINDS"]
 TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter", "qkv_rope", "quant_e4m3")
 
@@ -24,9 +24,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libssa.so")
 
 WORK_APPEND, WORK_QUERY, WORK_STATELESS = 0, 1, 2
-OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES, OPT_TIMING, OPT_FUSED_MERGE = 1, 2, 3, 4, 5, 6
-OPT_CTA_PAIR = 7
-OPT_GRAPH_ARENA_RESET = 8
+OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES, OPT_TIMING = 1, 2, 3, 4, 5
+OPT_GRAPH_ARENA_RESET, OPT_CLUSTER, OPT_PDL, OPT_PIPE_CHUNKS, OPT_QKV_DEBUG, OPT_CM_MERGE = 8, 9, 10, 11, 12, 13
 BF16, FP32 = 0, 1
 
 _STATUS = {0: "SSA_OK", -1: "SSA_ERR_INVALID_ARG", -2: "SSA_ERR_UNKNOWN_SESSION", -3: "SSA_ERR_POOL_EXHAUSTED",
@@ -67,7 +66,7 @@ class WorkItem(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("kernel_launches", "rows_computed", "query_rows",
                                               "tokens_appended", "pages_reserved", "h2d_bytes", "d2h_bytes",
-                                              "tc_launches", "tc_pair_launches")]
+                                              "tc_launches", "cm_launches", "plan_uploads")]
 
 
 def _load():
@@ -120,6 +119,8 @@ def _load():
         "ssa_status_str": (ctypes.c_char_p, [i32]),
         "ssa_last_error": (ctypes.c_char_p, []),
         "ssa_abi_version": (i32, []),
+        "ssa_debug_last_plan": (i32, [vp, P(i64)]),
+        "ssa_debug_tc_clusters": (i32, [i32, i32]),
         "ssa_debug_plan": (i32, [i32, P(i32), P(i32), i32, i32, i32, i32, i32, i32, i32, P(i32), i32]),
     }
     for name, (res, args) in sig.items():
@@ -363,6 +364,13 @@ class Store:
 
     def set_option(self, option, value):
         _check(lib.ssa_store_set_option(self._h, option, value), "store_set_option")
+
+    def last_plan(self):
+        """Shape of the last attention launch: units, groups, CTAs per layer, cluster size of a
+        cluster-merge launch (0: combine kernel / SIMT), largest split count."""
+        out = (ctypes.c_int64 * 5)()
+        _check(lib.ssa_debug_last_plan(self._h, out), "debug_last_plan")
+        return dict(zip(("units", "groups", "ctas", "cm_C", "max_split"), list(out)))
 
     def timing(self, reset=False):
         """{kind: (ms_total, launches)} recorded under OPT_TIMING (syncs)."""

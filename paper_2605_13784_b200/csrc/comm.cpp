@@ -155,6 +155,7 @@ ssa_status ssa_sharded_partial(ssa_store_t st, ssa_session_t id, int32_t layer, 
   if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
   if (n_q <= 0 || !Q || !K || !V || !part || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   cudaStream_t cs = (cudaStream_t)stream;
   const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;
   const int64_t rows = Lin * n_q;
@@ -184,6 +185,7 @@ ssa_status ssa_merge_rank_partials(ssa_store_t st, int32_t world, int64_t rows, 
   if (rc != SSA_OK) return rc;
   if (world <= 0 || rows <= 0 || !parts || !O) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   cudaStream_t cs = (cudaStream_t)stream;
   IoSet io;
   io.o = {O, (size_t)rows * st->cfg.num_q_heads * st->cfg.head_dim * st->elem};
@@ -227,6 +229,7 @@ ssa_status ssa_sharded_push(ssa_store_t st, ssa_session_t id, int32_t layer, int
   if (!s) { set_error("unknown session %d", id); return SSA_ERR_UNKNOWN_SESSION; }
   if (n_q <= 0 || !Q || !K || !V || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   cudaStream_t cs = (cudaStream_t)stream;
   const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;
   const int64_t rows = Lin * n_q;
@@ -276,6 +279,7 @@ ssa_status ssa_sharded_merge(ssa_store_t st, int32_t layer, int32_t n_q, void* O
   if (!c || !c->peers) { set_error("sharded_merge: ssa_comm_attach_peers first"); return SSA_ERR_STATE; }
   if (n_q <= 0 || !O || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   cudaStream_t cs = (cudaStream_t)stream;
   const int64_t rows = (layer < 0 ? st->cfg.num_layers : 1) * (int64_t)n_q;
   IoSet io;
@@ -300,6 +304,7 @@ ssa_status ssa_sharded_query(ssa_store_t st, ssa_session_t id, int32_t layer, in
   }
   if (n_q <= 0 || !O || layer < -1 || layer >= st->cfg.num_layers) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   CommState* c = st->comm;
   cudaStream_t cs = (cudaStream_t)stream;
   const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;

@@ -79,7 +79,8 @@ struct Bars {
   uint64_t p_full[2];
   uint64_t o_final[2];
   uint32_t tmem_base;
-  uint32_t merge_flag[2];
+  int32_t pwin_base[2][2];        // page-id windows of the TMA producers: [K / V producer][slot] first entry
+  alignas(16) int32_t pwin[2][2][32];         // entries [base, base + 32) of the slot's page table
 };
 
 struct TcMaps {
@@ -193,6 +194,29 @@ __device__ unsigned long long g_trace[kTraceCtas][12][kTraceTiles][2];
 #define TRACE(cond, row, j, w, val) do { } while (0)
 #endif
 
+// Optional launch-phase trace (debug builds with -DSSA_GTRACE): %globaltimer (ns) of
+// a few events per CTA, per pool layer (mod 32) of a launch, read back by
+// ssa_debug_trace() as [32 layers][256 CTAs][16]; 8-13: CM epilogue (rows staged,
+// cluster barrier 1 passed, block reduced, ticket taken, merge done, barrier 2 passed).
+// 0 entry, 1 setup done, 2 Q landed (MMA issuer), 3 first K stage landed,
+// 4 first S of slot 0 seen by the softmax, 5 last PV of slot 0 done, 6 epilogue
+// done, 7 SM id.
+#ifdef SSA_GTRACE
+constexpr int kGtCtas = 256;
+__device__ unsigned long long g_gtrace[32][kGtCtas][16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GTRACE(cond, ev) \
+  do { if ((cond) && blockIdx.x < kGtCtas) g_gtrace[(p.layer0 + blockIdx.y) & 31][blockIdx.x][ev] = gtime(); } while (0)
+#define GTRACE_T(cond, ev) GTRACE((cond) && threadIdx.x == 128, ev)
+#else
+#define GTRACE(cond, ev) do { } while (0)
+#define GTRACE_T(cond, ev) do { } while (0)
+#endif
+
 // Optional exp2 offload (SSA_POLY_PAIRS_OF_8 = n > 0): n of every 8 element
 // pairs use 2^x = 2^j * p(f) on the FMA pipe (j = rint(x) by the 1.5*2^23 magic
 // add, f in [-0.5, 0.5], degree-3 minimax p with relative error 7.5e-5, far
@@ -201,6 +225,343 @@ __device__ unsigned long long g_trace[kTraceCtas][12][kTraceTiles][2];
 #define SSA_POLY_PAIRS_OF_8 0
 #endif
 constexpr int kPolyPairsOf8 = SSA_POLY_PAIRS_OF_8;
+
+// Page id of entry `pi` of a segment's page table, through a 32-entry window in
+// shared memory owned by one producer thread and refilled with 16-byte loads
+// when `pi` leaves it: one load latency per 32 pages instead of one per TMA box.
+__device__ __forceinline__ int32_t page_window(int32_t& base, int32_t* win, const SegDesc& sg, int pi) {
+  if (pi < base || pi >= base + 32) {
+    base = pi & ~3;
+    const int n = min(32, sg.n_pages - base);
+    const int4* src = reinterpret_cast<const int4*>(sg.pages + base);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (4 * i + 3 < n) {
+        *reinterpret_cast<int4*>(win + 4 * i) = __ldg(src + i);
+      } else {
+        for (int j = 4 * i; j < n && j < 4 * i + 4; ++j) win[j] = __ldg(sg.pages + base + j);
+      }
+    }
+  }
+  return win[pi - base];
+}
+
+// ---------------------------------------------------------------- cluster merge (CM)
+// CM launches (AttnParams::cm_C = C >= 1): every unit belongs to a split group and
+// the C CTAs of a thread-block cluster (consecutive blockIdx.x) hold C key ranges
+// of one q tile (SPLIT pairs: a CTA's two slots are two further ranges, merged in
+// the CTA) or of two q tiles (SHARED pairs).  Each CTA leaves the normalized O rows
+// (fp32) and lse of its q tile(s) in its idle ring shared memory; after a cluster
+// barrier CTA rank r merges row block r over the C CTAs through DSMEM (log-sum-exp,
+// reading R-11) and writes O.  A group spread over K > 1 clusters writes the block
+// as a partial instead, and the last of the K CTAs of rank r to arrive (atomic
+// ticket, no spin waits) merges the K partials.  No combine launch, no partials in
+// HBM when K = 1.
+constexpr int kXStride = 132;                 // fp32 row stride: 16-B aligned, conflict-free float4 stores
+constexpr int kXFloats = kM * kXStride + kM;   // rows + lse
+
+// Barrier over every thread of the cluster (C > 1) or of the CTA (named barrier
+// 4; callers sit at different points of the warp-role branches).
+__device__ __forceinline__ void cm_sync(int C) {
+  if (C > 1)
+    cluster_sync_all();
+  else
+    asm volatile("bar.sync 4, %0;" ::"n"(kThreads) : "memory");
+}
+
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+
+// Slot rows -> exchange buffer: O * inv_l (zeros for a row with no keys) and lse.
+__device__ __forceinline__ void cm_stage_rows(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
+                                              bool has) {
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    uint32_t ro[32];
+    tmem_ld32(o_col + q4 * 32, ro);
+    tmem_wait_ld();
+    if (live) {
+      float* dst = X + rr * kXStride + q4 * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(dst + i) =
+            has ? make_float4(__uint_as_float(ro[i]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l,
+                              __uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (live) X[kM * kXStride + rr] = has ? lse : -CUDART_INF_F;
+}
+
+// Split pair: slot 0 merges slot 1's staged rows with its own (R-11), in place.
+__device__ __forceinline__ void cm_merge_rows(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
+                                              bool has) {
+  float a0 = 0.f, a1 = 0.f, lm = -CUDART_INF_F;
+  if (live) {
+    const float l1 = X[kM * kXStride + rr];
+    const float l0 = has ? lse : -CUDART_INF_F;
+    const float L = fmaxf(l0, l1);
+    if (L != -CUDART_INF_F) {
+      const float w0 = l0 == -CUDART_INF_F ? 0.f : exp2f(l0 - L);
+      const float w1 = l1 == -CUDART_INF_F ? 0.f : exp2f(l1 - L);
+      const float inv = 1.f / (w0 + w1);
+      a0 = w0 * inv * inv_l;
+      a1 = w1 * inv;
+      lm = L + __log2f(w0 + w1);
+    }
+  }
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    uint32_t ro[32];
+    tmem_ld32(o_col + q4 * 32, ro);
+    tmem_wait_ld();
+    if (live) {
+      float* dst = X + rr * kXStride + q4 * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 x1 = *reinterpret_cast<const float4*>(dst + i);
+        float4 v;
+        v.x = (a0 != 0.f ? a0 * __uint_as_float(ro[i]) : 0.f) + a1 * x1.x;
+        v.y = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 1]) : 0.f) + a1 * x1.y;
+        v.z = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 2]) : 0.f) + a1 * x1.z;
+        v.w = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 3]) : 0.f) + a1 * x1.w;
+        *reinterpret_cast<float4*>(dst + i) = v;
+      }
+    }
+  }
+  if (live) X[kM * kXStride + rr] = lm;
+}
+
+__device__ __forceinline__ void store_bf16x8(__nv_bfloat16* out, const float* v) {
+  uint4 u;
+  u.x = pack_bf16(v[0], v[1]);
+  u.y = pack_bf16(v[2], v[3]);
+  u.z = pack_bf16(v[4], v[5]);
+  u.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(out) = u;
+}
+
+// Row block `rank` of one q tile's exchange buffers over the C CTAs of the
+// cluster, by warpgroup k.  Warp wq takes rows rank*R + wq + 4i; lane l takes
+// columns [4l, 4l+4) -- every (D)SMEM and global access of a warp is one whole
+// 512-byte row (coalesced: DSMEM runs at global-memory-like segment rates).
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* out, float4 v) {
+  uint2 u;
+  u.x = pack_bf16(v.x, v.y);
+  u.y = pack_bf16(v.z, v.w);
+  *reinterpret_cast<uint2*>(out) = u;
+}
+
+template <int C>
+__device__ __forceinline__ void cm_reduce(const AttnParams& p, const WorkUnit& w, const float* X, int k) {
+  constexpr int R = (kM + C - 1) / C;       // rows of this CTA's block (the last blocks may be short)
+  constexpr int RB = C >= 16 ? 1 : 16 / C > 0 ? 16 / C : 1;  // rows per warp per batch of loads
+  const int t = threadIdx.x - 128 - 128 * k;
+  const int wq = t >> 5, lane = t & 31;
+  const uint32_t rank = C > 1 ? cluster_ctarank() : 0u;
+  const int G = p.G;
+  const int ly = blockIdx.y;
+  const int row0 = (int)rank * R;
+  const int row_end = min(row0 + R, w.q_ntok * G);   // live rows of the block
+  const SegDesc sg = p.segs[w.seg];
+  const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+  const Group gr = p.groups[w.group];
+  const int K = gr.n_splits;   // clusters holding key ranges of this group
+  const uint32_t xa = smem_u32(X);
+  const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
+  auto out_ptr = [&](int row) {
+    const int64_t orow = in_l + sg.row0 + w.q_tok0 + row / G;
+    return static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + w.kv_head * G + row % G) * kD + 4 * lane;
+  };
+  for (int r0 = row0 + wq; r0 < row_end; r0 += 4 * RB) {
+    float lc[RB][C];
+    float4 v[RB][C];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int row = min(r0 + 4 * b, row_end - 1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t la = xa + (uint32_t)(kM * kXStride + row) * 4u;
+        const uint32_t va = xa + (uint32_t)(row * kXStride + 4 * lane) * 4u;
+        lc[b][c] = C > 1 ? ld_dsmem_f32(mapa_shared(la, (uint32_t)c)) : lds_f32(la);
+        v[b][c] = C > 1 ? ld_dsmem_v4(mapa_shared(va, (uint32_t)c)) : lds_f4(va);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int row = r0 + 4 * b;
+      if (row >= row_end) break;
+      float L = -CUDART_INF_F;
+#pragma unroll
+      for (int c = 0; c < C; ++c) L = fmaxf(L, lc[b][c]);
+      float wsum = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        // staged rows are finite (zeros for a CTA without keys): zero weights need no branch
+        const float wt = lc[b][c] == -CUDART_INF_F ? 0.f : exp2f(lc[b][c] - L);
+        wsum += wt;
+        acc.x = fmaf(wt, v[b][c].x, acc.x);
+        acc.y = fmaf(wt, v[b][c].y, acc.y);
+        acc.z = fmaf(wt, v[b][c].z, acc.z);
+        acc.w = fmaf(wt, v[b][c].w, acc.w);
+      }
+      const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+      acc = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      if (K == 1) {
+        store_bf16x4(out_ptr(row), acc);
+      } else {
+        *reinterpret_cast<float4*>(p.part_o + ((s0 + w.split) * kM + row) * kD + 4 * lane) = acc;
+        if (lane == 0) p.part_lse[(s0 + w.split) * kM + row] = wsum > 0.f ? L + __log2f(wsum) : -CUDART_INF_F;
+      }
+    }
+  }
+  GTRACE_T(true, 10);
+  if (K > 1 && p.cm_tickets) {
+    // In-kernel variant of cm_merge_kernel: the last of the K clusters' rank-r CTAs to
+    // arrive (atomic ticket, no spin waits) merges the K block partials of block r.
+    __threadfence();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
+    __shared__ uint32_t last[2];
+    if (t == 0) {
+      int* cnt = p.cm_tickets + ((int64_t)ly * p.n_groups + w.group) * C + rank;
+      const int old = atomicAdd(cnt, 1);
+      last[k] = old == K - 1 ? 1u : 0u;
+      if (old == K - 1) *cnt = 0;   // every arrival is in: ready for the next launch
+    }
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
+    GTRACE_T(true, 11);
+    if (last[k]) {
+      __threadfence();
+      constexpr int MB = 4;   // rows per batch of loads
+      for (int r0 = row0 + wq; r0 < row_end; r0 += 4 * MB) {
+        float m[MB], wsum[MB];
+        float4 acc[MB];
+#pragma unroll
+        for (int b = 0; b < MB; ++b) {
+          m[b] = -CUDART_INF_F;
+          wsum[b] = 0.f;
+          acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int j0 = 0; j0 < K; j0 += 4) {
+          float l[MB][4];
+          float4 v[MB][4];
+#pragma unroll
+          for (int b = 0; b < MB; ++b)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int row = min(r0 + 4 * b, row_end - 1);
+              const int j = min(j0 + jj, K - 1);
+              l[b][jj] = j0 + jj < K ? __ldcg(p.part_lse + (s0 + j) * kM + row) : -CUDART_INF_F;
+              v[b][jj] = __ldcg(reinterpret_cast<const float4*>(p.part_o + ((s0 + j) * kM + row) * kD) + lane);
+            }
+#pragma unroll
+          for (int b = 0; b < MB; ++b) {
+            float mb = m[b];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) mb = fmaxf(mb, l[b][jj]);
+            if (mb == -CUDART_INF_F) continue;
+            const float sc = m[b] == -CUDART_INF_F ? 0.f : exp2f(m[b] - mb);
+            wsum[b] *= sc;
+            acc[b] = make_float4(acc[b].x * sc, acc[b].y * sc, acc[b].z * sc, acc[b].w * sc);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const float wt = l[b][jj] == -CUDART_INF_F ? 0.f : exp2f(l[b][jj] - mb);
+              wsum[b] += wt;
+              acc[b].x = fmaf(wt, v[b][jj].x, acc[b].x);
+              acc[b].y = fmaf(wt, v[b][jj].y, acc[b].y);
+              acc[b].z = fmaf(wt, v[b][jj].z, acc[b].z);
+              acc[b].w = fmaf(wt, v[b][jj].w, acc[b].w);
+            }
+            m[b] = mb;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < MB; ++b) {
+          const int row = r0 + 4 * b;
+          if (row >= row_end) break;
+          const float inv = wsum[b] > 0.f ? 1.f / wsum[b] : 0.f;
+          store_bf16x4(out_ptr(row), make_float4(acc[b].x * inv, acc[b].y * inv, acc[b].z * inv, acc[b].w * inv));
+        }
+      }
+    }
+  }
+}
+
+// Groups spread over K > 1 clusters: merge the K block partials of every row
+// (log-sum-exp, R-11) -- a small grid launched right behind the attention
+// kernel (programmatic dependent launch: its prologue overlaps the attention
+// kernel's tail).  Block b of layer y: group b / 32, rows 4 (b % 32) .. +4, one
+// row per warp, lane l columns [4l, 4l+4) (coalesced 512-byte rows); the K
+// partials are read 8 at a time with an online rescale (one pass).
+__global__ void __launch_bounds__(128) cm_merge_kernel(const AttnParams p) {
+  griddep_launch_dependents();
+  const int g = blockIdx.x >> 5;
+  const Group gr = p.groups[g];
+  const int K = gr.n_splits;
+  const int G = p.G;
+  const int row = (blockIdx.x & 31) * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int ly = blockIdx.y;
+  const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
+  const SegDesc sg = p.segs[gr.seg];
+  griddep_wait();   // the attention grid's partials
+  if (K <= 1 || row >= gr.q_ntok * G) return;
+  constexpr int B = 8;
+  float m = -CUDART_INF_F, wsum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j0 = 0; j0 < K; j0 += B) {
+    float l[B];
+    float4 v[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int j = min(j0 + b, K - 1);
+      l[b] = j0 + b < K ? __ldcg(p.part_lse + (s0 + j) * kM + row) : -CUDART_INF_F;
+      v[b] = __ldcg(reinterpret_cast<const float4*>(p.part_o + ((s0 + j) * kM + row) * kD) + lane);
+    }
+    float mb = m;
+#pragma unroll
+    for (int b = 0; b < B; ++b) mb = fmaxf(mb, l[b]);
+    if (mb == -CUDART_INF_F) continue;
+    const float sc = m == -CUDART_INF_F ? 0.f : exp2f(m - mb);
+    wsum *= sc;
+    acc = make_float4(acc.x * sc, acc.y * sc, acc.z * sc, acc.w * sc);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const float wt = l[b] == -CUDART_INF_F ? 0.f : exp2f(l[b] - mb);
+      wsum += wt;
+      acc.x = fmaf(wt, v[b].x, acc.x);
+      acc.y = fmaf(wt, v[b].y, acc.y);
+      acc.z = fmaf(wt, v[b].z, acc.z);
+      acc.w = fmaf(wt, v[b].w, acc.w);
+    }
+    m = mb;
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+  const int64_t orow = in_l + sg.row0 + gr.q_tok0 + row / G;
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + gr.kv_head * G + row % G) * kD + 4 * lane;
+  store_bf16x4(out, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+}
 
 // D[tmem] (+)= A[tmem] * B[smem desc]  (A = P, K-major in TMEM).
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -231,6 +592,17 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ly = blockIdx.y;
+  GTRACE(threadIdx.x == 0, 0);
+  // the next grid in the stream may be scheduled now (it waits in griddepcontrol.wait
+  // before touching memory); its CTAs take SMs as this grid's CTAs exit
+  griddep_launch_dependents();
+#ifdef SSA_GTRACE
+  if (threadIdx.x == 0 && blockIdx.x < kGtCtas) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_gtrace[(p.layer0 + blockIdx.y) & 31][blockIdx.x][7] = smid;
+  }
+#endif
   const TcPair pr = p.pairs[blockIdx.x];
   const WorkUnit w0 = p.units[pr.ua];
   WorkUnit w1 = w0;
@@ -291,6 +663,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
+  GTRACE(threadIdx.x == 0, 1);
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsWG0));
@@ -325,6 +698,73 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
         const bool is_k = F8 ? lane == 0 : warp == 0;
+        const int pw = is_k ? 0 : 1;
+        const uint64_t pol = l2_policy_evict_first();
+        // Page ids of both slots' first tiles (a 16-byte-load window per slot) before
+        // waiting for the previous grid: page tables are written only by copies, which a
+        // programmatic launch never overlaps.
+        for (int k = 0; k < 2; ++k) {
+          bar.pwin_base[pw][k] = -(1 << 30);
+          const WorkUnit& w = k ? w1 : w0;
+          if (k == 1 && pr.ub < 0) continue;
+          const SegDesc sg = p.segs[w.seg];
+          if (w.tile_hi > w.tile_lo && w.tile_lo * kBN < sg.n_slots)
+            (void)page_window(bar.pwin_base[pw][k], bar.pwin[pw][k], sg, (w.tile_lo * kBN) / p.P);
+        }
+        const int E = nt0 + nt1 - nsh;
+        const int m01 = min(nt0, nt1) - nsh;
+        const int NR = is_k ? NK : NV;
+        uint8_t* ring = is_k ? k_base : v_base;
+        uint64_t* full = F8 ? (is_k ? bar.k_raw : bar.v_raw) : (is_k ? bar.k_full : bar.v_full);
+        uint64_t* empty = is_k ? bar.k_empty : bar.v_empty;
+        const CUtensorMap* pool_map = is_k ? &maps.pk : &maps.pv;
+        const CUtensorMap* tail_map = is_k ? &maps.kt : &maps.vt;
+        // load event e: (slot k, tile j) -- K or V tile into ring stage e % NR.  Returns
+        // false (nothing issued) for a tail tile when only pool tiles may be loaded yet.
+        // F8: codes, one 128-byte chunk per row, into the stage's upper half; the
+        // converter warps signal k_full / v_full.
+        auto issue = [&](int e, bool pool_only) -> bool {
+          int k, j;
+          if (e < nsh) { k = 0; j = e; }
+          else if (e - nsh < 2 * m01) { k = (e - nsh) & 1; j = nsh + ((e - nsh) >> 1); }
+          else { k = nt0 > nt1 ? 0 : 1; j = nsh + m01 + (e - nsh - 2 * m01); }
+          const WorkUnit& w = k ? w1 : w0;
+          const SegDesc sg = p.segs[w.seg];
+          const int tile = w.tile_lo + j;
+          const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
+          if (pool_only && tile >= n_pool_tiles) return false;
+          const int s = e % NR;
+          if (e >= NR) mbar_wait_lazy(&empty[s], ((e / NR) - 1) & 1);
+          uint8_t* dst = ring + s * kSlotBytes + (F8 ? kChunkBytes : 0);
+          constexpr int nchunk = F8 ? 1 : 2;
+          mbar_arrive_expect_tx(&full[s], nchunk * kChunkBytes);
+          if (tile < n_pool_tiles) {
+            const int key0 = tile * kBN;
+            const int nb = kBN / box_rows;
+            for (int b = 0; b < nb; ++b) {
+              const int slot = key0 + b * box_rows;
+              int32_t row = 0x7FFFFFF0;   // past the tensor -> TMA zero fill
+              if (slot < sg.n_slots) {
+                const int64_t page = page_window(bar.pwin_base[pw][k], bar.pwin[pw][k], sg, slot / p.P);
+                row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
+              }
+              for (int c = 0; c < nchunk; ++c)
+                tma_load_2d_hint(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row, pol);
+            }
+          } else {
+            const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
+            for (int c = 0; c < nchunk; ++c)
+              tma_load_3d(dst + c * kChunkBytes, tail_map, &full[s], c * 64, w.kv_head, krow);
+          }
+          return true;
+        };
+        // With p.pool_early (the previous grid does not write the pool) the first ring
+        // stages of pool tiles are issued before griddepcontrol.wait, so they land while
+        // the previous layer finishes; Q and the tails (inputs) always come after it.
+        int e0 = 0;
+        if (p.pool_early)
+          while (e0 < E && e0 < NR && issue(e0, true)) ++e0;
+        griddep_wait();
         if (is_k && dup) {
           mbar_arrive_expect_tx(&bar.q_full, 2 * 2 * 32 * 128);
           const int32_t qrow = (int32_t)(in_l + p.segs[w0.seg].row0 + w0.q_tok0);
@@ -342,52 +782,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
           }
         }
-        const int E = nt0 + nt1 - nsh;
-        const int m01 = min(nt0, nt1) - nsh;
-        // F8: codes, one 128-byte chunk per row, into the slot's upper half; the
-        // converter warps signal k_full / v_full
-        for (int e = 0; e < E; ++e) {
-          int k, j;
-          if (e < nsh) { k = 0; j = e; }
-          else if (e - nsh < 2 * m01) { k = (e - nsh) & 1; j = nsh + ((e - nsh) >> 1); }
-          else { k = nt0 > nt1 ? 0 : 1; j = nsh + m01 + (e - nsh - 2 * m01); }
-          const WorkUnit& w = k ? w1 : w0;
-          const SegDesc sg = p.segs[w.seg];
-          const int tile = w.tile_lo + j;
-          const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
-          {
-            const bool ik = is_k;
-            const int NR = ik ? NK : NV;
-            uint8_t* ring = ik ? k_base : v_base;
-            uint64_t* full = F8 ? (ik ? bar.k_raw : bar.v_raw) : (ik ? bar.k_full : bar.v_full);
-            uint64_t* empty = ik ? bar.k_empty : bar.v_empty;
-            const CUtensorMap* pool_map = ik ? &maps.pk : &maps.pv;
-            const CUtensorMap* tail_map = ik ? &maps.kt : &maps.vt;
-            const int s = e % NR;
-            if (e >= NR) mbar_wait_lazy(&empty[s], ((e / NR) - 1) & 1);
-            uint8_t* dst = ring + s * kSlotBytes + (F8 ? kChunkBytes : 0);
-            constexpr int nchunk = F8 ? 1 : 2;
-            mbar_arrive_expect_tx(&full[s], nchunk * kChunkBytes);
-            if (tile < n_pool_tiles) {
-              const int key0 = tile * kBN;
-              const int nb = kBN / box_rows;
-              for (int b = 0; b < nb; ++b) {
-                const int slot = key0 + b * box_rows;
-                int32_t row = 0x7FFFFFF0;   // past the tensor -> TMA zero fill
-                if (slot < sg.n_slots) {
-                  const int64_t page = __ldg(sg.pages + slot / p.P);
-                  row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
-                }
-                for (int c = 0; c < nchunk; ++c)
-                  tma_load_2d(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row);
-              }
-            } else {
-              const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
-              for (int c = 0; c < nchunk; ++c)
-                tma_load_3d(dst + c * kChunkBytes, tail_map, &full[s], c * 64, w.kv_head, krow);
-            }
-          }
-        }
+        for (int e = e0; e < E; ++e) (void)issue(e, false);
       }
     } else if (warp == 1) {
       // ----------------------------------------------------------- MMA issuer
@@ -401,6 +796,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const uint64_t vd0 = sdesc_sw128(smem_u32(v_base), kChunkBytes, 1024);
         constexpr uint64_t kStageStep = kSlotBytes >> 4;
         mbar_wait(F8 ? &bar.q_ready : &bar.q_full, 0);
+        GTRACE(true, 2);
         tc_fence_after();
         const int jmax = max(nt0, nt1);
         // prologue: S(k, 0); then per j: PV(k, j) and S(k, j+1) for k = 0, 1
@@ -433,6 +829,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               const int e = event_of(k, jn, nsh, nt0, nt1);
               const int s = e % NK;
               mbar_wait(&bar.k_full[s], (e / NK) & 1);
+              GTRACE(e == 0, 3);
               TRACE(true, 10, jn, k, clock64());
               tc_fence_after();
               const uint64_t qd = k ? qd1 : qd0;
@@ -450,6 +847,10 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           }
         }
       }
+    }
+    if (p.cm_C > 0) {   // the two cluster barriers of the CM epilogue
+      cm_sync(p.cm_C);
+      cm_sync(p.cm_C);
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
@@ -483,6 +884,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const bool is_pool = tile < n_pool_tiles;
         const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBN;
         mbar_wait(&bar.s_full[k], j & 1);
+        GTRACE(r == 0 && k == 0 && j == 0, 4);
         TRACE(r == 0, k, j, 0, clock64());
         tc_fence_after();
         {
@@ -592,72 +994,34 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       // ----------------------------------------------------------- epilogue
       if (nt > 0) {
         mbar_wait(&bar.o_final[k], 0);
+        GTRACE(r == 0 && k == 0, 5);
         tc_fence_after();
       }
-      const int rows = w.q_ntok * G;
+      griddep_wait();   // before the first global write (O / partials of the previous grid's readers)
       const float inv_l = (l_run > 0.f ? 1.f / l_run : 0.f) * (F8 ? p.o_scale : 1.f);   // F8: V scale
+      const float lse = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
       const int h = w.kv_head * G + (rr >= 0 ? rr : 0) % G;
       const bool live = rr >= 0 && rr < w.q_ntok * G;
       const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
       const int64_t orow = in_l + sg.row0 + tok;
       const int unit = k ? pr.ub : pr.ua;
       const int64_t pslot = (int64_t)ly * p.n_units + unit;
-      if (pr.merge) {
-        // The two slots are the two key ranges of one q tile and the whole split group:
-        // log-sum-exp merge (R-11) in the CTA.  Slot 1 leaves its normalized O and lse in
-        // the (now idle) ring shared memory, slot 0 merges and writes O -- no partials in
-        // HBM, no combine launch for the group.
-        float* xo = reinterpret_cast<float*>(k_base);   // [128][129] fp32 (padded rows)
-        float* xl = xo + 128 * 129;                      // [128]
-        const float lse = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
-        if (k == 1) {
-          // the ring may still feed slot 0's last MMAs: wait until they have completed
-          if (nt0 > 0) mbar_wait(&bar.o_final[0], 0);
-#pragma unroll 1
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t ro[32];
-            tmem_ld32(o_col + q4 * 32, ro);
-            tmem_wait_ld();
-            if (live)
-#pragma unroll
-              for (int i = 0; i < 32; ++i) xo[rr * 129 + q4 * 32 + i] = __uint_as_float(ro[i]) * inv_l;
-          }
-          if (live) xl[rr] = lse;
-        }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (k == 0) {
-          float w0 = 0.f, w1 = 0.f;
-          if (live) {
-            const float l1 = xl[rr];
-            const float L = fmaxf(lse, l1);
-            w0 = lse == -CUDART_INF_F ? 0.f : exp2f(lse - L);
-            w1 = l1 == -CUDART_INF_F ? 0.f : exp2f(l1 - L);
-            const float inv = (w0 + w1) > 0.f ? 1.f / (w0 + w1) : 0.f;
-            w0 *= inv * inv_l;
-            w1 *= inv;
-          }
-#pragma unroll 1
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t ro[32];
-            tmem_ld32(o_col + q4 * 32, ro);
-            tmem_wait_ld();
-            if (live) {
-              const float* x1 = xo + rr * 129 + q4 * 32;
-              __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32;
-#pragma unroll
-              for (int i = 0; i < 32; i += 8) {
-                float v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = fmaf(w0, __uint_as_float(ro[i + u]), w1 * x1[i + u]);
-                uint4 pk4;
-                pk4.x = pack_bf16(v[0], v[1]);
-                pk4.y = pack_bf16(v[2], v[3]);
-                pk4.z = pack_bf16(v[4], v[5]);
-                pk4.w = pack_bf16(v[6], v[7]);
-                *reinterpret_cast<uint4*>(out + i) = pk4;
-              }
-            }
-          }
+      if (p.cm_C > 0) {
+        // Cluster merge (CM launch): the ring becomes the exchange buffer of the q
+        // tile(s) once every MMA of the CTA has completed; rows are left normalized
+        // (fp32) with their lse and merged across the cluster after the CTA barrier.
+        const int nt_o = k ? nt0 : nt1;
+        if (pr.ub >= 0 && nt_o > 0) mbar_wait(&bar.o_final[k ^ 1], 0);
+        tc_fence_after();
+        float* X0 = reinterpret_cast<float*>(k_base);
+        if (pr.same_q && pr.ub >= 0) {
+          // split pair: slot 1 stages its rows, slot 0 merges them into its own (R-11)
+          if (k == 1) cm_stage_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f);
+          asm volatile("bar.sync 3, 256;" ::: "memory");
+          if (k == 0) cm_merge_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f);
+          GTRACE_T(true, 8);
+        } else {
+          cm_stage_rows(X0 + (pr.same_q ? 0 : k) * kXFloats, rr, live, o_col, inv_l, lse, l_run > 0.f);
         }
       } else {
 #pragma unroll
@@ -679,87 +1043,46 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
             }
           } else {
             float* out = p.part_o + (pslot * kM + rr) * kD + q4 * 32;
+            const bool has = l_run > 0.f;
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               *reinterpret_cast<float4*>(out + i) =
-                  make_float4(__uint_as_float(ro[i]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l,
-                              __uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l);
+                  has ? make_float4(__uint_as_float(ro[i]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l,
+                                    __uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
         }
       }
-      if (w.group >= 0 && live)
-        p.part_lse[pslot * kM + rr] = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
-      }   // !pr.merge
-      // ------------------------------------------------- fused split-KV merge (R-11)
-      if (w.group >= 0 && p.group_counters) {
-        const Group gr = p.groups[w.group];
-        int* cnt = p.group_counters + (int64_t)ly * p.n_groups + w.group;
-        __threadfence();   // release this thread's partial row
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
-        if (r == 0) {
-          __threadfence();
-          const int old = atomicAdd(cnt, 1);
-          bar.merge_flag[k] = (old == gr.n_splits - 1) ? 1u : 0u;
-        }
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
-        if (bar.merge_flag[k]) {
-          __threadfence();
-          if (live) {
-            const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
-            float L = -CUDART_INF_F;
-            for (int s = 0; s < gr.n_splits; ++s) L = fmaxf(L, __ldcg(p.part_lse + (s0 + s) * kM + rr));
-            float wsum = 0.f;
-            for (int s = 0; s < gr.n_splits; ++s) {
-              const float ls = __ldcg(p.part_lse + (s0 + s) * kM + rr);
-              if (ls != -CUDART_INF_F) wsum += exp2f(ls - L);
-            }
-            const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-#pragma unroll 1
-            for (int q4 = 0; q4 < kD / 32; ++q4) {       // 32 columns at a time
-              float4 acc[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int s = 0; s < gr.n_splits; ++s) {
-                const float ls = __ldcg(p.part_lse + (s0 + s) * kM + rr);
-                if (ls == -CUDART_INF_F) continue;
-                const float wt = exp2f(ls - L) * inv;
-                const float4* src = reinterpret_cast<const float4*>(p.part_o + ((s0 + s) * kM + rr) * kD + q4 * 32);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const float4 v = __ldcg(src + i);
-                  acc[i].x = fmaf(wt, v.x, acc[i].x);
-                  acc[i].y = fmaf(wt, v.y, acc[i].y);
-                  acc[i].z = fmaf(wt, v.z, acc[i].z);
-                  acc[i].w = fmaf(wt, v.w, acc[i].w);
-                }
-              }
-              if (p.o_f32) {
-                float4* out = reinterpret_cast<float4*>(p.o_f32 + (orow * p.Hq + h) * kD + q4 * 32);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) out[i] = acc[i];
-              } else {
-                uint4* out = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD + q4 * 32);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  uint4 v;
-                  v.x = pack_bf16(acc[2 * i].x, acc[2 * i].y);
-                  v.y = pack_bf16(acc[2 * i].z, acc[2 * i].w);
-                  v.z = pack_bf16(acc[2 * i + 1].x, acc[2 * i + 1].y);
-                  v.w = pack_bf16(acc[2 * i + 1].z, acc[2 * i + 1].w);
-                  out[i] = v;
-                }
-              }
-            }
-            if (p.lse_out) p.lse_out[orow * p.Hq + h] = wsum > 0.f ? L + __log2f(wsum) : -CUDART_INF_F;
-          }
-          if (r == 0) *cnt = 0;   // ready for the next launch
+      if (w.group >= 0 && live) p.part_lse[pslot * kM + rr] = lse;
+      }   // !cm
+    }
+    if (p.cm_C > 0) {
+      cm_sync(p.cm_C);   // every CTA of the cluster has staged its rows
+      GTRACE_T(true, 9);
+      if (k < (two_q ? 2 : 1)) {
+        const float* X = reinterpret_cast<const float*>(k_base) + k * kXFloats;
+        const WorkUnit& wk = k ? w1 : w0;
+        switch (p.cm_C) {
+          case 1: cm_reduce<1>(p, wk, X, k); break;
+          case 2: cm_reduce<2>(p, wk, X, k); break;
+          case 3: cm_reduce<3>(p, wk, X, k); break;
+          case 4: cm_reduce<4>(p, wk, X, k); break;
+          case 5: cm_reduce<5>(p, wk, X, k); break;
+          case 6: cm_reduce<6>(p, wk, X, k); break;
+          case 7: cm_reduce<7>(p, wk, X, k); break;
+          case 8: cm_reduce<8>(p, wk, X, k); break;
+          default: cm_reduce<16>(p, wk, X, k); break;
         }
       }
+      GTRACE_T(true, 12);
+      cm_sync(p.cm_C);   // peers have finished reading this CTA's shared memory
+      GTRACE_T(true, 13);
     }
   }
   tc_fence_before();
   __syncthreads();
+  GTRACE(threadIdx.x == 0, 6);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -815,7 +1138,11 @@ bool encode_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* di
 int tc_key_tile() { return kBN; }
 
 int tc_debug_trace(void* host, size_t bytes) {
-#ifdef SSA_TRACE
+#if defined(SSA_GTRACE)
+  if (bytes < sizeof(g_gtrace)) return -1;
+  if (cudaMemcpyFromSymbol(host, g_gtrace, sizeof(g_gtrace)) != cudaSuccess) return -1;
+  return (int)sizeof(g_gtrace);
+#elif defined(SSA_TRACE)
   if (bytes < sizeof(g_trace)) return -1;
   if (cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)) != cudaSuccess) return -1;
   return (int)sizeof(g_trace);
@@ -829,8 +1156,7 @@ bool tc_supported_shape(int D, int G, bool bf16) {
   return bf16 && D == kD && G >= 1 && G <= 16 && (kM % G) == 0 && get_encode() != nullptr;
 }
 
-cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, cudaStream_t s) {
-  (void)q_tiles_opt;
+cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s) {
   if (p.n_pairs == 0 || n_layers == 0) return cudaSuccess;
   if (!tc_supported_shape(p.D, p.G, true)) return cudaErrorNotSupported;
   TcMaps maps;
@@ -863,17 +1189,91 @@ cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, c
     if (!encode_map(&maps.pk, p.poolK, 2, dims, str, box, u8)) return cudaErrorInvalidValue;
     if (!encode_map(&maps.pv, p.poolV, 2, dims, str, box, u8)) return cudaErrorInvalidValue;
   }
-  const size_t smem = (size_t)kNumSlots * kSlotBytes + sizeof(Bars) + 1024;
-  static bool configured[2] = {false, false};
   auto kern = p.kv_fp8 ? attn_tc_kernel<true> : attn_tc_kernel<false>;
-  if (!configured[p.kv_fp8 ? 1 : 0]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured[p.kv_fp8 ? 1 : 0] = true;
+  cudaError_t e = tc_configure(p.kv_fp8 != 0);
+  if (e != cudaSuccess) return e;
+  if (p.cm_C > 1 && p.n_pairs % p.cm_C) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_pairs, n_layers, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = tc_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (p.cm_C > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)p.cm_C;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
-  dim3 grid(p.n_pairs, n_layers);
-  kern<<<grid, kThreads, smem, s>>>(p, maps, box_rows);
-  return cudaGetLastError();
+  if (pdl) {
+    // programmatic dependent launch: the CTA prologue (barriers, TMEM, descriptor and
+    // page-id prefetch) overlaps the previous grid's tail; memory is touched only
+    // after griddepcontrol.wait
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, p, maps, box_rows);
+}
+
+cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_groups * 32, n_layers, 1);
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, cm_merge_kernel, p);
+}
+
+size_t tc_smem_bytes() { return (size_t)kNumSlots * kSlotBytes + sizeof(Bars) + 1024; }
+
+// cudaFuncSetAttribute is per device: configure each (device, variant) once.
+cudaError_t tc_configure(bool f8) {
+  static std::mutex mu;
+  static uint64_t done[2] = {0, 0};   // bit d: device d configured
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && (done[f8 ? 1 : 0] >> dev) & 1) return cudaSuccess;
+  auto kern = f8 ? attn_tc_kernel<true> : attn_tc_kernel<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);   // clusters of 16
+  if (e != cudaSuccess) return e;
+  if (dev < 64) done[f8 ? 1 : 0] |= 1ull << dev;
+  return cudaSuccess;
+}
+
+// Clusters of `c` CTAs (one per SM) that can be co-resident on the current device.
+int tc_max_active_clusters(int c, bool f8) {
+  if (tc_configure(f8) != cudaSuccess) return 0;
+  auto kern = f8 ? attn_tc_kernel<true> : attn_tc_kernel<false>;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c * 64, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = tc_smem_bytes();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)c;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 }  // namespace ssa

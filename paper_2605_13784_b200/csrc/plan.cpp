@@ -7,6 +7,7 @@
 // launch fills the GPU (148 SMs on B200).  Units of one (segment, q tile, kv
 // head) form a Group merged by the combine kernel (log-sum-exp, reading R-11).
 #include <algorithm>
+#include <cmath>
 #include <functional>
 #include <queue>
 #include <tuple>
@@ -155,44 +156,6 @@ static int shared_tiles(const std::vector<SegDesc>& segs, const WorkUnit& a, con
   return std::max(0, std::min(std::min(na, nb), pool_tiles - a.tile_lo));
 }
 
-void pair_units_cta2(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
-                     std::vector<char>* used) {
-  out->clear();
-  const int n = (int)plan.units.size();
-  used->assign(n, 0);
-  // Two units can share every tcgen05.mma of a CTA pair when all their key
-  // tiles are the same keys: same KV head and tile range, and the same segment
-  // (q tiles of one append / prompt) or the same cached pool with no private
-  // own-token tiles in the range.
-  auto pool_tiles = [&](const WorkUnit& u) { return (segs[u.seg].n_slots + key_tile - 1) / key_tile; };
-  auto same_keys = [&](const WorkUnit& a, const WorkUnit& b) {
-    if (a.kv_head != b.kv_head || a.tile_lo != b.tile_lo || a.tile_hi != b.tile_hi) return false;
-    if (a.seg == b.seg) return a.q_tok0 != b.q_tok0;
-    const SegDesc& x = segs[a.seg];
-    const SegDesc& y = segs[b.seg];
-    return x.pages == y.pages && x.n_slots == y.n_slots && x.hole_lo == y.hole_lo && x.hole_hi == y.hole_hi &&
-           a.tile_hi <= pool_tiles(a);
-  };
-  std::vector<int> order(n);
-  for (int i = 0; i < n; ++i) order[i] = i;
-  auto key_of = [&](int i) {
-    const WorkUnit& u = plan.units[i];
-    const SegDesc& s = segs[u.seg];
-    return std::make_tuple(u.kv_head, u.tile_lo, u.tile_hi, (uintptr_t)s.pages, s.n_slots, u.seg, u.q_tok0);
-  };
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key_of(a) < key_of(b); });
-  for (int ii = 0; ii + 1 < n; ++ii) {
-    const int a = order[ii], b = order[ii + 1];
-    if ((*used)[a] || (*used)[b]) continue;
-    if (plan.units[a].tile_hi == plan.units[a].tile_lo) continue;
-    if (same_keys(plan.units[a], plan.units[b])) {
-      (*used)[a] = (*used)[b] = 1;
-      out->push_back({a, b, plan.units[a].tile_hi - plan.units[a].tile_lo, 0});
-    }
-  }
-  std::stable_sort(out->begin(), out->end(), [](const TcPair& x, const TcPair& y) { return x.n_shared > y.n_shared; });
-}
-
 void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
                 const std::vector<char>* skip) {
   out->clear();
@@ -249,6 +212,191 @@ void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile
     return 2 * (wa + wb) + (wa + wb - p.n_shared);
   };
   std::stable_sort(out->begin(), out->end(), [&](const TcPair& a, const TcPair& b) { return work(a) > work(b); });
+}
+
+}  // namespace ssa
+
+namespace ssa {
+
+double plan_cm(const std::vector<SegDesc>& segs, const PlanConfig& c, int C, int max_clusters, Plan* plan,
+               std::vector<TcPair>* pairs) {
+  plan->units.clear();
+  plan->groups.clear();
+  pairs->clear();
+  if (C < 1 || max_clusters < 1) return -1.0;
+  struct Item { int seg, kvh, tok0, ntok; int tiles; };
+  std::vector<Item> items;
+  for (int s = 0; s < (int)segs.size(); ++s) {
+    const SegDesc& sg = segs[s];
+    const int pool_tiles = (int)ceil_div(sg.n_slots, c.key_tile);
+    for (int tok0 = 0; tok0 < sg.m; tok0 += c.q_tile_tokens) {
+      const int ntok = std::min(c.q_tile_tokens, sg.m - tok0);
+      const int tail_tiles = (int)ceil_div(std::min(tok0 + ntok, sg.tail_m), c.key_tile);
+      for (int h = 0; h < c.Hkv; ++h) items.push_back({s, h, tok0, ntok, pool_tiles + tail_tiles});
+    }
+  }
+  if (items.empty()) return -1.0;
+  // pair-items: SHARED (two q tiles over common leading key tiles) or SPLIT (one q tile)
+  struct PItem { int a, b; int sh; double work; int cap; };
+  std::vector<int> order(items.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  auto key_of = [&](int i) {
+    const Item& it = items[i];
+    const SegDesc& sg = segs[it.seg];
+    return std::make_tuple(it.kvh, (uintptr_t)sg.pages, sg.n_slots, sg.hole_lo, sg.hole_hi, it.seg, it.tok0);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key_of(x) < key_of(y); });
+  auto common = [&](const Item& x, const Item& y) -> int {
+    if (x.kvh != y.kvh) return 0;
+    if (x.seg == y.seg) return std::min(x.tiles, y.tiles);
+    const SegDesc& a = segs[x.seg];
+    const SegDesc& b = segs[y.seg];
+    if (a.n_slots == 0 || a.pages != b.pages || a.n_slots != b.n_slots || a.hole_lo != b.hole_lo || a.hole_hi != b.hole_hi)
+      return 0;
+    return (int)ceil_div(a.n_slots, c.key_tile);
+  };
+  std::vector<PItem> pis;
+  for (size_t i = 0; i < order.size(); ++i) {
+    const Item& x = items[order[i]];
+    if (i + 1 < order.size()) {
+      const Item& y = items[order[i + 1]];
+      const int sh = common(x, y);
+      if (sh > 0) {
+        pis.push_back({order[i], order[i + 1], sh, (double)(x.tiles + y.tiles - sh), std::max(1, sh)});
+        ++i;
+        continue;
+      }
+    }
+    // SPLIT: a CTA's two slots take two key ranges of the q tile
+    pis.push_back({order[i], -1, 0, 0.5 * x.tiles + 0.5, std::max(1, x.tiles / 2)});
+  }
+  // clusters per pair-item: K_p = 1 each, then one more to the most loaded while they fit
+  const int np = (int)pis.size();
+  std::vector<int> K(np, 1);
+  int used = np;
+  auto per_cta = [&](int i) { return pis[i].work / (double)(C * K[i]); };
+  if (np <= max_clusters) {
+    std::priority_queue<std::pair<double, int>> q;
+    for (int i = 0; i < np; ++i) q.push({per_cta(i), i});
+    while (used < max_clusters && !q.empty()) {
+      const int i = q.top().second;
+      q.pop();
+      if (C * (K[i] + 1) > pis[i].cap) continue;   // no empty ranges beyond this
+      ++K[i];
+      ++used;
+      q.push({per_cta(i), i});
+    }
+    // give back clusters that do not lower the makespan (ties: one spare cluster for
+    // one of several equally loaded items only adds a merge)
+    double mx = 0.0;
+    for (int i = 0; i < np; ++i) mx = std::max(mx, per_cta(i));
+    for (int i = 0; i < np; ++i)
+      while (K[i] > 1 && pis[i].work / (double)(C * (K[i] - 1)) <= mx) {
+        --K[i];
+        --used;
+      }
+  }
+  // cost: largest per-CTA range, with waves if the clusters do not fit at once
+  double cost = 0.0;
+  const double waves = std::ceil((double)used / (double)max_clusters);
+  for (int i = 0; i < np; ++i) {
+    const double merge = (C > 1 ? 0.25 : 0.0) + (K[i] > 1 ? 1.0 + 0.5 * (K[i] - 1) / (double)C : 0.0);
+    cost = std::max(cost, per_cta(i) + merge);
+  }
+  cost *= waves;
+  // units, groups and CTAs, cluster by cluster
+  for (int i = 0; i < np; ++i) {
+    const PItem& pi = pis[i];
+    const int S = C * K[i];
+    auto new_group = [&](const Item& it) {
+      plan->groups.push_back({it.seg, it.kvh, it.tok0, it.ntok, (int)plan->units.size(), K[i]});
+      return (int)plan->groups.size() - 1;
+    };
+    if (pi.b < 0) {
+      const Item& it = items[pi.a];
+      const int g = new_group(it);
+      for (int u = 0; u < 2 * S; ++u) {
+        WorkUnit w;
+        w.seg = it.seg;
+        w.kv_head = it.kvh;
+        w.q_tok0 = it.tok0;
+        w.q_ntok = it.ntok;
+        w.tile_lo = (int)((int64_t)it.tiles * u / (2 * S));
+        w.tile_hi = (int)((int64_t)it.tiles * (u + 1) / (2 * S));
+        w.group = g;
+        w.split = (u / 2) / C;
+        if (c.fault == 1 && u == 2 * S - 1) w.tile_hi = std::max(w.tile_lo, w.tile_hi - 1);
+        plan->units.push_back(w);
+      }
+      const int u0 = plan->groups[g].unit0;
+      for (int j = 0; j < S; ++j) pairs->push_back({u0 + 2 * j, u0 + 2 * j + 1, 0, 1});
+    } else {
+      const Item& ia = items[pi.a];
+      const Item& ib = items[pi.b];
+      const int ga = new_group(ia);
+      for (int j = 0; j < S; ++j) {
+        WorkUnit w;
+        w.seg = ia.seg;
+        w.kv_head = ia.kvh;
+        w.q_tok0 = ia.tok0;
+        w.q_ntok = ia.ntok;
+        w.tile_lo = (int)((int64_t)pi.sh * j / S);
+        w.tile_hi = j == S - 1 ? ia.tiles : (int)((int64_t)pi.sh * (j + 1) / S);
+        w.group = ga;
+        w.split = j / C;
+        plan->units.push_back(w);
+      }
+      const int gb = new_group(ib);
+      for (int j = 0; j < S; ++j) {
+        WorkUnit w;
+        w.seg = ib.seg;
+        w.kv_head = ib.kvh;
+        w.q_tok0 = ib.tok0;
+        w.q_ntok = ib.ntok;
+        w.tile_lo = (int)((int64_t)pi.sh * j / S);
+        w.tile_hi = j == S - 1 ? ib.tiles : (int)((int64_t)pi.sh * (j + 1) / S);
+        w.group = gb;
+        w.split = j / C;
+        if (c.fault == 1 && j == S - 1) w.tile_hi = std::max(w.tile_lo, w.tile_hi - 1);
+        plan->units.push_back(w);
+      }
+      const int ua0 = plan->groups[ga].unit0, ub0 = plan->groups[gb].unit0;
+      for (int j = 0; j < S; ++j) {
+        const WorkUnit& a = plan->units[ua0 + j];
+        const WorkUnit& b = plan->units[ub0 + j];
+        const int n_sh = std::max(0, std::min(std::min(a.tile_hi, b.tile_hi), pi.sh) - a.tile_lo);
+        pairs->push_back({ua0 + j, ub0 + j, n_sh, 0});
+      }
+    }
+  }
+  return cost;
+}
+
+void cm_regroup(Plan* plan, const std::vector<TcPair>& pairs) {
+  // singleton groups for unsplit units
+  for (int u = 0; u < (int)plan->units.size(); ++u) {
+    WorkUnit& w = plan->units[u];
+    if (w.group >= 0) continue;
+    plan->groups.push_back({w.seg, w.kv_head, w.q_tok0, w.q_ntok, u, 1});
+    w.group = (int)plan->groups.size() - 1;
+    w.split = 0;
+  }
+  // CTA index of every unit within its group
+  std::vector<int> n_ctas(plan->groups.size(), 0);
+  for (const TcPair& pr : pairs) {
+    WorkUnit& a = plan->units[pr.ua];
+    const int ia = n_ctas[a.group]++;
+    a.split = ia;
+    if (pr.ub >= 0) {
+      WorkUnit& b = plan->units[pr.ub];
+      if (pr.same_q && b.group == a.group) {
+        b.split = ia;   // merged with `a` in the CTA
+      } else {
+        b.split = n_ctas[b.group]++;
+      }
+    }
+  }
+  for (size_t g = 0; g < plan->groups.size(); ++g) plan->groups[g].n_splits = n_ctas[g];
 }
 
 }  // namespace ssa

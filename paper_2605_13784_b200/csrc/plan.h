@@ -34,10 +34,23 @@ void plan_units(const std::vector<SegDesc>& segs, const PlanConfig& c, Plan* out
 void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
                 const std::vector<char>* skip = nullptr);
 
-// Pair units whose key tiles are the same keys into cta_group::2 CTA pairs
-// (kernels_tc2.cu): ua runs on CTA rank 0, ub on rank 1; n_shared = tiles.
-// `used` marks the paired units (the rest go to pair_units).
-void pair_units_cta2(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile, std::vector<TcPair>* out,
-                     std::vector<char>* used);
+// Cluster-merge plans (kernels_tc.cu "CM"; AttnParams::cm_C).
+//
+// plan_cm: a single launch layer.  Every (segment, q tile, kv head) item is a
+// group; consecutive q tiles of one segment over the same keys (or single-q-tile
+// segments over one cached pool, e.g. Flash Queries) pair up as SHARED CTAs, a
+// lone q tile runs as SPLIT CTAs (two key ranges per CTA).  Pair-item p gets K_p
+// clusters of C CTAs (consecutive CTAs, C key ranges each), K_p chosen so that
+// the clusters fit `max_clusters` and the largest per-CTA key range is smallest.
+// Returns the estimated makespan in key tiles (+ merge overheads), or -1 if the
+// plan does not apply.
+double plan_cm(const std::vector<SegDesc>& segs, const PlanConfig& c, int C, int max_clusters, Plan* plan,
+               std::vector<TcPair>* pairs);
+
+// cm_regroup: turn an LPT plan (plan_units + pair_units) into a C = 1 CM plan:
+// every unit gets a group (singletons for unsplit units), Group::n_splits becomes
+// the number of CTAs holding the group and WorkUnit::split the unit's CTA index
+// within it (both units of a SPLIT pair share one, merged in the CTA).
+void cm_regroup(Plan* plan, const std::vector<TcPair>& pairs);
 
 }  // namespace ssa

@@ -62,7 +62,6 @@ struct TcPair {
   int32_t ua, ub;     // unit indices (ub = -1: single slot)
   int32_t n_shared;   // leading tiles shared by both slots
   int32_t same_q;
-  int32_t merge;      // the two units are the whole split group: merged in the CTA's epilogue
 };
 
 struct AttnParams {
@@ -90,11 +89,18 @@ struct AttnParams {
   int32_t fault;         // SSA_OPT_FAULT_INJECT
   const TcPair* pairs;   // tcgen05 CTAs (per layer)
   int32_t n_pairs;
-  // fused split-KV merge (tcgen05 path): the last unit of a group to finish
-  // merges the group's partials; counters are zero between launches.
-  int32_t* group_counters;   // [layers][n_groups], or null: separate combine kernel
-  float* o_f32;              // optional fp32 O output (O layout) instead of O
-  float* lse_out;            // optional lse output (log2, [rows][Hq])
+  // Cluster merge (tcgen05 path, kernels_tc.cu "CM"): cm_C = cluster size (CTAs
+  // per cluster, consecutive blockIdx.x), 0 = off (partials + combine kernel).
+  // In CM every unit has a group; Group::n_splits = K clusters per group and
+  // WorkUnit::split = the unit's cluster index in [0, K); groups with K > 1 leave
+  // K block partials for cm_merge_kernel.
+  int32_t cm_C;
+  // 1: the previous grid in the stream does not write the KV pool, so pool tiles may
+  // be loaded before griddepcontrol.wait (programmatic dependent launch)
+  int32_t pool_early;
+  // groups over K > 1 clusters: merge tickets [layers][n_groups][cm_C] (zero between
+  // launches) for the in-kernel last-arriver merge, or null: cm_merge_kernel
+  int32_t* cm_tickets;
   // FP8 KV variant (reading R-22): pools and Kt/Vt hold E4M3 codes; scale_log2
   // already includes k_scale, o_scale = v_scale multiplies 1/l
   int32_t kv_fp8;

@@ -341,24 +341,44 @@ void ssa_store::fill_cached(const Session& s, SegDesc* sg) const {
 
 static bool capturing(void* stream);
 
+// Scratch grows in stream order (cudaMallocAsync / cudaFreeAsync on the call's
+// stream): earlier calls on other streams are ordered before it by enter().
 ssa_status ssa_store::ensure_scratch(size_t part_o_floats, size_t part_lse_floats, cudaStream_t st) {
   if (part_o_floats > part_o_cap || part_lse_floats > part_lse_cap) {
     if (capturing(st)) {
       ssa::set_error("CUDA-graph capture: warm up the call once before capturing (split-KV scratch)");
       return SSA_ERR_STATE;
     }
-    SSA_CUDA(this, cudaStreamSynchronize(st));
-    SSA_CUDA(this, cudaDeviceSynchronize());
-    if (part_o) cudaFree(part_o);
-    if (part_lse) cudaFree(part_lse);
+    if (part_o) SSA_CUDA(this, cudaFreeAsync(part_o, st));
+    if (part_lse) SSA_CUDA(this, cudaFreeAsync(part_lse, st));
     part_o = nullptr;
     part_lse = nullptr;
     part_o_cap = std::max(part_o_floats, part_o_cap * 2);
     part_lse_cap = std::max(part_lse_floats, part_lse_cap * 2);
-    SSA_CUDA(this, cudaMalloc(&part_o, part_o_cap * sizeof(float)));
-    SSA_CUDA(this, cudaMalloc(&part_lse, part_lse_cap * sizeof(float)));
+    SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&part_o), part_o_cap * sizeof(float), st));
+    SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&part_lse), part_lse_cap * sizeof(float), st));
   }
   return SSA_OK;
+}
+
+// Cross-stream ordering of the store's device work (one dispatch order).
+ssa_status ssa_store::enter(cudaStream_t st) {
+  if (capturing(st)) return SSA_OK;
+  if (order_valid && st != order_stream) SSA_CUDA(this, cudaStreamWaitEvent(st, order_ev, 0));
+  return SSA_OK;
+}
+void ssa_store::leave(cudaStream_t st) {
+  if (capturing(st) || failed) return;
+  if (!order_ev && cudaEventCreateWithFlags(&order_ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (cudaEventRecord(order_ev, st) == cudaSuccess) {
+    order_stream = st;
+    order_valid = true;
+  } else {
+    cudaGetLastError();
+  }
 }
 
 // --------------------------------------------------------------- staging
@@ -409,11 +429,10 @@ ssa_status ssa_store::stage_plan(IoSet* io, cudaStream_t st) {
   };
   plan_one(io->q); plan_one(io->k); plan_one(io->v); plan_one(io->o);
   if (need > stage_cap) {
-    SSA_CUDA(this, cudaDeviceSynchronize());
-    if (stage) cudaFree(stage);
+    if (stage) SSA_CUDA(this, cudaFreeAsync(stage, st));
     stage = nullptr;
     stage_cap = std::max(need, stage_cap * 2);
-    SSA_CUDA(this, cudaMalloc(&stage, stage_cap));
+    SSA_CUDA(this, cudaMallocAsync(&stage, stage_cap, st));
   }
   for (IoBuf* b : {&io->q, &io->k, &io->v, &io->o})
     if (b->host) b->dev = static_cast<char*>(stage) + b->stage_off;
@@ -431,8 +450,7 @@ ssa_status ssa_store::run_pipelined(std::vector<SegDesc>& segs, IoSet& io, int64
   if (rc != SSA_OK) return rc;
   // 2 chunks measured best on the 32-layer 32k query (1.01 vs 1.09 ms unpipelined;
   // 4 and 8 chunks were slower: smaller launches, more per-chunk overhead)
-  int chunks = std::min(2, n_layers);
-  if (const char* e = getenv("SSA_PIPE_CHUNKS")) chunks = std::max(1, std::min(atoi(e), n_layers));   // experiments
+  int chunks = std::min(opt_pipe_chunks > 0 ? (int)opt_pipe_chunks : 2, n_layers);
   if (!h2d_stream) {
     SSA_CUDA(this, cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
     SSA_CUDA(this, cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
@@ -486,164 +504,187 @@ ssa_status ssa_store::unstage_output(IoSet* io, cudaStream_t st) {
 }
 
 // --------------------------------------------------------------- one launch
+// Cluster size of a CM plan for a single-layer tcgen05 launch (kernels_tc.cu
+// "CM"): the planner is run for C in 1..8 and 16 (or the forced SSA_OPT_CLUSTER
+// size) against the device's co-resident cluster count and the cheapest plan wins.
+int ssa_store::max_clusters(int C) {
+  if (C < 1 || C > 16) return 0;
+  if (max_clusters_[kv_fp8][C] < 0) {
+    const int n = C == 1 ? num_sms : tc_max_active_clusters(C, kv_fp8);
+    max_clusters_[kv_fp8][C] = n > 0 ? n : 0;
+  }
+  return max_clusters_[kv_fp8][C];
+}
+
 // Runs KA (scatter of appended segments) and the attention kernels for `segs`
 // over input layers [0, n_layers) mapped to pool layers layer0 + y.
+//
+// Work lists (segments, units, groups, CTA pairs, scatter segments) are a pure
+// function of the call shape; the store keeps the device copy of the last 16
+// shapes' lists, so a repeated call (per-layer queries, the steps of a session,
+// Flash Query cycles) launches with no planning and no host->device copy.
 ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t rows_per_layer,
                           int32_t layer0, int32_t n_layers, int32_t in_layer_stride, bool compute_o,
                           bool query_plane, cudaStream_t st, const RunOpts& opts) {
   const int G = cfg.num_q_heads / cfg.num_kv_heads;
   const int D = cfg.head_dim;
-  // ---- plan attention
-  Plan plan;
-  PlanConfig pc;
   const bool use_tc = compute_o && tc_eligible(segs);
   if (kv_fp8 && compute_o && !use_tc) {
     ssa::set_error("E4M3 KV cache: attention needs the tcgen05 path (sm_100, default backend)");
     return SSA_ERR_UNSUPPORTED;
   }
-  if (compute_o) {
-    pc.Hkv = cfg.num_kv_heads;
-    pc.key_tile = use_tc ? tc_key_tile() : simt_key_tile();
-    pc.q_tile_tokens = std::max(1, (use_tc ? tc_rows_tile() : simt_rows_tile(G, D)) / G);
-    pc.n_layers = n_layers;
-    pc.num_sms = num_sms;
-    pc.ctas_per_sm = 2;   // SIMT: 2 CTAs/SM; tcgen05: 2 slots per CTA
-    pc.max_splits = (int)opt_max_splits;
-    pc.min_tiles_per_unit = use_tc ? 2 : 2;
-    pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
-    pc.split_overhead_tiles = use_tc ? kTcSplitOverheadTiles : 1.0;
-    pc.fault = (int)opt_fault;
-    pc.force_groups = opts.force_groups;
-    pc.pair_slots = use_tc;
-  }
-  // tcgen05: units with identical key tiles run as cta_group::2 CTA pairs
-  // (kernels_tc2.cu), the rest as two-slot CTAs (kernels_tc.cu).
-  std::vector<TcPair> pairs, pairs2;
-  const bool fused_req = use_tc && opt_fused_merge;
-  const bool want_pairs2 = use_tc && opt_cta_pair && !fused_req && !kv_fp8;
-  if (compute_o) {
-    // plan cache key: options + per segment (m, own keys, cached slots, R0 hole, pool class)
-    std::vector<int64_t> key = {use_tc, want_pairs2, pc.Hkv, pc.key_tile, pc.q_tile_tokens, pc.n_layers, pc.num_sms,
-                                pc.max_splits, pc.fault, pc.force_groups, (int64_t)segs.size()};
-    for (size_t i = 0; i < segs.size(); ++i) {
-      size_t cls = i;   // first segment reading the same page table
-      for (size_t j = 0; j < i; ++j)
-        if (segs[j].pages == segs[i].pages) { cls = j; break; }
-      key.insert(key.end(), {segs[i].m, segs[i].tail_m, segs[i].n_slots, segs[i].hole_lo, segs[i].hole_hi,
-                             (int64_t)cls});
-    }
-    bool hit = false;
-    for (size_t e = 0; e < plan_cache.size(); ++e)
-      if (plan_cache[e].key == key) {
-        PlanCacheEntry ent = std::move(plan_cache[e]);
-        plan_cache.erase(plan_cache.begin() + e);
-        plan = ent.plan;
-        pairs = ent.pairs;
-        pairs2 = ent.pairs2;
-        plan_cache.push_back(std::move(ent));
-        ++plan_cache_hits;
-        hit = true;
-        break;
-      }
-    if (!hit) {
-      plan_units(segs, pc, &plan);
-      if (use_tc) {
-        std::vector<char> in_pair2;
-        if (want_pairs2) pair_units_cta2(segs, plan, pc.key_tile, &pairs2, &in_pair2);
-        pair_units(segs, plan, pc.key_tile, &pairs, pairs2.empty() ? nullptr : &in_pair2);
-      }
-      if (plan_cache.size() >= 8) plan_cache.erase(plan_cache.begin());
-      plan_cache.push_back({std::move(key), plan, pairs, pairs2});
-    }
-  }
-  // ---- split groups that are exactly one SPLIT pair are merged inside that CTA
-  // (kernels_tc.cu epilogue): no partial traffic and no combine work for them
-  bool any_combine = !plan.groups.empty();
-  if (use_tc && !plan.groups.empty() && !opt_fused_merge && !opts.force_groups && opts.n_peers == 0 &&
-      !opts.o_f32 && !opts.lse_out && !getenv("SSA_NO_CTA_MERGE")) {
-    for (auto& pr : pairs) {
-      if (pr.ub < 0 || !pr.same_q) continue;
-      const int g = plan.units[pr.ua].group;
-      if (g < 0 || g != plan.units[pr.ub].group || plan.groups[g].n_splits != 2) continue;
-      pr.merge = 1;
-      plan.groups[g].n_splits = 0;
-    }
-    any_combine = false;
-    for (auto& g : plan.groups) any_combine = any_combine || g.n_splits > 0;
-  }
-  // ---- append segments for the scatter
-  std::vector<int32_t> app_idx;
-  for (int i = 0; i < (int)segs.size(); ++i)
-    if (segs[i].append_slot0 >= 0) app_idx.push_back(i);
-  std::vector<SegDesc> app_segs;
-  std::vector<int32_t> prefix(1, 0);
-  for (int i : app_idx) {
-    app_segs.push_back(segs[i]);
-    prefix.push_back(prefix.back() + segs[i].m);
-  }
-  // ---- upload descriptors through the ring (one span); a call being captured
-  // into a CUDA graph takes a persistent span of the graph arena instead
+  // sharded partial outputs (fp32 O / lse / peer push) go through the combine kernel
+  const bool special = opts.force_groups || opts.o_f32 || opts.lse_out || opts.n_peers > 0;
+  const bool cm = use_tc && !special;
   const bool cap = capturing(st);
-  if (cap && ((!app_segs.empty() && !opts.skip_scatter) || opt_timing)) {
-    ssa::set_error("CUDA-graph capture: only query-plane calls can be captured (and not with SSA_OPT_TIMING)");
+  // ---- cache key: every input of the planner and of the uploaded lists
+  std::vector<int64_t> key = {compute_o, use_tc, cm, opt_cluster, n_layers, opt_max_splits, opt_fault,
+                              opts.force_groups, (int64_t)segs.size()};
+  for (const SegDesc& sg : segs)
+    key.insert(key.end(), {sg.row0, sg.m, sg.tail_m, sg.n_slots, sg.hole_lo, sg.hole_hi, sg.append_slot0,
+                           sg.n_pages, (int64_t)(uintptr_t)sg.pages});
+  PlanCacheEntry* ent = nullptr;
+  for (size_t e = 0; e < plan_cache.size(); ++e)
+    if (plan_cache[e].key == key) {
+      ent = &plan_cache[e];
+      ent->last_use = ++plan_clock;
+      ++plan_cache_hits;
+      break;
+    }
+  PlanCacheEntry fresh;
+  if (!ent) {
+    fresh.key = std::move(key);
+    Plan& plan = fresh.plan;
+    if (compute_o) {
+      PlanConfig pc;
+      pc.Hkv = cfg.num_kv_heads;
+      pc.key_tile = use_tc ? tc_key_tile() : simt_key_tile();
+      pc.q_tile_tokens = std::max(1, (use_tc ? tc_rows_tile() : simt_rows_tile(G, D)) / G);
+      pc.n_layers = n_layers;
+      pc.num_sms = num_sms;
+      pc.ctas_per_sm = 2;   // SIMT: 2 CTAs/SM; tcgen05: 2 slots per CTA
+      pc.max_splits = (int)opt_max_splits;
+      pc.min_tiles_per_unit = 2;
+      pc.unit_overhead_tiles = use_tc ? 2.0 : 1.0;
+      pc.split_overhead_tiles = use_tc ? kTcSplitOverheadTiles : 1.0;
+      pc.fault = (int)opt_fault;
+      pc.force_groups = opts.force_groups;
+      pc.pair_slots = use_tc;
+      fresh.cm_C = 0;
+      if (cm && n_layers == 1 && opt_cluster >= 0) {
+        double best = -1.0;
+        for (int C : {1, 2, 3, 4, 5, 6, 7, 8, 16}) {
+          if (opt_cluster > 0 && C != opt_cluster) continue;
+          Plan pl;
+          std::vector<TcPair> prs;
+          const double cost = plan_cm(segs, pc, C, max_clusters(C), &pl, &prs);
+          if (cost >= 0.0 && (best < 0.0 || cost < best)) {
+            best = cost;
+            plan = std::move(pl);
+            fresh.pairs = std::move(prs);
+            fresh.cm_C = C;
+          }
+        }
+      }
+      if (fresh.cm_C == 0) {
+        plan_units(segs, pc, &plan);
+        if (use_tc) pair_units(segs, plan, pc.key_tile, &fresh.pairs);
+        if (cm) {
+          cm_regroup(&plan, fresh.pairs);
+          fresh.cm_C = 1;
+        }
+      }
+      for (auto& g : plan.groups) fresh.max_split = std::max(fresh.max_split, g.n_splits);
+    }
+    // ---- host image of the lists: segments, units, groups, scatter segments + prefix, CTA pairs
+    std::vector<SegDesc> app_segs;
+    std::vector<int32_t> prefix(1, 0);
+    for (const SegDesc& sg : segs)
+      if (sg.append_slot0 >= 0) {
+        app_segs.push_back(sg);
+        prefix.push_back(prefix.back() + sg.m);
+      }
+    fresh.n_app = (int32_t)app_segs.size();
+    fresh.app_tokens = prefix.back();
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const std::pair<const void*, size_t> parts[6] = {
+        {segs.data(), segs.size() * sizeof(SegDesc)},
+        {plan.units.data(), plan.units.size() * sizeof(WorkUnit)},
+        {plan.groups.data(), plan.groups.size() * sizeof(Group)},
+        {app_segs.data(), app_segs.size() * sizeof(SegDesc)},
+        {prefix.data(), prefix.size() * sizeof(int32_t)},
+        {fresh.pairs.data(), fresh.pairs.size() * sizeof(TcPair)}};
+    size_t total = 0;
+    for (int i = 0; i < 6; ++i) {
+      fresh.off[i] = total;
+      total += al(parts[i].second);
+    }
+    fresh.bytes = total;
+    fresh.image.resize(total);
+    for (int i = 0; i < 6; ++i)
+      if (parts[i].second) memcpy(fresh.image.data() + fresh.off[i], parts[i].first, parts[i].second);
+    // ---- device copy: the graph arena for a call being captured (the captured copy
+    // node writes it at every replay; not cached), else a cached allocation
+    if (cap) {
+      if (arena_used + total > arena_cap) {
+        ssa::set_error("CUDA-graph capture: graph arena exhausted (%zu of %zu bytes used)", arena_used, arena_cap);
+        return SSA_ERR_STATE;
+      }
+      memcpy(arena_h + arena_used, fresh.image.data(), total);
+      SSA_CUDA(this, cudaMemcpyAsync(arena_d + arena_used, arena_h + arena_used, total, cudaMemcpyHostToDevice, st));
+      fresh.dev = arena_d + arena_used;
+      arena_used += total;
+    } else {
+      const size_t off = ring.alloc(total);
+      if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
+      memcpy(ring.host(off), fresh.image.data(), total);
+      SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&fresh.dev), total, st));
+      SSA_CUDA(this, cudaMemcpyAsync(fresh.dev, ring.host(off), total, cudaMemcpyHostToDevice, st));
+      SSA_CUDA(this, ring.fence(off, off + total, st));
+      // evict the least recently used unpinned entry beyond 16 (freed in stream order)
+      int n_unpinned = 0, lru = -1;
+      for (size_t e = 0; e < plan_cache.size(); ++e)
+        if (!plan_cache[e].pinned) {
+          ++n_unpinned;
+          if (lru < 0 || plan_cache[e].last_use < plan_cache[lru].last_use) lru = (int)e;
+        }
+      if (n_unpinned >= 16 && lru >= 0) {
+        SSA_CUDA(this, cudaFreeAsync(plan_cache[lru].dev, st));
+        plan_cache.erase(plan_cache.begin() + lru);
+      }
+      fresh.last_use = ++plan_clock;
+      plan_cache.push_back(std::move(fresh));
+      ent = &plan_cache.back();
+    }
+    stats.plan_uploads += 1;
+  } else if (cap) {
+    ent->pinned = true;   // a captured graph reads this entry's device copy at every replay
+  }
+  const PlanCacheEntry& E = ent ? *ent : fresh;
+  const Plan& plan = E.plan;
+  const auto d_segs = reinterpret_cast<const SegDesc*>(E.dev + E.off[0]);
+  const auto d_units = reinterpret_cast<const WorkUnit*>(E.dev + E.off[1]);
+  const auto d_groups = reinterpret_cast<const Group*>(E.dev + E.off[2]);
+  const auto d_app = reinterpret_cast<const SegDesc*>(E.dev + E.off[3]);
+  const auto d_pre = reinterpret_cast<const int32_t*>(E.dev + E.off[4]);
+  const auto d_pairs = reinterpret_cast<const TcPair*>(E.dev + E.off[5]);
+  if (cap && opt_timing) {
+    ssa::set_error("CUDA-graph capture: not with SSA_OPT_TIMING");
     return SSA_ERR_STATE;
   }
-  const size_t b_segs = segs.size() * sizeof(SegDesc);
-  const size_t b_units = plan.units.size() * sizeof(WorkUnit);
-  const size_t b_groups = plan.groups.size() * sizeof(Group);
-  const size_t b_app = app_segs.size() * sizeof(SegDesc);
-  const size_t b_pre = prefix.size() * sizeof(int32_t);
-  const size_t b_pairs = pairs.size() * sizeof(TcPair);
-  const size_t b_pairs2 = pairs2.size() * sizeof(TcPair);
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t total = al(b_segs) + al(b_units) + al(b_groups) + al(b_app) + al(b_pre) + al(b_pairs) + al(b_pairs2);
-  size_t off = 0;
-  if (cap) {
-    if (arena_used + total > arena_cap) {
-      ssa::set_error("CUDA-graph capture: graph arena exhausted (%zu of %zu bytes used)", arena_used, arena_cap);
-      return SSA_ERR_STATE;
-    }
-    off = arena_used;
-    arena_used += total;
-  } else {
-    off = ring.alloc(total);
-    if (off == SIZE_MAX) return cuda_fail(cudaErrorMemoryAllocation, "ring.alloc(work list)", __LINE__);
-  }
-  char* const host_base = cap ? arena_h : ring.host(0);
-  char* const dev_base = cap ? arena_d : ring.dev(0);
-  size_t o = off;
-  auto put = [&](const void* src, size_t b) {
-    const size_t here = o;
-    if (b) memcpy(host_base + here, src, b);
-    o += al(b);
-    return dev_base + here;
-  };
-  auto d_segs = reinterpret_cast<const SegDesc*>(put(segs.data(), b_segs));
-  auto d_units = reinterpret_cast<const WorkUnit*>(put(plan.units.data(), b_units));
-  auto d_groups = reinterpret_cast<const Group*>(put(plan.groups.data(), b_groups));
-  auto d_app = reinterpret_cast<const SegDesc*>(put(app_segs.data(), b_app));
-  auto d_pre = reinterpret_cast<const int32_t*>(put(prefix.data(), b_pre));
-  auto d_pairs = reinterpret_cast<const TcPair*>(put(pairs.data(), b_pairs));
-  auto d_pairs2 = reinterpret_cast<const TcPair*>(put(pairs2.data(), b_pairs2));
-  if (cap)
-    SSA_CUDA(this, cudaMemcpyAsync(arena_d + off, arena_h + off, total, cudaMemcpyHostToDevice, st));
-  else
-    SSA_CUDA(this, ring.to_device(off, total, st));
 
   // ---- E4M3 KV (R-22): codes of the call's K/V, the tails' and the scatter's source
   const void* k_src = io.k.dev;
   const void* v_src = io.v.dev;
-  if (kv_fp8 && io.k.dev && (compute_o || (!app_segs.empty() && !opts.skip_scatter))) {
+  if (kv_fp8 && io.k.dev && (compute_o || (E.n_app > 0 && !opts.skip_scatter))) {
     QuantParams qp{};
     qp.n = (int64_t)(in_layer_stride ? n_layers : 1) * rows_per_layer * cfg.num_kv_heads * D;
     if ((size_t)(2 * qp.n) > kv8_cap) {
       if (cap) { ssa::set_error("CUDA-graph capture: warm up the call once before capturing (E4M3 scratch)"); return SSA_ERR_STATE; }
-      SSA_CUDA(this, cudaStreamSynchronize(st));
-      SSA_CUDA(this, cudaDeviceSynchronize());
-      if (kv8) cudaFree(kv8);
+      if (kv8) SSA_CUDA(this, cudaFreeAsync(kv8, st));
       kv8 = nullptr;
       kv8_cap = std::max((size_t)(2 * qp.n), 2 * kv8_cap);
-      SSA_CUDA(this, cudaMalloc(&kv8, kv8_cap));
+      SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&kv8), kv8_cap, st));
     }
     qp.K = io.k.dev;
     qp.V = io.v.dev;
@@ -653,6 +694,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     qp.v_scale = cfg.v_scale;
     cudaEvent_t t0 = tick(st);
     SSA_CUDA(this, launch_quant_e4m3(qp, st));
+    note_kernel(st, false);
     if (t0) timed_push(6, t0, tick(st));
     stats.kernel_launches++;
     k_src = qp.K8;
@@ -660,7 +702,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   }
 
   // ---- KA: scatter new K/V into pages
-  if (!app_segs.empty() && !opts.skip_scatter) {
+  if (E.n_app > 0 && !opts.skip_scatter) {
     ScatterParams sp{};
     sp.K = k_src;
     sp.V = v_src;
@@ -676,17 +718,20 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     sp.elem_bytes = pelem;
     sp.segs = d_app;
     sp.tok_prefix = d_pre;
-    sp.n_segs = (int32_t)app_segs.size();
-    sp.total_tokens = prefix.back();
+    sp.n_segs = E.n_app;
+    sp.total_tokens = E.app_tokens;
     cudaEvent_t t0 = tick(st);
     SSA_CUDA(this, launch_scatter(sp, n_layers, st));
     if (t0) timed_push(4, t0, tick(st));
     stats.kernel_launches++;
+    note_kernel(st, true);
   }
   // ---- attention (+ combine)
   if (compute_o && !plan.units.empty()) {
     const int rows_tile = use_tc ? tc_rows_tile() : simt_rows_tile(G, D);
-    if (!plan.groups.empty()) {
+    const bool combine = !plan.groups.empty() && E.cm_C == 0;
+    const bool partials = combine || E.max_split > 1;
+    if (partials) {
       const size_t n_po = (size_t)n_layers * plan.units.size() * rows_tile * D;
       const size_t n_pl = (size_t)n_layers * plan.units.size() * rows_tile;
       ssa_status s = ensure_scratch(n_po, n_pl, st);
@@ -719,43 +764,43 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.part_o = part_o;
     ap.part_lse = part_lse;
     ap.rows_tile = rows_tile;
-    ap.key_tile = pc.key_tile;
+    ap.key_tile = use_tc ? tc_key_tile() : simt_key_tile();
     ap.fault = (int32_t)opt_fault;
     ap.pairs = d_pairs;
-    ap.n_pairs = (int32_t)pairs.size();
-    const bool fused = use_tc && !plan.groups.empty() && opt_fused_merge && opts.n_peers == 0;
-    if (fused) {
-      const size_t need = (size_t)n_layers * plan.groups.size();
-      if (need > counters_cap) {
-        SSA_CUDA(this, cudaDeviceSynchronize());
-        if (counters) cudaFree(counters);
-        counters = nullptr;
-        counters_cap = std::max(need, counters_cap * 2);
-        SSA_CUDA(this, cudaMalloc(&counters, counters_cap * sizeof(int32_t)));
-        SSA_CUDA(this, cudaMemset(counters, 0, counters_cap * sizeof(int32_t)));
+    ap.n_pairs = (int32_t)E.pairs.size();
+    ap.cm_C = E.cm_C;
+    // pool tiles may be prefetched before griddepcontrol.wait unless the grid right
+    // before this one on the stream is one of the store's pool writers
+    ap.pool_early = (opt_pdl != 0 && !(pool_writer_last && last_kernel_stream == st)) ? 1 : 0;
+    const bool merge_in_kernel = E.cm_C > 0 && E.max_split > 1 && opt_cm_merge == 0;
+    if (merge_in_kernel) {
+      const size_t need = (size_t)n_layers * plan.groups.size() * E.cm_C;
+      if (need > tickets_cap) {
+        if (cap) { ssa::set_error("CUDA-graph capture: warm up the call once before capturing (merge tickets)"); return SSA_ERR_STATE; }
+        if (tickets) SSA_CUDA(this, cudaFreeAsync(tickets, st));
+        tickets = nullptr;
+        tickets_cap = std::max(need, tickets_cap * 2);
+        SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&tickets), tickets_cap * sizeof(int32_t), st));
+        SSA_CUDA(this, cudaMemsetAsync(tickets, 0, tickets_cap * sizeof(int32_t), st));
       }
-      ap.group_counters = counters;
-      ap.o_f32 = opts.o_f32;
-      ap.lse_out = opts.lse_out;
+      ap.cm_tickets = tickets;
     }
     cudaEvent_t t0 = tick(st);
     if (use_tc) {
-      if (!pairs2.empty()) {
-        SSA_CUDA(this, launch_attn_tc2(ap, d_pairs2, (int)pairs2.size(), n_layers, st));
-        stats.tc_pair_launches++;
-        if (!pairs.empty()) {   // the two-slot launch below is counted there
-          stats.kernel_launches++;
-          stats.tc_launches++;
-        }
+      SSA_CUDA(this, launch_attn_tc(ap, n_layers, opt_pdl != 0 && !t0, st));
+      stats.tc_launches++;
+      if (E.cm_C > 0) stats.cm_launches++;
+      if (E.cm_C > 0 && E.max_split > 1 && !merge_in_kernel) {   // groups over several clusters: merge kernel
+        SSA_CUDA(this, launch_cm_merge(ap, n_layers, opt_pdl != 0 && !t0, st));
+        stats.kernel_launches++;
       }
-      SSA_CUDA(this, launch_attn_tc(ap, n_layers, (int)opt_tc_qtiles, st));
     } else {
       SSA_CUDA(this, launch_attn_simt(ap, n_layers, cfg.dtype == SSA_BF16, st));
     }
     if (t0) timed_push(query_plane ? 1 : 0, t0, tick(st));
     stats.kernel_launches++;
-    if (use_tc) stats.tc_launches++;
-    if (!plan.groups.empty() && !fused && any_combine) {
+    note_kernel(st, false);
+    if (combine) {
       CombineParams cp{};
       cp.part_o = part_o;
       cp.part_lse = part_lse;
@@ -777,9 +822,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       cp.n_peers = opts.n_peers;
       cp.lse_off = opts.lse_off;
       cudaEvent_t t1 = tick(st);
-      int max_split = 1;
-      for (auto& g : plan.groups) max_split = std::max(max_split, g.n_splits);
-      SSA_CUDA(this, launch_combine(cp, n_layers, cfg.dtype == SSA_BF16, st, max_split));
+      SSA_CUDA(this, launch_combine(cp, n_layers, cfg.dtype == SSA_BF16, st, std::max(1, E.max_split)));
       if (t1) timed_push(query_plane ? 3 : 2, t1, tick(st));
       stats.kernel_launches++;
     }
@@ -788,16 +831,18 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     stats.rows_computed += rows;
     if (query_plane) stats.query_rows += rows;
   }
-  if (!cap) SSA_CUDA(this, ring.fence(off, off + total, st));
   last_plan_units = (int64_t)plan.units.size();
   last_plan_groups = (int64_t)plan.groups.size();
   last_used_tc = use_tc;
+  last_cm_C = E.cm_C;
+  last_max_split = E.max_split;
+  last_n_ctas = (int64_t)E.pairs.size();
   return SSA_OK;
 }
 
 bool ssa_store::tc_eligible(const std::vector<SegDesc>& segs) const {
   (void)segs;
-  if (opt_backend == 1 || !sm100) return false;
+  if (opt_backend == 1 || !sm100) return false;   // SIMT backend forced, or not an sm_100 device
   const int G = cfg.num_q_heads / cfg.num_kv_heads;
   // bf16 with head_dim 128 always runs on tcgen05: even a 1-token GQA query
   // (4 of 128 rows used) is HBM-bound there — per 128-key tile the two MMAs
@@ -814,10 +859,7 @@ extern "C" {
 int32_t ssa_abi_version(void) { return SSA_ABI_VERSION; }
 
 int32_t ssa_debug_trace(void* host, size_t bytes) {
-  const int a = ssa::tc_debug_trace(host, bytes);
-  if (a <= 0) return a;
-  const int b = ssa::tc2_debug_trace(static_cast<char*>(host) + a, bytes - (size_t)a);
-  return b < 0 ? a : a + b;
+  return ssa::tc_debug_trace(host, bytes);
 }
 
 const char* ssa_status_str(ssa_status s) {
@@ -901,6 +943,7 @@ ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
   }
   for (int64_t p = 0; p < cfg->num_pages; ++p) st->free_pages.push((int32_t)p);
   st->page_ref.assign(cfg->num_pages, 0);
+  for (auto& row : st->max_clusters_) for (int& c : row) c = -1;
   st->sessions.reserve(std::min(cfg->max_sessions, 4096));
   *out = st;
   return SSA_OK;
@@ -924,7 +967,10 @@ ssa_store::~ssa_store() {
   for (auto e : pipe_events) cudaEventDestroy(e);
   if (h2d_stream) cudaStreamDestroy(h2d_stream);
   if (d2h_stream) cudaStreamDestroy(d2h_stream);
-  if (counters) cudaFree(counters);
+  for (auto& e : plan_cache)
+    if (e.dev) cudaFree(e.dev);
+  if (tickets) cudaFree(tickets);
+  if (order_ev) cudaEventDestroy(order_ev);
   if (sample_part) cudaFree(sample_part);
   if (sample_cnt) cudaFree(sample_cnt);
   destroy_comm();
@@ -951,6 +997,16 @@ ssa_status ssa_store_stats(ssa_store_t st, ssa_stats* out, int32_t reset) {
   return SSA_OK;
 }
 
+ssa_status ssa_debug_last_plan(ssa_store_t st, int64_t out[5]) {
+  if (!st || !out) return SSA_ERR_INVALID_ARG;
+  out[0] = st->last_plan_units;
+  out[1] = st->last_plan_groups;
+  out[2] = st->last_n_ctas;
+  out[3] = st->last_cm_C;
+  out[4] = st->last_max_split;
+  return SSA_OK;
+}
+
 ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
   if (!st) return SSA_ERR_INVALID_ARG;
   switch (option) {
@@ -959,9 +1015,19 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
     case SSA_OPT_FAULT_INJECT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_fault = value; break;
     case SSA_OPT_TC_Q_TILES: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_tc_qtiles = value; break;
     case SSA_OPT_TIMING: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_timing = value; break;
-    case SSA_OPT_FUSED_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_fused_merge = value; break;
-    case SSA_OPT_CTA_PAIR: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_cta_pair = value; break;
-    case SSA_OPT_GRAPH_ARENA_RESET: if (value != 1) return SSA_ERR_INVALID_ARG; st->arena_used = 0; break;
+    case SSA_OPT_GRAPH_ARENA_RESET:
+      if (value != 1) return SSA_ERR_INVALID_ARG;
+      st->arena_used = 0;
+      for (auto& e : st->plan_cache) e.pinned = false;   // old graphs are dropped
+      break;
+    case SSA_OPT_CLUSTER:
+      if (value < -1 || value > 16 || (value > 8 && value != 16)) return SSA_ERR_INVALID_ARG;
+      st->opt_cluster = value;
+      break;
+    case SSA_OPT_PDL: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_pdl = value; break;
+    case SSA_OPT_CM_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
+    case SSA_OPT_PIPE_CHUNKS: if (value < -1 || value > 64) return SSA_ERR_INVALID_ARG; st->opt_pipe_chunks = value; break;
+    case SSA_OPT_QKV_DEBUG: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_qkv_debug = value; break;
     default: return SSA_ERR_INVALID_ARG;
   }
   return SSA_OK;
@@ -1035,6 +1101,7 @@ ssa_status ssa_session_create(ssa_store_t st, int32_t n_prefix, const void* Q, c
   }
   SSA_NO_CAPTURE(stream);
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   int live = 0;
   int32_t id = -1;
   for (int i = 0; i < (int)st->sessions.size(); ++i) {
@@ -1078,6 +1145,7 @@ ssa_status ssa_session_append(ssa_store_t st, ssa_session_t id, int32_t n_new, c
   if (n_new <= 0 || !K || !V || (O && !Q)) { set_error("append: invalid arguments"); return SSA_ERR_INVALID_ARG; }
   if (s->ticket_open) { set_error("append: a per-layer append is open"); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   ssa_status rc = do_append(st, *s, n_new, Q, K, V, O, (cudaStream_t)stream);
   if (rc == SSA_OK && new_version) *new_version = s->version;
   return rc;
@@ -1091,6 +1159,7 @@ ssa_status ssa_append_begin(ssa_store_t st, ssa_session_t id, int32_t n_new, int
   if (n_new <= 0 || !ticket) return SSA_ERR_INVALID_ARG;
   if (s->ticket_open) { set_error("append_begin: ticket already open"); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, nullptr);
   std::vector<int32_t> got;
   ssa_status rc = st->evict_for_append(*s, n_new, nullptr);
   if (rc != SSA_OK) return rc;
@@ -1119,10 +1188,10 @@ ssa_status ssa_append_layer(ssa_store_t st, ssa_session_t id, int32_t ticket, in
   ssa_status rc = SSA_OK;
   Session* s = check_ticket(st, id, ticket, &rc);
   if (!s) return rc;
-  SSA_NO_CAPTURE(stream);
   if (layer < 0 || layer >= st->cfg.num_layers || !K || !V || (O && !Q)) return SSA_ERR_INVALID_ARG;
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   const int32_t n_new = s->ticket_n_new;
   IoSet io;
   io.q = {O ? Q : nullptr, tensor_bytes(st, 1, n_new, st->cfg.num_q_heads)};
@@ -1208,6 +1277,7 @@ ssa_status ssa_session_evict_oldest(ssa_store_t st, ssa_session_t id, int64_t n,
     return SSA_ERR_INVALID_ARG;
   }
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   ssa_status rc = st->evict(*s, n, (cudaStream_t)stream);
   if (rc == SSA_OK && new_version) *new_version = s->version;
   return rc;
@@ -1235,6 +1305,7 @@ ssa_status ssa_session_alias_prefix(ssa_store_t st, ssa_session_t donor_id, int6
   }
   if (d->ticket_open) return SSA_ERR_STATE;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   const int64_t P = st->cfg.page_size;
   const int64_t end_slot = st->slots_for(*d, len);
   const int64_t full = end_slot / P;                 // pages shared whole
@@ -1330,6 +1401,7 @@ ssa_status ssa_flash_query_batch(ssa_store_t st, ssa_session_t id, int32_t layer
   }
   if (total >= (1LL << 31)) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;
   IoSet io;
   io.q = {Q, tensor_bytes(st, Lin, total, st->cfg.num_q_heads)};
@@ -1338,9 +1410,8 @@ ssa_status ssa_flash_query_batch(ssa_store_t st, ssa_session_t id, int32_t layer
   io.o = {O, tensor_bytes(st, Lin, total, st->cfg.num_q_heads)};
   cudaStream_t cs = (cudaStream_t)stream;
   // host buffers with all layers: chunked copies overlapped with the kernels
-  const char* pe = getenv("SSA_PIPE_CHUNKS");
-  const bool pipelined = layer < 0 && Lin >= 4 && !(pe && atoi(pe) == 0) && !capturing(stream) &&
-                         (getenv("SSA_PIPE_FORCE") || !is_device_ptr(Q) || !is_device_ptr(K) || !is_device_ptr(V) || !is_device_ptr(O));
+  const bool pipelined = layer < 0 && Lin >= 4 && st->opt_pipe_chunks >= 0 && !capturing(stream) &&
+                         (!is_device_ptr(Q) || !is_device_ptr(K) || !is_device_ptr(V) || !is_device_ptr(O));
   ssa_status rc = pipelined ? SSA_OK : st->stage_inputs(&io, cs);
   if (rc != SSA_OK) return rc;
   std::vector<SegDesc> segs;
@@ -1397,6 +1468,7 @@ ssa_status ssa_batch_run(ssa_store_t st, int32_t layer, int32_t n_items, const s
   }
   if (n_rows >= (1LL << 31)) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   cudaStream_t cs = (cudaStream_t)stream;
   // Reserve pages for every APPEND item, in item order, all-or-none (R-7).
   ssa_status rc = SSA_OK;
@@ -1572,6 +1644,7 @@ ssa_status ssa_session_load_kv(ssa_store_t st, ssa_session_t id, int64_t count, 
   if (count <= 0 || count >= (1LL << 31) || !K || !V) return SSA_ERR_INVALID_ARG;
   if (s->ticket_open) return SSA_ERR_STATE;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   return do_append(st, *s, (int32_t)count, nullptr, K, V, nullptr, (cudaStream_t)stream);
 }
 
@@ -1586,25 +1659,28 @@ ssa_status ssa_greedy_sample(ssa_store_t st, ssa_dtype dtype, int32_t n_rows, in
     return SSA_ERR_INVALID_ARG;
   }
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   cudaStream_t cs = (cudaStream_t)stream;
   // about four CTAs per SM over all rows, at least 4096 logits per CTA
   int splits = std::max(1, (4 * st->num_sms + n_rows - 1) / n_rows);
   splits = std::min(splits, std::max(1, vocab / 4096));
   const size_t part = (size_t)n_rows * splits * sample_partial_bytes();
-  if (part > st->sample_part_cap) {
-    SSA_CUDA(st, cudaDeviceSynchronize());
-    if (st->sample_part) cudaFree(st->sample_part);
+  if ((part > st->sample_part_cap || (size_t)n_rows + 1 > st->sample_cnt_cap) && capturing(stream)) {
+    set_error("CUDA-graph capture: warm up the call once before capturing (sampling scratch)");
+    return SSA_ERR_STATE;
+  }
+  if (part > st->sample_part_cap) {   // stream-ordered growth (enter() ordered earlier calls)
+    if (st->sample_part) SSA_CUDA(st, cudaFreeAsync(st->sample_part, cs));
     st->sample_part = nullptr;
     st->sample_part_cap = std::max(part, 2 * st->sample_part_cap);
-    SSA_CUDA(st, cudaMalloc(&st->sample_part, st->sample_part_cap));
+    SSA_CUDA(st, cudaMallocAsync(&st->sample_part, st->sample_part_cap, cs));
   }
   if ((size_t)n_rows + 1 > st->sample_cnt_cap) {
-    SSA_CUDA(st, cudaDeviceSynchronize());
-    if (st->sample_cnt) cudaFree(st->sample_cnt);
+    if (st->sample_cnt) SSA_CUDA(st, cudaFreeAsync(st->sample_cnt, cs));
     st->sample_cnt = nullptr;
     st->sample_cnt_cap = std::max<size_t>(n_rows + 1, 2 * st->sample_cnt_cap);
-    SSA_CUDA(st, cudaMalloc(&st->sample_cnt, st->sample_cnt_cap * sizeof(int32_t)));
-    SSA_CUDA(st, cudaMemset(st->sample_cnt, 0, st->sample_cnt_cap * sizeof(int32_t)));
+    SSA_CUDA(st, cudaMallocAsync(reinterpret_cast<void**>(&st->sample_cnt), st->sample_cnt_cap * sizeof(int32_t), cs));
+    SSA_CUDA(st, cudaMemsetAsync(st->sample_cnt, 0, st->sample_cnt_cap * sizeof(int32_t), cs));
   }
   SampleParams sp{};
   sp.logits = logits;
@@ -1746,12 +1822,13 @@ static ssa_status qkv_launch(ssa_store* st, int32_t n, int32_t hidden, int64_t p
     qp.v_scale = st->cfg.v_scale;
   }
   qp.splits = qkv_choose_splits(n, qp.Hq + 2 * qp.Hkv, hidden, st->num_sms);
-  if (const char* e = getenv("SSA_QKV_DEBUG")) qp.debug = atoi(e);
+  qp.debug = (int32_t)st->opt_qkv_debug;
   qp.trace = g_qkv_trace;
   cudaEvent_t t0 = st->tick(cs);
   SSA_CUDA(st, launch_qkv_rope(qp, cs));
   if (t0) st->timed_push(5, t0, st->tick(cs));
   st->stats.kernel_launches++;
+  st->note_kernel(cs, qp.poolK != nullptr);   // K/V written straight into pages
   return SSA_OK;
 }
 
@@ -1760,19 +1837,23 @@ ssa_status ssa_qkv_rope(ssa_store_t st, int32_t n, int32_t hidden, int64_t pos0,
   SSA_CHECK_STORE(st);
   if (!qkv_args_ok(st, n, hidden, X, W, stream) || !Q || !K || !V || pos0 < 0) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   return qkv_launch(st, n, hidden, pos0, rope_theta, X, W, Q, K, V, nullptr, 0, 0, (cudaStream_t)stream);
 }
 
-static ssa_status qkv_scratch(ssa_store* st, int64_t n, void** q, void** k, void** v) {
+static ssa_status qkv_scratch(ssa_store* st, int64_t n, void** q, void** k, void** v, cudaStream_t cs) {
   const size_t eq = (size_t)n * st->cfg.num_q_heads * st->cfg.head_dim * 2;
   const size_t ek = (size_t)n * st->cfg.num_kv_heads * st->cfg.head_dim * 2;
   const size_t need = eq + 2 * ek;
   if (need > st->qkv_scratch_cap) {
-    SSA_CUDA(st, cudaDeviceSynchronize());
-    if (st->qkv_scratch) cudaFree(st->qkv_scratch);
+    if (capturing(cs)) {
+      set_error("CUDA-graph capture: warm up the call once before capturing (projection scratch)");
+      return SSA_ERR_STATE;
+    }
+    if (st->qkv_scratch) SSA_CUDA(st, cudaFreeAsync(st->qkv_scratch, cs));
     st->qkv_scratch = nullptr;
     st->qkv_scratch_cap = std::max(need, 2 * st->qkv_scratch_cap);
-    SSA_CUDA(st, cudaMalloc(&st->qkv_scratch, st->qkv_scratch_cap));
+    SSA_CUDA(st, cudaMallocAsync(&st->qkv_scratch, st->qkv_scratch_cap, cs));
   }
   *q = st->qkv_scratch;
   *k = static_cast<uint8_t*>(st->qkv_scratch) + eq;
@@ -1791,9 +1872,10 @@ ssa_status ssa_append_layer_fused(ssa_store_t st, ssa_session_t id, int32_t tick
   if (!qkv_args_ok(st, s->ticket_n_new, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
   if (s->ticket_done[layer]) { set_error("layer %d already appended", layer); return SSA_ERR_STATE; }
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   const int32_t n_new = s->ticket_n_new;
   void *q, *k, *v;
-  if ((rc = qkv_scratch(st, n_new, &q, &k, &v)) != SSA_OK) return rc;
+  if ((rc = qkv_scratch(st, n_new, &q, &k, &v, (cudaStream_t)stream)) != SSA_OK) return rc;
   cudaStream_t cs = (cudaStream_t)stream;
   const int64_t slot0 = st->slot_of(*s, s->n_tokens);
   // positions never re-based (R-8): the next token's position counts evicted tokens
@@ -1826,8 +1908,9 @@ ssa_status ssa_session_query_fused(ssa_store_t st, ssa_session_t id, int32_t lay
   if (layer < 0 || layer >= st->cfg.num_layers || !dev_ok(O, stream)) return SSA_ERR_INVALID_ARG;
   if (!qkv_args_ok(st, n_q, hidden, X, W, stream)) return SSA_ERR_INVALID_ARG;
   cudaSetDevice(st->cfg.device);
+  SSA_ORDERED(st, stream);
   void *q, *k, *v;
-  ssa_status rc = qkv_scratch(st, n_q, &q, &k, &v);
+  ssa_status rc = qkv_scratch(st, n_q, &q, &k, &v, (cudaStream_t)stream);
   if (rc != SSA_OK) return rc;
   cudaStream_t cs = (cudaStream_t)stream;
   const int64_t pos0 = s->n_tokens + s->n_evicted;   // query tokens follow the cache (R-8)
@@ -1836,6 +1919,7 @@ ssa_status ssa_session_query_fused(ssa_store_t st, ssa_session_t id, int32_t lay
 }
 
 int32_t ssa_debug_qkv_clusters(int32_t splits) { return qkv_max_active_clusters(splits); }
+int32_t ssa_debug_tc_clusters(int32_t size, int32_t e4m3) { return tc_max_active_clusters(size, e4m3 != 0); }
 
 /* experiments: per-CTA %globaltimer stamps of the next fused-projection launches */
 int32_t ssa_debug_qkv_trace(void* device_buf) {

@@ -68,19 +68,25 @@ struct RunOpts {
 // tcgen05 path (kernels_tc.cu)
 int tc_key_tile();
 int tc_debug_trace(void* host, size_t bytes);
-int tc2_debug_trace(void* host, size_t bytes);
 int tc_rows_tile();
-cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, int q_tiles_opt, cudaStream_t s);
+cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s);
+size_t tc_smem_bytes();
+cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s);
+cudaError_t tc_configure(bool f8);
+int tc_max_active_clusters(int c, bool f8);
 bool tc_supported_shape(int D, int G, bool bf16);
 // bf16 tensor map, 128-byte swizzle (kernels_tc.cu); false if the driver entry point is missing.
 bool encode_bf16_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
                      const cuuint64_t* strides_bytes, const cuuint32_t* box);
-// cta_group::2 path (kernels_tc2.cu): CTA pairs sharing each K/V tile, S double-buffered.
-cudaError_t launch_attn_tc2(const AttnParams& p, const TcPair* d_pairs2, int n_pairs2, int n_layers, cudaStream_t s);
 
 }  // namespace ssa
 
 struct CommState;
+
+// Public calls that enqueue device work are ordered after the store's previous call.
+#define SSA_ORDERED(st, stream)                     \
+  ssa_store::Ordered ssa_ordered_((st), (stream)); \
+  if (!ssa_ordered_.ok) return SSA_ERR_CUDA
 
 struct ssa_store {
   ssa_store_config cfg{};
@@ -104,13 +110,28 @@ struct ssa_store {
   // Plans of recent calls (planner + CTA pairing are pure functions of the segment
   // shapes and options): per-layer calls of one step, repeated queries between
   // appends and Flash Query cycles skip the LPT search.
+  // Each entry keeps the device copy of its work lists (segments, units, groups,
+  // scatter segments, CTA pairs), so a repeated call shape launches without an
+  // upload.  Entries read by a captured CUDA graph are pinned (never evicted).
   struct PlanCacheEntry {
     std::vector<int64_t> key;
     ssa::Plan plan;
-    std::vector<ssa::TcPair> pairs, pairs2;
+    std::vector<ssa::TcPair> pairs;
+    int32_t cm_C = 0;          // cluster-merge launch (AttnParams::cm_C), 0 = combine kernel / SIMT
+    int32_t max_split = 0;     // largest Group::n_splits
+    int32_t n_app = 0;         // scatter segments
+    int32_t app_tokens = 0;
+    std::vector<char> image;   // host copy of the lists
+    size_t off[6] = {};
+    size_t bytes = 0;
+    char* dev = nullptr;
+    bool pinned = false;
+    int64_t last_use = 0;
   };
-  std::vector<PlanCacheEntry> plan_cache;   // most recent last, at most 8
-  int64_t plan_cache_hits = 0;
+  std::vector<PlanCacheEntry> plan_cache;   // at most 16 unpinned entries
+  int64_t plan_cache_hits = 0, plan_clock = 0;
+  int max_clusters_[2][17];   // [E4M3][C]: co-resident clusters of C CTAs (-1 = not queried)
+  int max_clusters(int C);
   // CUDA-graph capture (query plane): work lists of captured calls live in this
   // arena (pinned host + device, bump-allocated, never recycled while the store
   // lives) so the captured H2D copy node reads the same bytes at every replay.
@@ -128,20 +149,47 @@ struct ssa_store {
   void* qkv_scratch = nullptr;   // fused projection: dense Q/K/V of the current call
   size_t qkv_scratch_cap = 0;
   size_t stage_cap = 0;
-  int32_t* counters = nullptr;   // fused-merge group counters (zero between launches)
   void* sample_part = nullptr;   // greedy sampling: per-(row, split) partials
   size_t sample_part_cap = 0;
   int32_t* sample_cnt = nullptr; // per-row tickets (zero between launches)
   size_t sample_cnt_cap = 0;
-  size_t counters_cap = 0;
-  int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0, opt_fused_merge = 0;
-#ifndef SSA_CTA_PAIR_DEFAULT
-#define SSA_CTA_PAIR_DEFAULT 0
-#endif
-  int64_t opt_cta_pair = SSA_CTA_PAIR_DEFAULT;   // SSA_OPT_CTA_PAIR
+  int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0;
+  int64_t opt_cluster = 0;       // SSA_OPT_CLUSTER
+  int64_t opt_pdl = 1;           // SSA_OPT_PDL
+  int64_t opt_cm_merge = 1;      // SSA_OPT_CM_MERGE
+  int32_t* tickets = nullptr;    // CM merge tickets (zero between launches)
+  size_t tickets_cap = 0;
+  int64_t opt_pipe_chunks = 0;   // SSA_OPT_PIPE_CHUNKS
+  int64_t opt_qkv_debug = 0;     // SSA_OPT_QKV_DEBUG
+  // Cross-stream ordering: the device work of a call waits for the previous
+  // call's work when it runs on another stream (event recorded at each call's
+  // end), so pages, scratch, staging and work lists are reused in call order.
+  // The store's last kernel launch: its stream and whether it wrote the KV pool
+  // (scatter, fused projection into pages) -- a programmatic launch right behind
+  // such a grid must not read the pool before griddepcontrol.wait.
+  cudaStream_t last_kernel_stream = nullptr;
+  bool pool_writer_last = false;
+  void note_kernel(cudaStream_t st, bool writes_pool) {
+    last_kernel_stream = st;
+    pool_writer_last = writes_pool;
+  }
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t order_stream = nullptr;
+  bool order_valid = false;
+  ssa_status enter(cudaStream_t st);
+  void leave(cudaStream_t st);
+  // enter() / leave() around a public call that enqueues device work
+  struct Ordered {
+    ssa_store* st;
+    cudaStream_t s;
+    bool ok;
+    Ordered(ssa_store* st_, void* s_) : st(st_), s(static_cast<cudaStream_t>(s_)) { ok = st->enter(s) == SSA_OK; }
+    ~Ordered() { st->leave(s); }
+  };
   ssa_stats stats{};
   int32_t ticket_seq = 0;
-  int64_t last_plan_units = 0, last_plan_groups = 0;
+  int64_t last_plan_units = 0, last_plan_groups = 0, last_n_ctas = 0;
+  int32_t last_cm_C = 0, last_max_split = 0;
   bool last_used_tc = false;
   CommState* comm = nullptr;
   // SSA_OPT_TIMING
