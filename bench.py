@@ -147,25 +147,127 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_query_sample(n=CFG["n_ctx"], kv_heads=1, q_len=CFG["q_len"]):
-    """The fp64 oracle on a bounded sample of the workload: one layer, `kv_heads` KV
-    heads (and their 4 q heads each), a 32-token query over n cached tokens.
-    Returns (seconds, algorithmic bytes of the sample)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_inputs(layers, n=CFG["n_ctx"], q_len=CFG["q_len"], seed=2, m_append=0):
+    """The bench session's inputs for `layers` (market stream, seed as the GPU arm): cached K/V
+    of tokens [0, n), and either the 32-token query (domain 1) or, with m_append > 0, the
+    append of tokens [n, n + m_append) (domain 0) -- bf16 bit patterns (uint16).  Generated
+    with the torch implementation of streams.py on the GPU when there is one (bit-identical to
+    the numpy one, tests/test_streams.py), else with numpy."""
     import numpy as np
-    import oracle
     import streams
-    spec = streams.StreamSpec("market", seed=2)
-    hq_s = kv_heads * (CFG["hq"] // CFG["hkv"])
-    K = streams.gen_tensor_np(spec, 0, 0, 0, streams.TENSOR_K, 0, n, kv_heads, CFG["d"])
-    V = streams.gen_tensor_np(spec, 0, 0, 0, streams.TENSOR_V, 0, n, kv_heads, CFG["d"])
-    Q = streams.gen_tensor_np(spec, 0, 1, 0, streams.TENSOR_Q, 0, q_len, hq_s, CFG["d"])
-    Kq = streams.gen_tensor_np(spec, 0, 1, 0, streams.TENSOR_K, 0, q_len, kv_heads, CFG["d"])
-    Vq = streams.gen_tensor_np(spec, 0, 1, 0, streams.TENSOR_V, 0, q_len, kv_heads, CFG["d"])
+    spec = streams.StreamSpec("market", seed=seed)
+    dom, tok0, m = (0, n, m_append) if m_append else (1, 0, q_len)
+    try:
+        import torch
+        use_torch = torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        use_torch = False
+
+    def gen(domain, layer, tensor, t0, cnt, heads):
+        if use_torch:
+            x = streams.gen_tensor_torch(spec, 0, domain, layer, tensor, t0, cnt, heads, CFG["d"], hkv=CFG["hkv"],
+                                         device="cuda")
+            return x.view(torch.int16).cpu().numpy().view(np.uint16)
+        return streams.gen_tensor_np(spec, 0, domain, layer, tensor, t0, cnt, heads, CFG["d"], hkv=CFG["hkv"])
+    out = []
+    for l in layers:
+        out.append(dict(K=gen(0, l, streams.TENSOR_K, 0, n, CFG["hkv"]), V=gen(0, l, streams.TENSOR_V, 0, n, CFG["hkv"]),
+                        Q=gen(dom, l, streams.TENSOR_Q, tok0, m, CFG["hq"]), Kn=gen(dom, l, streams.TENSOR_K, tok0, m, CFG["hkv"]),
+                        Vn=gen(dom, l, streams.TENSOR_V, tok0, m, CFG["hkv"])))
+    return out
+
+
+def oracle_layers(inputs, workers, heads=None):
+    """The fp64 oracle (oracle.attention_rows, Eq. attention P:145 on the rows of Eq.
+    query-attention P:150-155) over every (layer, KV head) of `inputs`, the tasks spread over
+    `workers` host threads (the C oracle runs with the GIL released).  Returns
+    (seconds, outputs [layer][m][Hq][d] fp64)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    import oracle
+    g = CFG["hq"] // CFG["hkv"]
+    scale = oracle.default_scale(CFG["d"])
+    outs = [np.zeros(x["Q"].shape, dtype=np.float64) for x in inputs]
+
+    def task(li, h):
+        x = inputs[li]
+        n = x["K"].shape[0]
+        m = x["Q"].shape[0]
+        keys = oracle.to_f64(np.concatenate([x["K"][:, h], x["Kn"][:, h]], axis=0))
+        vals = oracle.to_f64(np.concatenate([x["V"][:, h], x["Vn"][:, h]], axis=0))
+        nvis = np.arange(n + 1, n + m + 1, dtype=np.int64)     # causal over the new tokens (R-2)
+        for qh in range(h * g, (h + 1) * g):
+            o, _ = oracle.attention_rows(oracle.to_f64(x["Q"][:, qh]), keys, vals, nvis, scale)
+            outs[li][:, qh] = o
+    oracle.build()
     t0 = time.perf_counter()
-    oracle.segment_rows(K, V, Q, Kq, Vq, kv_heads, oracle.default_scale(CFG["d"]))
-    dt = time.perf_counter() - t0
-    nbytes = query_bytes_per_layer(n, q_len, hq_s, kv_heads, CFG["d"])
-    return dt, nbytes
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        futs = [ex.submit(task, li, h) for li in range(len(inputs))
+                for h in (range(CFG["hkv"]) if heads is None else heads)]
+        for f in futs:
+            f.result()
+    return time.perf_counter() - t0, outs
+
+
+def cpu_baseline_leg(gpu_out=None):
+    """SURVEY §8(d) "oracle timing": the fp64 oracle on the GPU box's host cores -- the whole
+    32-layer 32-token query at n = 32,768 (all cores), one 256-token append layer at
+    n = 32,512 (all cores) and one (layer, KV head) task single-threaded; plus, when the GPU
+    output of the headline query is given, its parity against these oracle rows (layers 0 and
+    31 in full) with the derived per-element bound (tests/helpers.attention_bound)."""
+    import numpy as np
+    cores = os.cpu_count() or 1
+    q_in = oracle_inputs(range(CFG["L"]))
+    t_q, o_q = oracle_layers(q_in, cores)
+    nb = query_bytes_per_layer(CFG["n_ctx"], CFG["q_len"], CFG["hq"], CFG["hkv"], CFG["d"]) * CFG["L"]
+    fl_q = 4 * CFG["hq"] * CFG["d"] * CFG["q_len"] * CFG["n_ctx"] * CFG["L"]
+    t1, _ = oracle_layers(q_in[:1], 1, heads=[0])
+    n0 = CFG["n_ctx"] - CFG["m_append"]
+    a_rows = 64    # bounded: the first 64 of the append's 256 rows of one layer (cost ~ rows, each sees ~n keys)
+    a_in = oracle_inputs([0], n=n0, m_append=a_rows)
+    t_a = oracle_layers(a_in, cores)[0] * CFG["m_append"] / a_rows
+    out = {"value": nb / t_q / 1e9, "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+           "sample": "fp64 C oracle (oracle.attention_rows) over (layer, KV head) tasks on all host threads: the "
+                     "whole 32-layer 32-token query at n=32,768 (the headline query), "
+                     f"{t_q:.2f} s",
+           "query_32_layers_s": t_q, "query_gflops": fl_q / t_q / 1e9,
+           "append_one_layer_s": t_a,
+           "append_sample": f"rows 0..{a_rows - 1} of the 256-token append at n=32,512 (layer 0, all heads), "
+                            f"scaled by 256/{a_rows}",
+           "append_one_layer_tok_s": CFG["m_append"] / t_a,
+           "append_32_layers_s_extrapolated": t_a * CFG["L"],
+           "single_thread_one_layer_kv_head_s": t1,
+           "single_thread_query_32_layers_s_extrapolated": t1 * CFG["hkv"] * CFG["L"]}
+    if gpu_out is not None:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle
+        from helpers import attention_bound
+        errs, ratios = [], []
+        for li in (0, CFG["L"] - 1):
+            x = q_in[li]
+            want = o_q[li]
+            got = oracle.to_f64(gpu_out[li])
+            xa = dict(x, V=x["V"] & np.uint16(0x7FFF), Vn=x["Vn"] & np.uint16(0x7FFF))   # |V| (bf16 sign bit)
+            _, (A,) = oracle_layers([xa], cores)
+            bound = attention_bound(A, want, x["K"].shape[0] + x["Q"].shape[0])
+            e = np.abs(got - want)
+            errs.append(e)
+            ratios.append(float((e / bound).max()))
+        e = np.concatenate([x.ravel() for x in errs])
+        out["parity_sample"] = {"rows": "headline query output, layers 0 and 31, all 32 tokens x 32 heads",
+                                "max_abs": float(e.max()), "mean_abs": float(e.mean()),
+                                "tolerance": [2e-2, 2e-3], "max_err_over_derived_bound": max(ratios)}
+    return out
 
 
 def arm_config():
@@ -177,25 +279,31 @@ def arm_config():
 
 
 def run_reference(args):
+    """This tier's reference arm: the fp64 oracle as it stands, on all host cores, timed on a
+    bounded sample of the workload per step (4 of the 32 layers of the 32-token query at
+    n = 32,768); value = algorithmic query-plane GB/s of the sample."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import oracle
-    oracle.build()
+    cores = os.cpu_count() or 1
+    layers = list(range(4))
+    inp = oracle_inputs(layers)
     for _ in range(args.warmup):
-        oracle_query_sample(n=4096)
-    times, nbytes = [], 0
+        oracle_layers(inp[:1], cores)
+    times = []
     for _ in range(args.steps):
-        dt, nbytes = oracle_query_sample()
+        dt, _ = oracle_layers(inp, cores)
         times.append(dt)
+    nbytes = query_bytes_per_layer(CFG["n_ctx"], CFG["q_len"], CFG["hq"], CFG["hkv"], CFG["d"]) * len(layers)
     v = nbytes / statistics.mean(times) / 1e9
     line = {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (streams.py market stream)",
             "config": arm_config(),
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": "fp64 C oracle: one layer, one KV head (4 q heads), 32-token query over 32,768 cached tokens, per step"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+                             "sample": "fp64 C oracle on all host threads: 4 of the 32 layers of the 32-token query "
+                                       "over 32,768 cached tokens, per step"},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -236,6 +344,12 @@ def extend_session(st, sid, torch, dev, spec, n_from, n_to, chunk=4096, session=
                                                   CFG["d"], device=dev) for l in range(CFG["L"])])
         st.load_kv(sid, K, V)
         tok += m
+
+
+def from_bf16(torch, t):
+    """A device bf16 tensor as numpy bf16 bit patterns (uint16)."""
+    import numpy as np
+    return t.detach().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
 def gen_new(torch, dev, spec, domain, tok0, m, session=0):
@@ -324,28 +438,76 @@ def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Q
     return out
 
 
-def leg_graph(st, sid, torch, stream, Qq, Kq, Vq, steps, warmup):
-    """SURVEY §8(d) "query latency per layer and for 32 layers (CUDA graph)": the 32-token query
-    as 32 single-layer calls (the form a real model issues, one per layer), eager and captured
-    into one CUDA graph (work lists in the store's graph arena), vs the one all-layer call."""
-    L = CFG["L"]
-    O = torch.empty_like(Qq)
+def leg_per_layer(st, sid, torch, dev, spec, stream, peaks, steps, n0, Qa, Ka, Va, Qq, Kq, Vq):
+    """SURVEY §8(d) config [1] "per layer ... (CUDA graph)": the forms a model issues (Alg. 1
+    L282 / Alg. 2 L295 run Forward layer by layer, so layer l+1's Q needs layer l's O).
+    query_per_layer_graph: the 32-token (and 1-token) query as 32 single-layer calls captured in
+    one CUDA graph; append_per_layer_graph: the 256-token append as append_begin + 32
+    append_layer calls captured in one graph (scatter + attention per layer) + commit.  Device
+    time of the graph replay (CUDA events on the stream)."""
+    L, hq, hkv, d = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"]
+    m_app = CFG["m_append"]
+    out = {}
+    Oa = torch.empty_like(Qa)
+    cs = torch.cuda.Stream()   # graphs are captured on a side stream, replayed on `stream`
+    st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # n -> 32,768 as in the headline query
+    n = n0 + m_app
+    for qn in (CFG["q_len"], 1):
+        q, k, v = (x[:, :qn].contiguous() for x in (Qq, Kq, Vq))
+        o = torch.empty_like(q)
 
-    def per_layer(s):
-        for l in range(L):
-            st.session_query(sid, Qq[l:l + 1], Kq[l:l + 1], Vq[l:l + 1], O[l:l + 1], layer=l, stream=s)
-    per_layer(stream)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        per_layer(torch.cuda.current_stream())
-    ms_graph = _timed(torch, stream, g.replay, steps, warmup)
-    ms_eager = _timed(torch, stream, lambda: per_layer(stream), steps, warmup)
-    ms_all = _timed(torch, stream, lambda: st.session_query(sid, Qq, Kq, Vq, O, stream=stream), steps, warmup)
-    return {"workload": "BJ.configs[1] 32-token query at n=32,768 as 32 per-layer calls",
-            "graph_ms_32_layers": ms_graph, "graph_us_per_layer": ms_graph * 1e3 / L,
-            "eager_ms_32_layers": ms_eager, "all_layer_call_ms": ms_all,
-            "note": "stream-timed (CUDA events around the replay / the calls), host gaps included"}
+        def per_layer(s):
+            for l in range(L):
+                st.session_query(sid, q[l:l + 1], k[l:l + 1], v[l:l + 1], o[l:l + 1], layer=l, stream=s)
+        per_layer(stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs):
+            per_layer(cs)
+        ms = _timed(torch, stream, g.replay, steps, 3)
+        plan = st.last_plan()
+        b = query_bytes_per_layer(n, qn, hq, hkv, d)
+        out[f"query_per_layer_graph_q{qn}"] = {
+            "us_per_layer": ms * 1e3 / L, "ms_32_layers": ms, "gbs": b * L / (ms * 1e-3) / 1e9,
+            "hbm_frac": b * L / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "plan": {"ctas": plan["ctas"], "cluster": plan["cm_C"], "clusters_per_group": plan["max_split"]}}
+        ms_all = _timed(torch, stream, lambda: st.session_query(sid, q, k, v, o, stream=stream), steps, 3)
+        out[f"query_per_layer_graph_q{qn}"]["all_layer_call_us_per_layer"] = ms_all * 1e3 / L
+    st.session_truncate(sid, n0)
+    # per-layer append: begin (host), 32 append_layer calls captured in one graph, commit
+    fl = append_flops_per_layer(n0, m_app, hq, d)
+    times = []
+    for r in range(steps + 2):
+        t = st.append_begin(sid, m_app)
+        if r == 0:    # eager warm-up: caches the work lists the captures reuse
+            for l in range(L):
+                st.append_layer(sid, t, l, Qa[l:l + 1], Ka[l:l + 1], Va[l:l + 1], Oa[l:l + 1], stream=stream)
+        else:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs):
+                for l in range(L):
+                    st.append_layer(sid, t, l, Qa[l:l + 1], Ka[l:l + 1], Va[l:l + 1], Oa[l:l + 1], stream=cs)
+        st.append_commit(sid, t)
+        if r > 0:
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            e1.synchronize()
+            if r >= 2:
+                times.append(e0.elapsed_time(e1))
+        st.session_truncate(sid, n0)
+    ms = statistics.mean(times)
+    plan = st.last_plan()
+    out["append_per_layer_graph"] = {
+        "us_per_layer": ms * 1e3 / L, "ms_32_layers": ms, "tflops": fl * L / (ms * 1e-3) / 1e12,
+        "tc_frac": fl * L / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"], "tok_per_s": m_app / (ms * 1e-3),
+        "plan": {"ctas": plan["ctas"], "cluster": plan["cm_C"], "clusters_per_group": plan["max_split"]},
+        "what": "scatter + attention per layer (graph of 64 kernels), FLOPs of the attention only"}
+    out["workload"] = "BJ.configs[1] session (n=32,768 for queries, 32,512 -> 32,768 for the append)"
+    out["note"] = "device time of the CUDA-graph replay (events on the stream), includes launch gaps"
+    return out
 
 
 def leg_multitenant(torch, dev, stream, peaks, steps, warmup):
@@ -772,6 +934,13 @@ def run_ours(args):
     h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV))
     d2h = hO.numel() * hO.element_size()
 
+    gpu_query_out = None
+    if rank == 0 and not args.no_cpu_baseline:   # the headline query's output at n = 32,768 for the parity sample
+        st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)
+        st.session_query(sid, Qq, Kq, Vq, Oq, stream=stream)
+        torch.cuda.synchronize()
+        gpu_query_out = from_bf16(torch, Oq)
+        st.session_truncate(sid, n0)
     legs = {}
     want = args.legs.split(",") if args.legs else []
 
@@ -788,8 +957,8 @@ def run_ours(args):
                                                     Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq))
         extend_session(st, sid, torch, dev, spec, st.info(sid)["n_tokens"], n0)
     if world == 1 and "graph" in want:
-        st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # n -> 32,768 as in the headline query
-        guarded("query_graph", lambda: leg_graph(st, sid, torch, stream, Qq, Kq, Vq, 10, 3))
+        guarded("per_layer", lambda: leg_per_layer(st, sid, torch, dev, spec, stream, peaks_l, 10, n0,
+                                                   Qa, Ka, Va, Qq, Kq, Vq))
         st.session_truncate(sid, n0)
     if world == 1 and "flash" in want:
         st.session_append(sid, Qa, Ka, Va, Oa, stream=stream)        # the 256-token update, n -> 32,768
@@ -827,23 +996,23 @@ def run_ours(args):
     line = None
     if rank == 0:
         clocks = clk.summary()
-        traffic = None
+        traffic, traffic_q, traffic_src = None, None, None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp):   # DRAM bytes per launch from the committed ncu --set full capture (labelled)
             try:
-                traffic = json.load(open(tp)).get("attn_data_bytes_per_launch")
-            except Exception:
-                traffic = None
+                tj = json.load(open(tp))
+                traffic, traffic_q = tj.get("attn_data_bytes_per_launch"), tj.get("attn_query_bytes_per_launch")
+                traffic_src = tj.get("source")
+            except Exception:  # noqa: BLE001
+                pass
         dominant_is_append = attn_a_ms >= attn_q_ms
         roof_append = {"bound": "tensor", "achieved": a_tflops, "peak": tc, "unit": "TFLOP/s",
-                       "frac": a_tflops / tc, "traffic": traffic,
+                       "frac": a_tflops / tc, "traffic": traffic, "traffic_source": traffic_src,
                        "kernel": "data-plane attention (256-token append, 32 layers/launch)",
                        "peak_source": f"{peak_src} bf16_tflops (burst)"}
         roof_query = {"bound": "hbm", "achieved": kern_q_gbs, "peak": hbm, "unit": "GB/s",
                       "frac": kern_q_gbs / hbm, "frac_of_nominal_7700": kern_q_gbs / NOMINAL_HBM_GBS,
-                      "traffic": (json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(
-                          "attn_query_bytes_per_launch") if os.path.exists(os.path.join(ROOT, "profiles",
-                                                                                       "traffic.json")) else None),
+                      "traffic": traffic_q, "traffic_source": traffic_src,
                       "kernel": "query-plane attention (32-token query, 32 layers/launch)",
                       "peak_source": f"{peak_src} hbm_gbs"}
         line = {
@@ -875,12 +1044,7 @@ def run_ours(args):
         }
         line.update(legs)
         if not args.no_cpu_baseline:
-            import oracle
-            oracle.build()
-            dt, nb = oracle_query_sample()
-            line["cpu_baseline"] = {"value": nb / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                                    "sample": "fp64 C oracle, single thread: one layer, one KV head (4 q heads), "
-                                              f"32-token query over 32,768 cached tokens ({dt:.1f} s)"}
+            line["cpu_baseline"] = cpu_baseline_leg(gpu_query_out)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

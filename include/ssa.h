@@ -122,6 +122,15 @@ typedef struct {
     int32_t kv_format;
     float k_scale;
     float v_scale;
+    /* Optional caller-owned KV pool (e.g. a torch allocation, so the
+     * framework's allocator owns device memory).  NULL: the store allocates the pool
+     * with cudaMalloc.  Otherwise pool_ptr must be device memory of cfg->device, 256-byte
+     * aligned, pool_bytes >= ssa_store_pool_bytes(cfg); K takes the first half and V
+     * the second half of ssa_store_pool_bytes(cfg).  The store zero-fills it at creation,
+     * never frees it, and the caller keeps it alive until ssa_store_destroy returns.
+     * A pointer that fails these checks gives SSA_ERR_INVALID_ARG. */
+    void *pool_ptr;
+    size_t pool_bytes;
 } ssa_store_config;
 
 enum { SSA_KV_SAME = 0, SSA_KV_E4M3 = 1 };
@@ -423,10 +432,13 @@ typedef enum {
     SSA_OPT_PIPE_CHUNKS = 11,   /* all-layer calls with host buffers: -1 no copy/compute
                                    pipelining, 0 default (2 layer chunks), n chunks */
     SSA_OPT_QKV_DEBUG = 12,     /* fused projection experiments: 0 off, 1 skip the epilogue */
-    SSA_OPT_CM_MERGE = 13       /* cluster-merge groups over several clusters: 1 (default)
+    SSA_OPT_CM_MERGE = 13,      /* cluster-merge groups over several clusters: 1 (default)
                                    a separate merge kernel (programmatic launch right
                                    behind the attention kernel), 0 the last arriving CTA
                                    merges inside the attention kernel */
+    SSA_OPT_L2_HINT = 14,       /* KV pool tiles loaded with an L2 evict-first hint: 0 (default)
+                                   when no key tile of the launch is read by two CTAs, 1 never,
+                                   2 always */
 } ssa_option;
 ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value);
 

@@ -16,7 +16,7 @@ import os
 
 __all__ = ["Store", "SsaError", "lib", "LIB_PATH", "WORK_APPEND", "WORK_QUERY", "WORK_STATELESS",
            "OPT_ATTN_BACKEND", "OPT_MAX_SPLITS", "OPT_FAULT_INJECT", "OPT_TC_Q_TILES", "OPT_TIMING",
-           "OPT_GRAPH_ARENA_RESET", "OPT_CLUSTER", "OPT_PDL", "OPT_PIPE_CHUNKS", "OPT_QKV_DEBUG", "OPT_CM_MERGE",
+           "OPT_GRAPH_ARENA_RESET", "OPT_CLUSTER", "OPT_PDL", "OPT_PIPE_CHUNKS", "OPT_QKV_DEBUG", "OPT_CM_MERGE", "OPT_L2_HINT",
            "debug_plan", "TIMING_KINDS"]
 TIMING_KINDS = ("attn_data", "attn_query", "combine_data", "combine_query", "scatter", "qkv_rope", "quant_e4m3")
 
@@ -26,6 +26,7 @@ LIB_PATH = os.path.join(_HERE, "libssa.so")
 WORK_APPEND, WORK_QUERY, WORK_STATELESS = 0, 1, 2
 OPT_ATTN_BACKEND, OPT_MAX_SPLITS, OPT_FAULT_INJECT, OPT_TC_Q_TILES, OPT_TIMING = 1, 2, 3, 4, 5
 OPT_GRAPH_ARENA_RESET, OPT_CLUSTER, OPT_PDL, OPT_PIPE_CHUNKS, OPT_QKV_DEBUG, OPT_CM_MERGE = 8, 9, 10, 11, 12, 13
+OPT_L2_HINT = 14
 BF16, FP32 = 0, 1
 
 _STATUS = {0: "SSA_OK", -1: "SSA_ERR_INVALID_ARG", -2: "SSA_ERR_UNKNOWN_SESSION", -3: "SSA_ERR_POOL_EXHAUSTED",
@@ -46,7 +47,8 @@ class StoreConfig(ctypes.Structure):
                 ("page_size", ctypes.c_int32), ("num_pages", ctypes.c_int64),
                 ("max_sessions", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("softmax_scale", ctypes.c_float),
-                ("kv_format", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float)]
+                ("kv_format", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
+                ("pool_ptr", ctypes.c_void_p), ("pool_bytes", ctypes.c_size_t)]
 
 
 KV_SAME, KV_E4M3 = 0, 1
@@ -178,12 +180,20 @@ class Store:
 
     def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, page_size=64, num_pages=1024,
                  max_sessions=64, device=0, dtype="bf16", softmax_scale=0.0, kv_format=None,
-                 k_scale=1.0, v_scale=1.0):
+                 k_scale=1.0, v_scale=1.0, pool=None):
         """kv_format None: K/V stored in `dtype`; "e4m3": E4M3 codes of K/k_scale, V/v_scale
-        (include/ssa.h, reading R-22)."""
+        (include/ssa.h, reading R-22).  pool: optional caller-owned device buffer for the KV
+        pool (a contiguous torch tensor of >= pool_bytes(...) bytes on `device`); the store
+        keeps a reference to it."""
+        self._pool = pool
+        pool_ptr, pool_nbytes = (None, 0)
+        if pool is not None:
+            pool_ptr = _ptr(pool)
+            pool_nbytes = pool.numel() * pool.element_size() if hasattr(pool, "numel") else int(pool.nbytes)
         self.cfg = StoreConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
                                max_sessions, device, BF16 if dtype == "bf16" else FP32, softmax_scale,
-                               KV_E4M3 if kv_format == "e4m3" else KV_SAME, k_scale, v_scale)
+                               KV_E4M3 if kv_format == "e4m3" else KV_SAME, k_scale, v_scale,
+                               pool_ptr, pool_nbytes)
         self.dtype = dtype
         self.kv_format = kv_format
         self.L, self.hq, self.hkv, self.d, self.P = num_layers, num_q_heads, num_kv_heads, head_dim, page_size

@@ -286,6 +286,13 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* out, float4 v) {
+  uint2 u;
+  u.x = pack_bf16(v.x, v.y);
+  u.y = pack_bf16(v.z, v.w);
+  *reinterpret_cast<uint2*>(out) = u;
+}
+
 // Slot rows -> exchange buffer: O * inv_l (zeros for a row with no keys) and lse.
 __device__ __forceinline__ void cm_stage_rows(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
                                               bool has) {
@@ -307,9 +314,11 @@ __device__ __forceinline__ void cm_stage_rows(float* X, int rr, bool live, uint3
   if (live) X[kM * kXStride + rr] = has ? lse : -CUDART_INF_F;
 }
 
-// Split pair: slot 0 merges slot 1's staged rows with its own (R-11), in place.
+// Split pair: slot 0 merges slot 1's staged rows with its own (R-11), in place --
+// or, with `out` (a CTA that holds its whole group: cluster of 1, one cluster per
+// group), straight into the bf16 output row.
 __device__ __forceinline__ void cm_merge_rows(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
-                                              bool has) {
+                                              bool has, __nv_bfloat16* out = nullptr) {
   float a0 = 0.f, a1 = 0.f, lm = -CUDART_INF_F;
   if (live) {
     const float l1 = X[kM * kXStride + rr];
@@ -339,11 +348,14 @@ __device__ __forceinline__ void cm_merge_rows(float* X, int rr, bool live, uint3
         v.y = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 1]) : 0.f) + a1 * x1.y;
         v.z = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 2]) : 0.f) + a1 * x1.z;
         v.w = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 3]) : 0.f) + a1 * x1.w;
-        *reinterpret_cast<float4*>(dst + i) = v;
+        if (out)
+          store_bf16x4(out + q4 * 32 + i, v);
+        else
+          *reinterpret_cast<float4*>(dst + i) = v;
       }
     }
   }
-  if (live) X[kM * kXStride + rr] = lm;
+  if (live && !out) X[kM * kXStride + rr] = lm;
 }
 
 __device__ __forceinline__ void store_bf16x8(__nv_bfloat16* out, const float* v) {
@@ -363,12 +375,6 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
   return v;
-}
-__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* out, float4 v) {
-  uint2 u;
-  u.x = pack_bf16(v.x, v.y);
-  u.y = pack_bf16(v.z, v.w);
-  *reinterpret_cast<uint2*>(out) = u;
 }
 
 template <int C>
@@ -623,6 +629,10 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   // stages.  K(e) is released by its S MMA, V(e) by its PV MMA, which run
   // about a tile later, so the rings and their producer warps progress
   // independently (K loads run further ahead).
+  // CM CTA whose groups it holds alone (cluster of 1, one cluster per group): the
+  // epilogue writes O straight from the slots, no exchange buffer / reduce
+  const bool cm_direct = p.cm_C == 1 && p.groups[w0.group].n_splits == 1 &&
+                         (pr.ub < 0 || p.groups[w1.group].n_splits == 1);
   const int NK = 3;
   const int NV = two_q ? 2 : 3;
   uint8_t* q_buf[2] = {tiles, two_q ? tiles + kSlotBytes : tiles};
@@ -748,8 +758,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
                 const int64_t page = page_window(bar.pwin_base[pw][k], bar.pwin[pw][k], sg, slot / p.P);
                 row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
               }
-              for (int c = 0; c < nchunk; ++c)
-                tma_load_2d_hint(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row, pol);
+              for (int c = 0; c < nchunk; ++c) {
+                if (p.l2_evict_first)
+                  tma_load_2d_hint(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row, pol);
+                else
+                  tma_load_2d(dst + c * kChunkBytes + b * box_rows * 128, pool_map, &full[s], c * 64, row);
+              }
             }
           } else {
             const int32_t krow = (int32_t)(in_l + sg.row0 + (tile - n_pool_tiles) * kBN);
@@ -848,7 +862,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         }
       }
     }
-    if (p.cm_C > 0) {   // the two cluster barriers of the CM epilogue
+    if (p.cm_C > 0 && !cm_direct) {   // the two cluster barriers of the CM epilogue
       cm_sync(p.cm_C);
       cm_sync(p.cm_C);
     }
@@ -1014,12 +1028,28 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         if (pr.ub >= 0 && nt_o > 0) mbar_wait(&bar.o_final[k ^ 1], 0);
         tc_fence_after();
         float* X0 = reinterpret_cast<float*>(k_base);
+        __nv_bfloat16* orow_ptr = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD;
         if (pr.same_q && pr.ub >= 0) {
           // split pair: slot 1 stages its rows, slot 0 merges them into its own (R-11)
           if (k == 1) cm_stage_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f);
           asm volatile("bar.sync 3, 256;" ::: "memory");
-          if (k == 0) cm_merge_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f);
+          if (k == 0) cm_merge_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f, cm_direct ? orow_ptr : nullptr);
           GTRACE_T(true, 8);
+        } else if (cm_direct) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t ro[32];
+            tmem_ld32(o_col + q4 * 32, ro);
+            tmem_wait_ld();
+            if (live)
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = l_run > 0.f ? __uint_as_float(ro[i + u]) * inv_l : 0.f;
+                store_bf16x8(orow_ptr + q4 * 32 + i, v);
+              }
+          }
         } else {
           cm_stage_rows(X0 + (pr.same_q ? 0 : k) * kXFloats, rr, live, o_col, inv_l, lse, l_run > 0.f);
         }
@@ -1057,7 +1087,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       if (w.group >= 0 && live) p.part_lse[pslot * kM + rr] = lse;
       }   // !cm
     }
-    if (p.cm_C > 0) {
+    if (p.cm_C > 0 && !cm_direct) {
       cm_sync(p.cm_C);   // every CTA of the cluster has staged its rows
       GTRACE_T(true, 9);
       if (k < (two_q ? 2 : 1)) {

@@ -101,6 +101,8 @@ struct AttnParams {
   // groups over K > 1 clusters: merge tickets [layers][n_groups][cm_C] (zero between
   // launches) for the in-kernel last-arriver merge, or null: cm_merge_kernel
   int32_t* cm_tickets;
+  // pool tiles are loaded with an L2 evict-first hint (read once per launch)
+  int32_t l2_evict_first;
   // FP8 KV variant (reading R-22): pools and Kt/Vt hold E4M3 codes; scale_log2
   // already includes k_scale, o_scale = v_scale multiplies 1/l
   int32_t kv_fp8;

@@ -595,6 +595,18 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
         }
       }
       for (auto& g : plan.groups) fresh.max_split = std::max(fresh.max_split, g.n_splits);
+      // L2 evict-first pays only when no key tile of the launch is read twice: one q-tile
+      // group per (cached pool, KV head) -- not appends, multi-tile queries or Flash batches
+      {
+        std::vector<std::pair<const int32_t*, int>> seen;
+        bool once = !plan.groups.empty();
+        for (auto& g : plan.groups) {
+          const std::pair<const int32_t*, int> kk{segs[g.seg].pages, g.kv_head};
+          if (std::find(seen.begin(), seen.end(), kk) != seen.end()) { once = false; break; }
+          seen.push_back(kk);
+        }
+        fresh.l2_hint = once;
+      }
     }
     // ---- host image of the lists: segments, units, groups, scatter segments + prefix, CTA pairs
     std::vector<SegDesc> app_segs;
@@ -772,6 +784,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     // pool tiles may be prefetched before griddepcontrol.wait unless the grid right
     // before this one on the stream is one of the store's pool writers
     ap.pool_early = (opt_pdl != 0 && !(pool_writer_last && last_kernel_stream == st)) ? 1 : 0;
+    ap.l2_evict_first = opt_l2_hint == 2 || (opt_l2_hint == 0 && E.l2_hint) ? 1 : 0;
     const bool merge_in_kernel = E.cm_C > 0 && E.max_split > 1 && opt_cm_merge == 0;
     if (merge_in_kernel) {
       const size_t need = (size_t)n_layers * plan.groups.size() * E.cm_C;
@@ -790,16 +803,18 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       SSA_CUDA(this, launch_attn_tc(ap, n_layers, opt_pdl != 0 && !t0, st));
       stats.tc_launches++;
       if (E.cm_C > 0) stats.cm_launches++;
-      if (E.cm_C > 0 && E.max_split > 1 && !merge_in_kernel) {   // groups over several clusters: merge kernel
-        SSA_CUDA(this, launch_cm_merge(ap, n_layers, opt_pdl != 0 && !t0, st));
-        stats.kernel_launches++;
-      }
     } else {
       SSA_CUDA(this, launch_attn_simt(ap, n_layers, cfg.dtype == SSA_BF16, st));
     }
     if (t0) timed_push(query_plane ? 1 : 0, t0, tick(st));
     stats.kernel_launches++;
     note_kernel(st, false);
+    if (E.cm_C > 0 && E.max_split > 1 && !merge_in_kernel) {   // groups over several clusters: merge kernel
+      cudaEvent_t t1 = tick(st);
+      SSA_CUDA(this, launch_cm_merge(ap, n_layers, opt_pdl != 0 && !t1, st));
+      if (t1) timed_push(query_plane ? 3 : 2, t1, tick(st));
+      stats.kernel_launches++;
+    }
     if (combine) {
       CombineParams cp{};
       cp.part_o = part_o;
@@ -931,7 +946,24 @@ ssa_status ssa_store_create(const ssa_store_config* cfg, ssa_store_t* out) {
   const size_t half = ssa_store_pool_bytes(cfg) / 2;
   st->pool_half_bytes = half;
   st->arena_cap = 4u << 20;
-  if ((e = cudaMalloc(&st->poolK, half)) != cudaSuccess || (e = cudaMalloc(&st->poolV, half)) != cudaSuccess ||
+  if (cfg->pool_ptr) {
+    // borrowed pool (caller-owned device memory of this device, big enough, aligned)
+    cudaPointerAttributes a{};
+    const bool ok = cudaPointerGetAttributes(&a, cfg->pool_ptr) == cudaSuccess && a.type == cudaMemoryTypeDevice &&
+                    a.device == cfg->device && cfg->pool_bytes >= 2 * half &&
+                    (reinterpret_cast<uintptr_t>(cfg->pool_ptr) & 255) == 0;
+    cudaGetLastError();
+    if (!ok) {
+      set_error("pool_ptr: not 256-byte aligned device memory of device %d with >= %zu bytes", cfg->device, 2 * half);
+      delete st;
+      return SSA_ERR_INVALID_ARG;
+    }
+    st->pool_owned = false;
+    st->poolK = cfg->pool_ptr;
+    st->poolV = static_cast<char*>(cfg->pool_ptr) + half;
+  }
+  if ((!cfg->pool_ptr && ((e = cudaMalloc(&st->poolK, half)) != cudaSuccess ||
+                          (e = cudaMalloc(&st->poolV, half)) != cudaSuccess)) ||
       (e = cudaMemset(st->poolK, 0, half)) != cudaSuccess || (e = cudaMemset(st->poolV, 0, half)) != cudaSuccess ||
       (e = st->ring.init(8u << 20)) != cudaSuccess ||
       (e = cudaMallocHost(reinterpret_cast<void**>(&st->arena_h), 4u << 20)) != cudaSuccess ||
@@ -955,8 +987,10 @@ ssa_store::~ssa_store() {
   for (auto e : spare_events) cudaEventDestroy(e);
   for (auto& s : sessions)
     if (s.d_pages) cudaFree(s.d_pages);
-  if (poolK) cudaFree(poolK);
-  if (poolV) cudaFree(poolV);
+  if (pool_owned) {
+    if (poolK) cudaFree(poolK);
+    if (poolV) cudaFree(poolV);
+  }
   if (part_o) cudaFree(part_o);
   if (part_lse) cudaFree(part_lse);
   if (stage) cudaFree(stage);
@@ -1026,6 +1060,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
       break;
     case SSA_OPT_PDL: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_pdl = value; break;
     case SSA_OPT_CM_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
+    case SSA_OPT_L2_HINT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_l2_hint = value; break;
     case SSA_OPT_PIPE_CHUNKS: if (value < -1 || value > 64) return SSA_ERR_INVALID_ARG; st->opt_pipe_chunks = value; break;
     case SSA_OPT_QKV_DEBUG: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_qkv_debug = value; break;
     default: return SSA_ERR_INVALID_ARG;

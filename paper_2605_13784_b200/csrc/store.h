@@ -100,6 +100,7 @@ struct ssa_store {
   bool sm100 = false;
   void* poolK = nullptr;
   void* poolV = nullptr;
+  bool pool_owned = true;   // false: ssa_store_config::pool_ptr (caller-owned)
   size_t pool_half_bytes = 0;
   std::vector<ssa::Session> sessions;
   std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_pages;
@@ -119,6 +120,7 @@ struct ssa_store {
     std::vector<ssa::TcPair> pairs;
     int32_t cm_C = 0;          // cluster-merge launch (AttnParams::cm_C), 0 = combine kernel / SIMT
     int32_t max_split = 0;     // largest Group::n_splits
+    bool l2_hint = false;      // every key tile is read by one CTA (no reuse in L2 to keep)
     int32_t n_app = 0;         // scatter segments
     int32_t app_tokens = 0;
     std::vector<char> image;   // host copy of the lists
@@ -157,6 +159,7 @@ struct ssa_store {
   int64_t opt_cluster = 0;       // SSA_OPT_CLUSTER
   int64_t opt_pdl = 1;           // SSA_OPT_PDL
   int64_t opt_cm_merge = 1;      // SSA_OPT_CM_MERGE
+  int64_t opt_l2_hint = 0;       // SSA_OPT_L2_HINT
   int32_t* tickets = nullptr;    // CM merge tickets (zero between launches)
   size_t tickets_cap = 0;
   int64_t opt_pipe_chunks = 0;   // SSA_OPT_PIPE_CHUNKS

@@ -48,3 +48,28 @@ def within(got, ref, dtype):
     mx, mn = errors(got, ref)
     tmax, tmean = TOL[dtype]
     return mx <= tmax and mn <= tmean, (mx, mn)
+
+
+def abs_bits(x):
+    """|x| of bf16 bit patterns (clear the sign bit) or floats, exactly."""
+    x = np.asarray(x)
+    return x & np.uint16(0x7FFF) if x.dtype == np.uint16 else np.abs(x)
+
+
+def attention_bound(A, o_ref, n_keys, p_unit=2.0 ** -8):
+    """Derived per-element error bound of a tcgen05 attention output against the fp64 oracle
+    (parity bound).  The kernel rounds each weight p_j to bf16 (relative error
+    <= 2^-8; fp16 for an E4M3 store: p_unit = 2^-11) before P V but normalises by the fp32 sum
+    of the unrounded weights, so the weight rounding moves O_e by at most p_unit *
+    sum_j w_j |v_j[e]| = p_unit * A_e, where A is the oracle's attention output with |V| in
+    place of V; fp32 accumulation over n keys adds at most n * 2^-24 * A_e; the one rounding of
+    O to bf16 adds 2^-8 |O_e|.  A 1.25 factor covers the fp32 score / exp2 / split-merge terms
+    (each below 2^-12 relative)."""
+    return 1.25 * (p_unit + n_keys * 2.0 ** -24) * np.asarray(A) + 2.0 ** -8 * np.abs(o_ref) + 1e-6
+
+
+def within_bound(got, ref, bound):
+    """(all errors within the derived bound, largest error / bound)."""
+    e = np.abs(f64(got) - ref)
+    r = e / bound
+    return bool((r <= 1.0).all()), float(r.max())

@@ -313,8 +313,6 @@ def test_fp8_per_layer_and_host_buffers(cuda):
     for O in (Oa, Ob):     # per-layer launches use cluster-merge plans: not bit-identical to all-layer
         ok, e = within(from_dev(O), Oref, "bf16")
         assert ok, e
-    a, b = Oa.float(), Ob.float()     # within two bf16 ulps of each other
-    assert bool(((a - b).abs() <= 2.0 ** -6 * torch.maximum(a.abs(), b.abs()) + 1e-3).all())
     assert a.digest(sa) == b.digest(sb)
     Qq, Kq, Vq = gen_qkv(spec, L, LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
     Od = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)

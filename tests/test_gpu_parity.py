@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 import streams
-from helpers import TOL, errors, f64, from_dev, gen_qkv, to_dev, within
+from helpers import TOL, abs_bits, attention_bound, errors, f64, from_dev, gen_qkv, to_dev, within, within_bound
 
 pytestmark = pytest.mark.gpu
 
@@ -25,6 +25,16 @@ def _rows_ref(ref, sid, layer, Q, K, V, tokens=None, heads=None):
     s = ref.sessions[sid]
     return oracle.segment_rows(s.k[layer][:s.n_tokens], s.v[layer][:s.n_tokens], Q, K, V, ref.hkv, ref.scale,
                                tokens, heads)[0]
+
+
+def _bound(ref, sid, Q, K, V, O_ref, heads=None):
+    """Derived per-element bound (helpers.attention_bound) of new-segment rows [L][m][H][d]
+    against the session's current cache: the oracle's attention of the same rows with |V|."""
+    s = ref.sessions[sid]
+    A = np.stack([oracle.segment_rows(s.k[l][:s.n_tokens], abs_bits(s.v[l][:s.n_tokens]), Q[l], K[l],
+                                      abs_bits(V[l]), ref.hkv, ref.scale, None, heads)[0]
+                  for l in range(Q.shape[0])])
+    return attention_bound(A, O_ref, s.n_tokens + Q.shape[1])
 
 
 # --------------------------------------------------------------------------- config 1 (toy fp32)
@@ -112,10 +122,11 @@ def _llama_session(cuda, spec, n0=512, appends=(256, 256), num_pages=256, backen
     for m in appends:
         Q, K, V = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 0, tok, m)
         O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
-        Ref_rows = [_rows_ref(ref, rsid, l, Q[l], K[l], V[l], heads=[0, 9, 31]) for l in range(LL["L"])]
+        Ref_rows = np.stack([_rows_ref(ref, rsid, l, Q[l], K[l], V[l], heads=[0, 9, 31]) for l in range(LL["L"])])
+        bound = _bound(ref, rsid, Q, K, V, Ref_rows, heads=[0, 9, 31])
         st.session_append(sid, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
         ref.session_append(rsid, Q, K, V, compute=False)
-        outs.append((from_dev(O)[:, :, [0, 9, 31]], np.stack(Ref_rows)))
+        outs.append((from_dev(O)[:, :, [0, 9, 31]], Ref_rows, bound))
         tok += m
     return st, ref, sid, rsid, tok, outs
 
@@ -128,14 +139,21 @@ def test_llama_append_and_query_bf16(cuda, stream_name, backend):
     spec = streams.StreamSpec(stream_name, seed=2)
     st, ref, sid, rsid, tok, outs = _llama_session(cuda, spec, backend=backend)
     assert (st.stats()["tc_launches"] > 0) == (backend == 2)
-    for got, want in outs:
+    for got, want, bound in outs:
         ok, e = within(got, want, "bf16")
         assert ok, ("append", e)
+        if backend == 2:   # the tcgen05 kernel's derived per-element bound (bf16 P, bf16 O)
+            ok, r = within_bound(got, want, bound)
+            assert ok, ("append bound", r)
     Qq, Kq, Vq = gen_qkv(spec, LL["L"], LL["hq"], LL["hkv"], LL["d"], 1, 0, 32)
     Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
     st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
-    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    want = ref.session_query(rsid, Qq, Kq, Vq)
+    ok, e = within(from_dev(Oq), want, "bf16")
     assert ok, ("query", e)
+    if backend == 2:
+        ok, r = within_bound(from_dev(Oq), want, _bound(ref, rsid, Qq, Kq, Vq, want))
+        assert ok, ("query bound", r)
     assert st.page_table(sid) == ref.page_table(rsid)
     assert st.digest(sid) == ref.digest(rsid)
 
@@ -258,8 +276,8 @@ def test_batch_run_snapshot(cuda):
 
 def test_per_layer_append_equals_all_layer(cuda):
     """Per-layer tickets (single-layer launches, cluster-merge plans) vs one all-layer append:
-    identical pages and digest (bit-exact), both within tolerance of the oracle and within
-    bf16 rounding of each other (the split structure differs, so the fp32 sums do too)."""
+    identical pages and digest (bit-exact), both within tolerance and within the derived
+    per-element bound of the oracle (the split structures differ, so the fp32 sums do too)."""
     import torch
     ssa = _ssa()
     L, hq, hkv, d, P = 3, 8, 2, 128, 64
@@ -272,7 +290,9 @@ def test_per_layer_append_equals_all_layer(cuda):
     sb = b.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
     rs, _ = ref.session_create(200, Q, K, V, compute=False)
     Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 200, 90)
-    Oref, _ = ref.session_append(rs, Q, K, V)
+    Oref = np.stack([_rows_ref(ref, rs, l, Q[l], K[l], V[l]) for l in range(L)])
+    bound = _bound(ref, rs, Q, K, V, Oref)
+    ref.session_append(rs, Q, K, V, compute=False)
     Oa = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
     a.session_append(sa, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), Oa)
     t = b.append_begin(sb, 90)
@@ -285,8 +305,8 @@ def test_per_layer_append_equals_all_layer(cuda):
     for O in (Oa, Ob):
         ok, e = within(from_dev(O), Oref, "bf16")
         assert ok, e
-    a, b = Oa.float(), Ob.float()     # within two bf16 ulps of each other
-    assert bool(((a - b).abs() <= 2.0 ** -6 * torch.maximum(a.abs(), b.abs()) + 1e-3).all())
+        ok, r = within_bound(from_dev(O), Oref, bound)
+        assert ok, r
     assert a.digest(sa) == b.digest(sb) and a.info(sa) == b.info(sb)
 
 
@@ -509,6 +529,7 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
     rsid, _ = ref.session_create(n, Q, K, V, compute=False)
     Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, nq)
     want = ref.session_query(rsid, Qq, Kq, Vq)
+    bound = _bound(ref, rsid, Qq, Kq, Vq, want)
     Qd, Kd, Vd = to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda)
     for C, merge in ((0, 1), (-1, 1), (1, 1), (1, 0), (2, 1), (2, 0), (4, 1), (4, 0), (6, 1), (8, 1)):
         st.set_option(ssa.OPT_CLUSTER, C)
@@ -523,6 +544,8 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
                 splits.append(plan["max_split"])
             ok, e = within(from_dev(O), want, "bf16")
             assert ok, (C, rep, e)
+            ok, r = within_bound(from_dev(O), want, bound)
+            assert ok, (C, rep, "bound", r)
         if C in (1, 2):
             assert max(splits) > 1, (C, splits)     # the cross-cluster (last-arriver) merge ran
     assert st.stats()["cm_launches"] >= 2 * L * 10
@@ -1024,3 +1047,39 @@ def test_query_plane_cuda_graph_capture(cuda, kv):
     torch.cuda.synchronize()
     assert torch.equal(O_all.view(torch.int16), want_all.view(torch.int16))
     st.close()
+
+
+def test_borrowed_pool_from_torch(cuda):
+    """ssa_store_config.pool_ptr: the KV pool lives in a torch allocation.  The
+    store writes its pages there (the K half of the buffer holds the session's keys at their
+    page slots), parity as with a store-owned pool; an undersized or host buffer is rejected."""
+    import torch
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    nb = ssa.Store.pool_bytes(L, hq, hkv, d, P, 64)
+    buf = torch.zeros(nb, dtype=torch.uint8, device=cuda)
+    st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64, pool=buf)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+    spec = streams.StreamSpec("market", seed=66)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 1000)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
+    sid = st.session_create(to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    rsid, Oref = ref.session_create(1000, Q, K, V)
+    ok, e = within(from_dev(O), Oref, "bf16")
+    assert ok, e
+    torch.cuda.synchronize()
+    # token 0 of layer 0, kv head 0 sits at page_table[0], slot 0: [L][pages][Hkv][P][d] bf16
+    pg = st.page_table(sid)[0]
+    k_pool = buf[: nb // 2].view(torch.int16).view(L, 64, hkv, P, d)
+    assert np.array_equal(k_pool[0, pg, 0, 0].cpu().numpy().view(np.uint16), K[0, 0, 0])
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 32)
+    Oq = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda)
+    st.session_query(sid, to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda), Oq)
+    ok, e = within(from_dev(Oq), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+    assert ok, e
+    assert st.digest(sid) == ref.digest(rsid)
+    st.close()
+    with pytest.raises(ssa.SsaError, match="INVALID_ARG"):
+        ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64, pool=torch.zeros(nb // 2, dtype=torch.uint8, device=cuda))
+    with pytest.raises(ssa.SsaError, match="INVALID_ARG"):
+        ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64, pool=torch.zeros(nb, dtype=torch.uint8))
