@@ -509,14 +509,21 @@ ssa_status ssa_comm_destroy(ssa_store_t store);
  * into every rank's gathered buffer by the kernel that produces it (NVLink
  * P2P stores from the split-KV combine epilogue), a system-scope release of a
  * per-rank epoch flag follows on the same stream, and each rank's merge waits
- * (acquire) for all flags of the epoch -- no collective launch, no staging copy.
- * peer_bufs[q] / peer_flags[q] (host arrays of `world` device addresses valid
- * in this process, e.g. from torch symmetric memory) are rank q's gathered
- * buffer ([world][chunk] fp32, buf_bytes each, chunk = rows*Hq*(D+1) as in
- * ssa_sharded_partial) and its uint32 flag array [world] (zero-initialised,
- * epochs increase by one per push).  Replaces any NCCL communicator.  After
- * attaching, ssa_sharded_query = ssa_sharded_push + ssa_sharded_merge.
- * Errors: SSA_ERR_INVALID_ARG (null / out-of-range), SSA_ERR_STATE (not attached). */
+ * (acquire, one spinning block) for all flags of the epoch -- no collective
+ * launch, no staging copy.  peer_bufs[q] / peer_flags[q] (host arrays of `world`
+ * device addresses valid in this process, e.g. from torch symmetric memory) are
+ * rank q's gathered buffer ([2][world][chunk] fp32, buf_bytes each, chunk =
+ * rows*Hq*(D+1) as in ssa_sharded_partial; epoch e uses half e & 1) and its
+ * uint32 flag array [2][world] (zero-initialised): ready[p] = the last epoch rank
+ * p pushed into this buffer, ack[p] = the last epoch rank p finished merging.  A
+ * push of epoch e first waits for every peer's ack of e - 2 (the merge that last
+ * read that half), so ranks may run any number of push/merge rounds back to back
+ * without a barrier; a rank alternates push and merge, and the chunk size is
+ * fixed after the first push.  Replaces any NCCL communicator.  After attaching,
+ * ssa_sharded_query = ssa_sharded_push + ssa_sharded_merge.  A peer that never
+ * signals fails the waiting launch after 10 s (sticky CUDA error) instead of
+ * hanging.  Errors: SSA_ERR_INVALID_ARG (null / out-of-range / buffers too
+ * small), SSA_ERR_STATE (not attached, push without merge, merge without push). */
 ssa_status ssa_comm_attach_peers(ssa_store_t store, int32_t rank, int32_t world, const uint64_t *peer_bufs,
                                  const uint64_t *peer_flags, size_t buf_bytes);
 ssa_status ssa_sharded_push(ssa_store_t store, ssa_session_t session, int32_t layer, int32_t n_q,

@@ -74,14 +74,17 @@ struct CommState {
   float* buf = nullptr;     // [send chunk | world gathered chunks]
   size_t cap = 0;           // floats
   // peer-memory path (ssa_comm_attach_peers): every rank's gathered buffer
-  // [world][chunk] floats and flag array [world] uint32, mapped in this process
+  // [2][world][chunk] floats (halves alternate by epoch parity) and flag array
+  // [2][world] uint32 (ready[q]: last epoch rank q pushed here; ack[q]: last
+  // epoch rank q finished merging), mapped in this process
   bool peers = false;
   std::vector<uint64_t> peer_buf, peer_flag;
   size_t peer_bytes = 0;
   uint64_t* d_peer_flag = nullptr;   // device copy of peer_flag
-  uint64_t* d_peer_chunk = nullptr;  // device: this rank's chunk slot in every peer buffer
+  uint64_t* d_peer_chunk = nullptr;  // device: [2][world] this rank's chunk slot in every peer buffer half
   int64_t chunk_for = -1;            // chunk size d_peer_chunk was built for
-  uint32_t epoch = 0;
+  uint32_t epoch = 0;                // last pushed epoch
+  uint32_t merged = 0;               // last merged epoch
 };
 
 void ssa_store::destroy_comm() {
@@ -214,7 +217,7 @@ ssa_status ssa_comm_attach_peers(ssa_store_t st, int32_t rank, int32_t world, co
   c->peer_bytes = buf_bytes;
   st->comm = c;
   COMM_CUDA(st, cudaMalloc(&c->d_peer_flag, world * sizeof(uint64_t)));
-  COMM_CUDA(st, cudaMalloc(&c->d_peer_chunk, world * sizeof(uint64_t)));
+  COMM_CUDA(st, cudaMalloc(&c->d_peer_chunk, 2 * world * sizeof(uint64_t)));
   COMM_CUDA(st, cudaMemcpy(c->d_peer_flag, peer_flags, world * sizeof(uint64_t), cudaMemcpyHostToDevice));
   return SSA_OK;
 }
@@ -234,19 +237,35 @@ ssa_status ssa_sharded_push(ssa_store_t st, ssa_session_t id, int32_t layer, int
   const int64_t Lin = layer < 0 ? st->cfg.num_layers : 1;
   const int64_t rows = Lin * n_q;
   const int64_t chunk = rows * st->cfg.num_q_heads * (int64_t)(st->cfg.head_dim + 1);
-  if ((size_t)(c->world * chunk) * sizeof(float) > c->peer_bytes) {
-    set_error("sharded_push: peer buffers hold %zu bytes, need %lld", c->peer_bytes,
-              (long long)(c->world * chunk * (int64_t)sizeof(float)));
+  if ((size_t)(2 * c->world * chunk) * sizeof(float) > c->peer_bytes) {
+    set_error("sharded_push: peer buffers hold %zu bytes, need %lld (two halves)", c->peer_bytes,
+              (long long)(2 * c->world * chunk * (int64_t)sizeof(float)));
     return SSA_ERR_INVALID_ARG;
   }
-  if (c->chunk_for != chunk) {   // this rank's chunk slot in every peer's gathered buffer
-    std::vector<uint64_t> slot(c->world);
-    for (int q = 0; q < c->world; ++q) slot[q] = c->peer_buf[q] + (uint64_t)c->rank * chunk * sizeof(float);
-    COMM_CUDA(st, cudaMemcpyAsync(c->d_peer_chunk, slot.data(), c->world * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                  cs));
+  if (c->epoch != c->merged) {
+    set_error("sharded_push: merge the previous epoch first");
+    return SSA_ERR_STATE;
+  }
+  if (c->chunk_for != chunk) {   // this rank's chunk slot in both halves of every peer's gathered buffer
+    if (c->chunk_for >= 0 && c->epoch > 0) {
+      set_error("sharded_push: the chunk size is fixed after the first push (re-attach to change it)");
+      return SSA_ERR_STATE;
+    }
+    std::vector<uint64_t> slot(2 * c->world);
+    for (int h = 0; h < 2; ++h)
+      for (int q = 0; q < c->world; ++q)
+        slot[h * c->world + q] = c->peer_buf[q] + ((uint64_t)h * c->world + c->rank) * chunk * sizeof(float);
+    COMM_CUDA(st, cudaMemcpyAsync(c->d_peer_chunk, slot.data(), 2 * c->world * sizeof(uint64_t),
+                                  cudaMemcpyHostToDevice, cs));
     COMM_CUDA(st, cudaStreamSynchronize(cs));
     c->chunk_for = chunk;
   }
+  const uint32_t e = c->epoch + 1;
+  // half e & 1 of every peer buffer was last read by the peers' merges of epoch e - 2:
+  // wait for their acks (slots [world, 2 world) of this rank's own flag array)
+  if (e >= 3)
+    COMM_CUDA(st, launch_wait_flags(reinterpret_cast<const uint32_t*>(c->peer_flag[c->rank]) + c->world, c->world,
+                                    e - 2, cs));
   const size_t el = st->elem;
   IoSet io;
   io.q = {Q, (size_t)rows * st->cfg.num_q_heads * st->cfg.head_dim * el};
@@ -262,13 +281,13 @@ ssa_status ssa_sharded_push(ssa_store_t st, ssa_session_t id, int32_t layer, int
   std::vector<SegDesc> segs{sg};
   RunOpts opts;
   opts.force_groups = true;
-  opts.peer_chunk = c->d_peer_chunk;
+  opts.peer_chunk = c->d_peer_chunk + (e & 1) * c->world;
   opts.n_peers = c->world;
   opts.lse_off = rows * st->cfg.num_q_heads * (int64_t)st->cfg.head_dim;
   if ((rc = st->run(segs, io, n_q, layer < 0 ? 0 : layer, (int32_t)Lin, 1, true, true, cs, opts)) != SSA_OK) return rc;
-  c->epoch += 1;
-  COMM_CUDA(st, launch_signal_peers(c->d_peer_flag, c->world, c->rank, c->epoch, cs));
-  st->stats.kernel_launches++;
+  c->epoch = e;
+  COMM_CUDA(st, launch_signal_peers(c->d_peer_flag, c->world, c->rank, e, cs));   // ready[rank] on every peer
+  st->stats.kernel_launches += e >= 3 ? 2 : 1;
   return SSA_OK;
 }
 
@@ -285,11 +304,22 @@ ssa_status ssa_sharded_merge(ssa_store_t st, int32_t layer, int32_t n_q, void* O
   IoSet io;
   io.o = {O, (size_t)rows * st->cfg.num_q_heads * st->cfg.head_dim * st->elem};
   if ((rc = st->stage_inputs(&io, cs)) != SSA_OK) return rc;
-  const float* gathered = reinterpret_cast<const float*>(c->peer_buf[c->rank]);
-  const uint32_t* flags = reinterpret_cast<const uint32_t*>(c->peer_flag[c->rank]);
+  if (c->epoch == c->merged) {
+    set_error("sharded_merge: no pushed epoch to merge");
+    return SSA_ERR_STATE;
+  }
+  const uint32_t e = c->epoch;
+  const int64_t chunk = rows * st->cfg.num_q_heads * (int64_t)(st->cfg.head_dim + 1);
+  if (chunk != c->chunk_for) return SSA_ERR_INVALID_ARG;
+  const float* gathered = reinterpret_cast<const float*>(c->peer_buf[c->rank]) + (e & 1) * c->world * chunk;
+  // every rank's chunk of epoch e has landed (ready slots [0, world) of this rank's flags)
+  COMM_CUDA(st, launch_wait_flags(reinterpret_cast<const uint32_t*>(c->peer_flag[c->rank]), c->world, e, cs));
   COMM_CUDA(st, launch_merge_ranks(gathered, c->world, rows, st->cfg.num_q_heads, st->cfg.head_dim, io.o.dev,
-                                   st->cfg.dtype == SSA_BF16, cs, flags, c->epoch));
-  st->stats.kernel_launches++;
+                                   st->cfg.dtype == SSA_BF16, cs));
+  // this rank is done reading half e & 1: ack[rank] = e on every peer (they may reuse it for e + 2)
+  COMM_CUDA(st, launch_signal_peers(c->d_peer_flag, c->world, c->world + c->rank, e, cs));
+  c->merged = e;
+  st->stats.kernel_launches += 3;
   return st->unstage_output(&io, cs);
 }
 
@@ -311,12 +341,11 @@ ssa_status ssa_sharded_query(ssa_store_t st, ssa_session_t id, int32_t layer, in
   const int64_t rows = Lin * n_q;
   const size_t chunk = (size_t)rows * st->cfg.num_q_heads * (st->cfg.head_dim + 1);
   const size_t need = chunk * (1 + c->world);
-  if (need > c->cap) {
-    COMM_CUDA(st, cudaDeviceSynchronize());
-    if (c->buf) cudaFree(c->buf);
+  if (need > c->cap) {   // stream-ordered growth
+    if (c->buf) COMM_CUDA(st, cudaFreeAsync(c->buf, cs));
     c->buf = nullptr;
     c->cap = std::max(need, c->cap * 2);
-    COMM_CUDA(st, cudaMalloc(&c->buf, c->cap * sizeof(float)));
+    COMM_CUDA(st, cudaMallocAsync(reinterpret_cast<void**>(&c->buf), c->cap * sizeof(float), cs));
   }
   rc = ssa_sharded_partial(st, id, layer, n_q, Q, K, V, c->rank == c->world - 1, c->buf, stream);
   if (rc != SSA_OK) return rc;

@@ -278,23 +278,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
 // [O fp32 rows*Hq*D | lse rows*Hq] (log2 units), reading R-11.
 template <typename T>
 __global__ void __launch_bounds__(256) merge_ranks_kernel(const float* parts, int world, int64_t rows, int Hq, int D,
-                                                          T* O, const uint32_t* flags, uint32_t epoch) {
-  if (flags) {
-    // peer-memory path: wait until every rank released this epoch's chunk
-    if (threadIdx.x < world) {
-      uint32_t v;
-      uint64_t t0, t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      do {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        // a peer that never pushes (failed or absent rank): fail the launch
-        // loudly after 10 s instead of hanging the GPU
-        if (t - t0 > 10000000000ull) __trap();
-      } while ((int32_t)(v - epoch) < 0);
-    }
-    __syncthreads();
-  }
+                                                          T* O) {
   const int64_t rh = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (rh >= rows * Hq) return;
@@ -417,28 +401,55 @@ cudaError_t launch_simt_t(const AttnParams& p, int n_layers, cudaStream_t s) {
 int simt_rows_tile(int G, int D) { (void)G; (void)D; return kRT; }
 
 cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
-                               cudaStream_t s, const uint32_t* flags, uint32_t epoch) {
+                               cudaStream_t s) {
   const int64_t warps = rows * Hq;
   if (warps == 0) return cudaSuccess;
   const int blocks = (int)((warps + 7) / 8);
   if (bf16)
-    merge_ranks_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<__nv_bfloat16*>(O),
-                                                             flags, epoch);
+    merge_ranks_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<__nv_bfloat16*>(O));
   else
-    merge_ranks_kernel<float><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<float*>(O), flags, epoch);
+    merge_ranks_kernel<float><<<blocks, 256, 0, s>>>(parts, world, rows, Hq, D, static_cast<float*>(O));
   return cudaGetLastError();
 }
 
-__global__ void signal_peers_kernel(const uint64_t* peer_flags, int n_peers, int rank, uint32_t epoch) {
+// Peer-memory exchange flags (A9): one warp; lane q releases `epoch` into slot
+// `slot` of peer q's flag array (st.release.sys after a system-scope fence, so
+// the stores this stream issued before -- the pushed chunk, or the merge's reads
+// being done -- are ordered before the flag).
+__global__ void signal_peers_kernel(const uint64_t* peer_flags, int n_peers, int slot, uint32_t epoch) {
   const int q = threadIdx.x;
   if (q >= n_peers) return;
-  __threadfence_system();   // the pushed chunk (previous kernel on this stream) before the flag
-  uint32_t* f = reinterpret_cast<uint32_t*>(peer_flags[q]) + rank;
+  __threadfence_system();
+  uint32_t* f = reinterpret_cast<uint32_t*>(peer_flags[q]) + slot;
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
 }
 
-cudaError_t launch_signal_peers(const uint64_t* peer_flags, int n_peers, int rank, uint32_t epoch, cudaStream_t s) {
-  signal_peers_kernel<<<1, 32 * ((n_peers + 31) / 32), 0, s>>>(peer_flags, n_peers, rank, epoch);
+// One block waits (acquire, system scope) until flags[i] >= epoch for i < n: the
+// kernels after it on the stream run only once every peer has released.  A single
+// spinning block never starves the peers' kernels of SMs (virtual ranks on one
+// GPU); a peer that never signals fails the launch after 10 s instead of hanging.
+__global__ void wait_flags_kernel(const uint32_t* flags, int n, uint32_t epoch) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    uint32_t v;
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) __trap();
+    } while (true);
+  }
+}
+
+cudaError_t launch_signal_peers(const uint64_t* peer_flags, int n_peers, int slot, uint32_t epoch, cudaStream_t s) {
+  signal_peers_kernel<<<1, 32 * ((n_peers + 31) / 32), 0, s>>>(peer_flags, n_peers, slot, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const uint32_t* flags, int n, uint32_t epoch, cudaStream_t s) {
+  wait_flags_kernel<<<1, 32, 0, s>>>(flags, n, epoch);
   return cudaGetLastError();
 }
 int simt_key_tile() { return kBK; }

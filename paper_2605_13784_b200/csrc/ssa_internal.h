@@ -226,9 +226,11 @@ cudaError_t launch_greedy(const SampleParams& p, bool bf16, cudaStream_t s);
 size_t sample_partial_bytes();
 // Merge `world` rank partials (packed chunks [O fp32 rows*Hq*D | lse rows*Hq]) into O.
 cudaError_t launch_merge_ranks(const float* parts, int world, int64_t rows, int Hq, int D, void* O, bool bf16,
-                               cudaStream_t s, const uint32_t* flags = nullptr, uint32_t epoch = 0);
-// Release `epoch` into flag slot `rank` of every peer (after the stream's prior work).
-cudaError_t launch_signal_peers(const uint64_t* peer_flags, int n_peers, int rank, uint32_t epoch, cudaStream_t s);
+                               cudaStream_t s);
+// Release `epoch` into flag slot `slot` of every peer (after the stream's prior work).
+cudaError_t launch_signal_peers(const uint64_t* peer_flags, int n_peers, int slot, uint32_t epoch, cudaStream_t s);
+// One block waits until flags[i] >= epoch for i < n (acquire, system scope).
+cudaError_t launch_wait_flags(const uint32_t* flags, int n, uint32_t epoch, cudaStream_t s);
 int simt_rows_tile(int G, int D);     // rows per SIMT unit
 int simt_key_tile();                  // keys per SIMT tile
 

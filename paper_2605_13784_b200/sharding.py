@@ -71,21 +71,22 @@ def chunk_floats(n_q: int, num_layers: int, num_q_heads: int, head_dim: int) -> 
 
 
 def attach_symmetric(store, max_chunk_floats: int, group=None):
-    """Allocate the gathered buffer ([world][chunk]) and the flag array in torch symmetric
-    memory over `group`, exchange the peer addresses and attach them to `store`
-    (ssa_comm_attach_peers).  Returns the (buffer, flags) tensors, which must stay alive."""
+    """Allocate the gathered buffer ([2][world][chunk]: halves alternate by epoch) and the flag
+    array ([2][world]: ready, ack) in torch symmetric memory over `group`, exchange the peer
+    addresses and attach them to `store` (ssa_comm_attach_peers).  Returns the (buffer, flags)
+    tensors, which must stay alive."""
     import torch
     import torch.distributed as dist
     import torch.distributed._symmetric_memory as symm_mem
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = torch.device("cuda", torch.cuda.current_device())
-    buf = symm_mem.empty(world * max_chunk_floats, dtype=torch.float32, device=dev)
-    flags = symm_mem.empty(max(world, 4), dtype=torch.int32, device=dev)
+    buf = symm_mem.empty(2 * world * max_chunk_floats, dtype=torch.float32, device=dev)
+    flags = symm_mem.empty(max(2 * world, 4), dtype=torch.int32, device=dev)
     flags.zero_()
     gname = group.group_name if group is not None else dist.group.WORLD.group_name
     hb = symm_mem.rendezvous(buf, gname)
     hf = symm_mem.rendezvous(flags, gname)
     dist.barrier(group)
     store.comm_attach_peers(rank, world, list(hb.buffer_ptrs), list(hf.buffer_ptrs),
-                            world * max_chunk_floats * 4)
+                            2 * world * max_chunk_floats * 4)
     return buf, flags

@@ -17,7 +17,7 @@ def run(rank, world, bufs, flags, K, V, Qs, Ks, Vs, out_q, n, cfg):
     st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
     sid = st.session_create(None, dv(K[:, lo:hi]), dv(V[:, lo:hi]))
     st.comm_attach_peers(rank, world, [b.data_ptr() for b in bufs], [f.data_ptr() for f in flags],
-                         bufs[0].numel() * 4)
+                         bufs[0].numel() * 4)   # [2][world][chunk] floats
     outs = []
     for Qq, Kq, Vq in zip(Qs, Ks, Vs):
         O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=dev)

@@ -867,7 +867,8 @@ def test_greedy_sample_parity(cuda, dtype, rows, vocab, stride):
 def test_sharded_peer_push_virtual_ranks(cuda, world, nq):
     """A9 over peer memory, `world` virtual ranks on one GPU: each rank's combine epilogue stores
     its partial into every rank's gathered buffer and releases an epoch flag; every rank's merge
-    acquires the flags and merges.  Two rounds exercise the epoch protocol."""
+    acquires the flags and merges, then acks.  Two rounds on one stream exercise the epoch
+    protocol and the alternating buffer halves."""
     import torch
     from paper_2605_13784_b200.sharding import chunk_floats, shard_range
     ssa = _ssa()
@@ -878,15 +879,15 @@ def test_sharded_peer_push_virtual_ranks(cuda, world, nq):
     ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
     rsid, _ = ref.session_create(n, Q, K, V, compute=False)
     ch = chunk_floats(nq, L, hq, d)
-    bufs = [torch.zeros(world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
-    flags = [torch.zeros(max(world, 4), dtype=torch.int32, device=cuda) for _ in range(world)]
+    bufs = [torch.zeros(2 * world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
+    flags = [torch.zeros(2 * world, dtype=torch.int32, device=cuda) for _ in range(world)]
     stores, sids = [], []
     for r in range(world):
         lo, hi = shard_range(n, r, world)
         st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
         sids.append(st.session_create(None, to_dev(K[:, lo:hi], cuda), to_dev(V[:, lo:hi], cuda)))
         st.comm_attach_peers(r, world, [b.data_ptr() for b in bufs], [f.data_ptr() for f in flags],
-                             world * ch * 4)
+                             2 * world * ch * 4)
         stores.append(st)
     for rnd in range(2):
         Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1 + rnd, 0, nq)
@@ -899,7 +900,62 @@ def test_sharded_peer_push_virtual_ranks(cuda, world, nq):
             ok, e = within(from_dev(O), want, "bf16")
             assert ok, (rnd, r, e)
         torch.cuda.synchronize()
-        assert all(int(f[r].item()) == rnd + 1 for f in flags for r in range(world))
+        assert all(int(f[q].item()) == rnd + 1 for f in flags for q in range(2 * world))   # ready + ack
+    with pytest.raises(ssa.SsaError, match="STATE"):   # a merge needs a pushed epoch
+        stores[0].sharded_merge(torch.empty(Qq.shape, dtype=torch.bfloat16, device=cuda))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_peer_push_pipelined_rounds(cuda, world):
+    """The peer-memory exchange under back-to-back per-layer rounds with no cross-rank
+    synchronisation: `world` virtual ranks on one GPU, each on its own stream, run 64 rounds of
+    push + merge (single-layer sharded queries, cycling layers and query inputs) before the one
+    host sync at the end.  Without the per-half acks a fast rank would overwrite a half a slow
+    rank's merge is still reading.  Every round of every rank must equal the oracle."""
+    import torch
+    from paper_2605_13784_b200.sharding import chunk_floats, shard_range
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    n, nq, rounds = 3001, 32, 64
+    spec = streams.StreamSpec("market", seed=43)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    inputs = [gen_qkv(spec, L, hq, hkv, d, 1 + i, 0, nq) for i in range(4)]
+    wants = [ref.session_query(rsid, *x) for x in inputs]
+    dev_in = [tuple(to_dev(a, cuda) for a in x) for x in inputs]
+    ch = chunk_floats(nq, 1, hq, d)
+    bufs = [torch.zeros(2 * world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
+    flags = [torch.zeros(2 * world, dtype=torch.int32, device=cuda) for _ in range(world)]
+    stores, sids, streams_ = [], [], []
+    for r in range(world):
+        lo, hi = shard_range(n, r, world)
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
+        sids.append(st.session_create(None, to_dev(K[:, lo:hi], cuda), to_dev(V[:, lo:hi], cuda)))
+        st.comm_attach_peers(r, world, [b.data_ptr() for b in bufs], [f.data_ptr() for f in flags],
+                             2 * world * ch * 4)
+        stores.append(st)
+        streams_.append(torch.cuda.Stream())
+    torch.cuda.synchronize()
+    outs = [[torch.empty((1, nq, hq, d), dtype=torch.bfloat16, device=cuda) for _ in range(rounds)]
+            for _ in range(world)]
+    for rnd in range(rounds):
+        i, l = rnd % 4, rnd % L
+        Qd, Kd, Vd = dev_in[i]
+        # rank order rotates so no rank is always first
+        for r in [(rnd + j) % world for j in range(world)]:
+            s = streams_[r]
+            stores[r].sharded_push(sids[r], Qd[l:l + 1], Kd[l:l + 1], Vd[l:l + 1], layer=l, stream=s)
+            stores[r].sharded_merge(outs[r][rnd], layer=l, stream=s)
+    torch.cuda.synchronize()
+    for rnd in range(rounds):
+        i, l = rnd % 4, rnd % L
+        for r in range(world):
+            ok, e = within(from_dev(outs[r][rnd]), wants[i][l:l + 1], "bf16")
+            assert ok, (rnd, r, e)
+            assert torch.equal(outs[r][rnd].view(torch.int16), outs[0][rnd].view(torch.int16))
+    for st in stores:
+        st.close()
 
 
 def test_sharded_symmetric_memory_world1(cuda):
@@ -950,8 +1006,8 @@ def test_sharded_peer_push_two_processes(cuda):
     Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
     qs = [gen_qkv(spec, L, hq, hkv, d, 1 + r, 0, 32) for r in range(3)]
     ch = chunk_floats(32, L, hq, d)
-    bufs = [torch.zeros(world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
-    flags = [torch.zeros(4, dtype=torch.int32, device=cuda) for _ in range(world)]
+    bufs = [torch.zeros(2 * world * ch, dtype=torch.float32, device=cuda) for _ in range(world)]
+    flags = [torch.zeros(2 * world, dtype=torch.int32, device=cuda) for _ in range(world)]
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     procs = [ctx.Process(target=p2p_worker.run,
@@ -971,7 +1027,7 @@ def test_sharded_peer_push_two_processes(cuda):
         for r in range(world):
             ok, e = within(results[r][i], want, "bf16")
             assert ok, (r, i, e)
-    assert all(int(f[r].item()) == 3 for f in flags for r in range(world))
+    assert all(int(f[q].item()) == 3 for f in flags for q in range(2 * world))   # ready + ack
 
 
 @pytest.mark.parametrize("kv", [None, "e4m3"])
@@ -1083,3 +1139,36 @@ def test_borrowed_pool_from_torch(cuda):
         ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64, pool=torch.zeros(nb // 2, dtype=torch.uint8, device=cuda))
     with pytest.raises(ssa.SsaError, match="INVALID_ARG"):
         ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64, pool=torch.zeros(nb, dtype=torch.uint8))
+
+
+def test_two_devices_in_one_process():
+    """Two stores on two devices of one process (per-device kernel attributes, per-device
+    plans): each runs its own session, and a sharded query over NCCL (world 2, one process,
+    ncclCommInitRank per device) equals the oracle.  Needs 2 GPUs."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    ssa = _ssa()
+    L, hq, hkv, d, P = 2, 32, 8, 128, 64
+    spec = streams.StreamSpec("market", seed=45)
+    n = 2000
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, 32)
+    want = ref.session_query(rsid, Qq, Kq, Vq)
+    for dev in (0, 1):
+        cd = torch.device("cuda", dev)
+        st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64, device=dev)
+        sid = st.session_create(None, to_dev(K, cd), to_dev(V, cd))
+        O = torch.empty(Qq.shape, dtype=torch.bfloat16, device=cd)
+        st.session_query(sid, to_dev(Qq, cd), to_dev(Kq, cd), to_dev(Vq, cd), O)
+        ok, e = within(from_dev(O), want, "bf16")
+        assert ok, (dev, e)
+        for l in range(L):   # single-layer calls: cluster-merge launches on this device
+            Ol = torch.empty((1, 32, hq, d), dtype=torch.bfloat16, device=cd)
+            st.session_query(sid, to_dev(Qq[l:l + 1], cd), to_dev(Kq[l:l + 1], cd), to_dev(Vq[l:l + 1], cd), Ol,
+                             layer=l)
+            ok, e = within(from_dev(Ol), want[l:l + 1], "bf16")
+            assert ok, (dev, l, e)
+        st.close()
