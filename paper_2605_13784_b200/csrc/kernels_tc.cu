@@ -79,8 +79,6 @@ struct Bars {
   uint64_t p_full[2];
   uint64_t o_final[2];
   uint32_t tmem_base;
-  int32_t pwin_base[2][2];        // page-id windows of the TMA producers: [K / V producer][slot] first entry
-  alignas(16) int32_t pwin[2][2][32];         // entries [base, base + 32) of the slot's page table
 };
 
 struct TcMaps {
@@ -225,26 +223,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define SSA_POLY_PAIRS_OF_8 0
 #endif
 constexpr int kPolyPairsOf8 = SSA_POLY_PAIRS_OF_8;
-
-// Page id of entry `pi` of a segment's page table, through a 32-entry window in
-// shared memory owned by one producer thread and refilled with 16-byte loads
-// when `pi` leaves it: one load latency per 32 pages instead of one per TMA box.
-__device__ __forceinline__ int32_t page_window(int32_t& base, int32_t* win, const SegDesc& sg, int pi) {
-  if (pi < base || pi >= base + 32) {
-    base = pi & ~3;
-    const int n = min(32, sg.n_pages - base);
-    const int4* src = reinterpret_cast<const int4*>(sg.pages + base);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (4 * i + 3 < n) {
-        *reinterpret_cast<int4*>(win + 4 * i) = __ldg(src + i);
-      } else {
-        for (int j = 4 * i; j < n && j < 4 * i + 4; ++j) win[j] = __ldg(sg.pages + base + j);
-      }
-    }
-  }
-  return win[pi - base];
-}
 
 // ---------------------------------------------------------------- cluster merge (CM)
 // CM launches (AttnParams::cm_C = C >= 1): every unit belongs to a split group and
@@ -516,57 +494,79 @@ __device__ __forceinline__ void cm_reduce(const AttnParams& p, const WorkUnit& w
 // Groups spread over K > 1 clusters: merge the K block partials of every row
 // (log-sum-exp, R-11) -- a small grid launched right behind the attention
 // kernel (programmatic dependent launch: its prologue overlaps the attention
-// kernel's tail).  Block b of layer y: group b / 32, rows 4 (b % 32) .. +4, one
-// row per warp, lane l columns [4l, 4l+4) (coalesced 512-byte rows); the K
-// partials are read 8 at a time with an online rescale (one pass).
+// kernel's tail).  Block b of layer y: group b / (32 / RW), rows 4 RW (b % (32 /
+// RW)) .. +4 RW; warp wq takes RW of them (rows +wq, +wq+4, ...), lane l columns
+// [4l, 4l+4) (coalesced 512-byte rows); loads of RW rows x 4 partials are in
+// flight at once, with an online rescale over the partials.  RW = 8 (few CTAs, so
+// most SMs stay free for the next grid's CTAs) for up to 8 partials, else 1.
+template <int RW>
 __global__ void __launch_bounds__(128) cm_merge_kernel(const AttnParams p) {
   griddep_launch_dependents();
-  const int g = blockIdx.x >> 5;
+  constexpr int kBlocksPerGroup = 32 / RW;
+  const int g = blockIdx.x / kBlocksPerGroup;
   const Group gr = p.groups[g];
   const int K = gr.n_splits;
   const int G = p.G;
-  const int row = (blockIdx.x & 31) * 4 + (threadIdx.x >> 5);
+  const int rows = gr.q_ntok * G;
+  const int r0 = (blockIdx.x % kBlocksPerGroup) * 4 * RW + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int ly = blockIdx.y;
   const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
   const SegDesc sg = p.segs[gr.seg];
   griddep_wait();   // the attention grid's partials
-  if (K <= 1 || row >= gr.q_ntok * G) return;
-  constexpr int B = 8;
-  float m = -CUDART_INF_F, wsum = 0.f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j0 = 0; j0 < K; j0 += B) {
-    float l[B];
-    float4 v[B];
+  if (K <= 1 || r0 >= rows) return;
+  constexpr int B = 4;
+  float m[RW], wsum[RW];
+  float4 acc[RW];
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const int j = min(j0 + b, K - 1);
-      l[b] = j0 + b < K ? __ldcg(p.part_lse + (s0 + j) * kM + row) : -CUDART_INF_F;
-      v[b] = __ldcg(reinterpret_cast<const float4*>(p.part_o + ((s0 + j) * kM + row) * kD) + lane);
-    }
-    float mb = m;
-#pragma unroll
-    for (int b = 0; b < B; ++b) mb = fmaxf(mb, l[b]);
-    if (mb == -CUDART_INF_F) continue;
-    const float sc = m == -CUDART_INF_F ? 0.f : exp2f(m - mb);
-    wsum *= sc;
-    acc = make_float4(acc.x * sc, acc.y * sc, acc.z * sc, acc.w * sc);
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const float wt = l[b] == -CUDART_INF_F ? 0.f : exp2f(l[b] - mb);
-      wsum += wt;
-      acc.x = fmaf(wt, v[b].x, acc.x);
-      acc.y = fmaf(wt, v[b].y, acc.y);
-      acc.z = fmaf(wt, v[b].z, acc.z);
-      acc.w = fmaf(wt, v[b].w, acc.w);
-    }
-    m = mb;
+  for (int b = 0; b < RW; ++b) {
+    m[b] = -CUDART_INF_F;
+    wsum[b] = 0.f;
+    acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  for (int j0 = 0; j0 < K; j0 += B) {
+    float l[RW][B];
+    float4 v[RW][B];
+#pragma unroll
+    for (int b = 0; b < RW; ++b)
+#pragma unroll
+      for (int jj = 0; jj < B; ++jj) {
+        const int row = min(r0 + 4 * b, rows - 1);
+        const int j = min(j0 + jj, K - 1);
+        l[b][jj] = j0 + jj < K ? __ldcg(p.part_lse + (s0 + j) * kM + row) : -CUDART_INF_F;
+        v[b][jj] = __ldcg(reinterpret_cast<const float4*>(p.part_o + ((s0 + j) * kM + row) * kD) + lane);
+      }
+#pragma unroll
+    for (int b = 0; b < RW; ++b) {
+      float mb = m[b];
+#pragma unroll
+      for (int jj = 0; jj < B; ++jj) mb = fmaxf(mb, l[b][jj]);
+      if (mb == -CUDART_INF_F) continue;
+      const float sc = m[b] == -CUDART_INF_F ? 0.f : exp2f(m[b] - mb);
+      wsum[b] *= sc;
+      acc[b] = make_float4(acc[b].x * sc, acc[b].y * sc, acc[b].z * sc, acc[b].w * sc);
+#pragma unroll
+      for (int jj = 0; jj < B; ++jj) {
+        const float wt = l[b][jj] == -CUDART_INF_F ? 0.f : exp2f(l[b][jj] - mb);
+        wsum[b] += wt;
+        acc[b].x = fmaf(wt, v[b][jj].x, acc[b].x);
+        acc[b].y = fmaf(wt, v[b][jj].y, acc[b].y);
+        acc[b].z = fmaf(wt, v[b][jj].z, acc[b].z);
+        acc[b].w = fmaf(wt, v[b][jj].w, acc[b].w);
+      }
+      m[b] = mb;
+    }
+  }
   const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
-  const int64_t orow = in_l + sg.row0 + gr.q_tok0 + row / G;
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + gr.kv_head * G + row % G) * kD + 4 * lane;
-  store_bf16x4(out, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+#pragma unroll
+  for (int b = 0; b < RW; ++b) {
+    const int row = r0 + 4 * b;
+    if (row >= rows) break;
+    const float inv = wsum[b] > 0.f ? 1.f / wsum[b] : 0.f;
+    const int64_t orow = in_l + sg.row0 + gr.q_tok0 + row / G;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + gr.kv_head * G + row % G) * kD + 4 * lane;
+    store_bf16x4(out, make_float4(acc[b].x * inv, acc[b].y * inv, acc[b].z * inv, acc[b].w * inv));
+  }
 }
 
 // D[tmem] (+)= A[tmem] * B[smem desc]  (A = P, K-major in TMEM).
@@ -708,19 +708,17 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const int64_t head_base = (int64_t)(p.layer0 + ly) * p.num_pages;
         const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
         const bool is_k = F8 ? lane == 0 : warp == 0;
-        const int pw = is_k ? 0 : 1;
         const uint64_t pol = l2_policy_evict_first();
-        // Page ids of both slots' first tiles (a 16-byte-load window per slot) before
-        // waiting for the previous grid: page tables are written only by copies, which a
-        // programmatic launch never overlaps.
-        for (int k = 0; k < 2; ++k) {
-          bar.pwin_base[pw][k] = -(1 << 30);
-          const WorkUnit& w = k ? w1 : w0;
-          if (k == 1 && pr.ub < 0) continue;
-          const SegDesc sg = p.segs[w.seg];
-          if (w.tile_hi > w.tile_lo && w.tile_lo * kBN < sg.n_slots)
-            (void)page_window(bar.pwin_base[pw][k], bar.pwin[pw][k], sg, (w.tile_lo * kBN) / p.P);
-        }
+        // With a programmatic launch, warm L1 with both slots' first page-table entries
+        // before waiting for the previous grid (page tables are written only by copies,
+        // which a programmatic launch never overlaps).
+        if (p.pool_early)
+          for (int k = 0; k < (pr.ub >= 0 ? 2 : 1); ++k) {
+            const WorkUnit& w = k ? w1 : w0;
+            const SegDesc sg = p.segs[w.seg];
+            if (w.tile_hi > w.tile_lo && w.tile_lo * kBN < sg.n_slots)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(sg.pages + (w.tile_lo * kBN) / p.P));
+          }
         const int E = nt0 + nt1 - nsh;
         const int m01 = min(nt0, nt1) - nsh;
         const int NR = is_k ? NK : NV;
@@ -755,7 +753,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
               const int slot = key0 + b * box_rows;
               int32_t row = 0x7FFFFFF0;   // past the tensor -> TMA zero fill
               if (slot < sg.n_slots) {
-                const int64_t page = page_window(bar.pwin_base[pw][k], bar.pwin[pw][k], sg, slot / p.P);
+                const int64_t page = __ldg(sg.pages + slot / p.P);
                 row = (int32_t)(((head_base + page) * p.Hkv + w.kv_head) * p.P + (slot % p.P));
               }
               for (int c = 0; c < nchunk; ++c) {
@@ -1250,9 +1248,10 @@ cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, bool pdl, cudaStre
   return cudaLaunchKernelEx(&cfg, kern, p, maps, box_rows);
 }
 
-cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s) {
+cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, int max_split, bool pdl, cudaStream_t s) {
+  const int rw = max_split <= 8 ? 8 : 1;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.n_groups * 32, n_layers, 1);
+  cfg.gridDim = dim3(p.n_groups * (32 / rw), n_layers, 1);
   cfg.blockDim = dim3(128, 1, 1);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1260,7 +1259,7 @@ cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, bool pdl, cudaStr
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, cm_merge_kernel, p);
+  return rw == 8 ? cudaLaunchKernelEx(&cfg, cm_merge_kernel<8>, p) : cudaLaunchKernelEx(&cfg, cm_merge_kernel<1>, p);
 }
 
 size_t tc_smem_bytes() { return (size_t)kNumSlots * kSlotBytes + sizeof(Bars) + 1024; }

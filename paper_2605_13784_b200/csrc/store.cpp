@@ -783,7 +783,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     ap.cm_C = E.cm_C;
     // pool tiles may be prefetched before griddepcontrol.wait unless the grid right
     // before this one on the stream is one of the store's pool writers
-    ap.pool_early = (opt_pdl != 0 && !(pool_writer_last && last_kernel_stream == st)) ? 1 : 0;
+    ap.pool_early = (opt_pdl != 0 && !opt_timing && !(pool_writer_last && last_kernel_stream == st)) ? 1 : 0;
     ap.l2_evict_first = opt_l2_hint == 2 || (opt_l2_hint == 0 && E.l2_hint) ? 1 : 0;
     const bool merge_in_kernel = E.cm_C > 0 && E.max_split > 1 && opt_cm_merge == 0;
     if (merge_in_kernel) {
@@ -811,7 +811,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     note_kernel(st, false);
     if (E.cm_C > 0 && E.max_split > 1 && !merge_in_kernel) {   // groups over several clusters: merge kernel
       cudaEvent_t t1 = tick(st);
-      SSA_CUDA(this, launch_cm_merge(ap, n_layers, opt_pdl != 0 && !t1, st));
+      SSA_CUDA(this, launch_cm_merge(ap, n_layers, E.max_split, opt_pdl != 0 && !t1, st));
       if (t1) timed_push(query_plane ? 3 : 2, t1, tick(st));
       stats.kernel_launches++;
     }

@@ -71,7 +71,7 @@ int tc_debug_trace(void* host, size_t bytes);
 int tc_rows_tile();
 cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s);
 size_t tc_smem_bytes();
-cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s);
+cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, int max_split, bool pdl, cudaStream_t s);
 cudaError_t tc_configure(bool f8);
 int tc_max_active_clusters(int c, bool f8);
 bool tc_supported_shape(int D, int G, bool bf16);

@@ -31,8 +31,14 @@ def step():
     st.session_truncate(sid, n0)
 
 
-settings = [dict(), {ssa.OPT_L2_HINT: 1}, {ssa.OPT_L2_HINT: 2}, {ssa.OPT_PDL: 0}, {ssa.OPT_PDL: 0, ssa.OPT_L2_HINT: 1}]
-for rep in range(2):
+if os.environ.get("AB_SET"):   # e.g. AB_SET=14:1,10:0 -> one setting
+    settings = [{int(k): int(v) for k, v in (kv.split(":") for kv in os.environ["AB_SET"].split(","))}]
+    os.environ["AB_ONLY_DEFAULT"] = "1"
+elif os.environ.get("AB_ONLY_DEFAULT"):
+    settings = [dict()]
+else:
+    settings = [dict(), {ssa.OPT_L2_HINT: 1}, {ssa.OPT_L2_HINT: 2}, {ssa.OPT_PDL: 0}, {ssa.OPT_PDL: 0, ssa.OPT_L2_HINT: 1}]
+for rep in range(1 if os.environ.get("AB_ONLY_DEFAULT") else int(os.environ.get("AB_REPS", "2"))):
     for opts in settings:
         for k, v in opts.items():
             st.set_option(k, v)
@@ -53,4 +59,4 @@ for rep in range(2):
               f"query attn {qa * 1e3:.1f} us ({bench.query_bytes_per_layer(C['n_ctx'], C['q_len'], C['hq'], C['hkv'], C['d']) * L / (qa * 1e-3) / 1e9:.0f} GB/s)",
               flush=True)
         for k in opts:
-            st.set_option(k, {ssa.OPT_PDL: 1, ssa.OPT_L2_HINT: 0}.get(k, 0))
+            st.set_option(k, {getattr(ssa, "OPT_PDL", -1): 1, getattr(ssa, "OPT_L2_HINT", -1): 0}.get(k, 0))
