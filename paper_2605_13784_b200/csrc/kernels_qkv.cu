@@ -409,10 +409,6 @@ static bool qkv_exchange_fits(int m, int s) {
 }
 
 int qkv_choose_splits(int m, int n_heads, int hidden, int num_sms) {
-  if (const char* e = getenv("SSA_QKV_SPLITS")) {   // experiments only
-    const int f = atoi(e);
-    if (f >= 1 && f <= kMaxSplits && f <= hidden / kBK && qkv_exchange_fits(m, f)) return f;
-  }
   // the most CTAs (tiles x S) whose clusters are all co-resident (one wave);
   // S = 1 when even that does not fit
   const int tiles = ((n_heads * kHeadD + kBN - 1) / kBN) * ((m + kBM - 1) / kBM);
@@ -477,13 +473,9 @@ cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s) {
     if (!encode_bf16_map(&maps.w, p.W, 2, dims, str, box)) return cudaErrorInvalidValue;
   }
   const size_t smem = qkv_smem_bytes();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(qkv_rope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(qkv_rope_kernel), (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(qkv_rope_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    (void)e;
-    configured = true;
   }
   const int n_tiles_n = (n_heads * kHeadD + kBN - 1) / kBN;
   const int n_tiles_m = (p.m + kBM - 1) / kBM;

@@ -29,6 +29,21 @@ __device__ __forceinline__ float ld_f(const __nv_bfloat16* p, int64_t i) { retur
 __device__ __forceinline__ void st_f(float* p, int64_t i, float v) { p[i] = v; }
 __device__ __forceinline__ void st_f(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
 
+// 16-byte vector load of VEC = 16 / sizeof(T) consecutive elements, as floats.
+__device__ __forceinline__ void ld_vec16(const float* p, int64_t i, float (&out)[4]) {
+  const float4 x = __ldg(reinterpret_cast<const float4*>(p + i));
+  out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
+}
+__device__ __forceinline__ void ld_vec16(const __nv_bfloat16* p, int64_t i, float (&out)[8]) {
+  const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + i));
+  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    out[2 * k] = __uint_as_float(w[k] << 16);
+    out[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+  }
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -67,15 +82,19 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
   const T* PK = static_cast<const T*>(p.poolK);
   const T* PV = static_cast<const T*>(p.poolV);
 
-  for (int idx = tid; idx < kRT * D; idx += kThreads) {
-    const int r = idx / D, e = idx % D;
-    float v = 0.f;
+  constexpr int VEC = 16 / sizeof(T);           // elements per 16-byte load
+  for (int idx = tid; idx < kRT * D / VEC; idx += kThreads) {
+    const int r = idx * VEC / D, e = idx * VEC % D;
+    float v[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) v[c] = 0.f;
     if (r < rows) {
       const int64_t row = in_row0 + wu.q_tok0 + r / G;
       const int h = wu.kv_head * G + r % G;
-      v = ld_f(Q, (row * p.Hq + h) * D + e) * p.scale_log2;
+      ld_vec16(Q, (row * p.Hq + h) * D + e, v);
     }
-    Qs[idx] = v;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) Qs[r * D + e + c] = v[c] * p.scale_log2;
   }
   if (tid < kRT) { mrow[tid] = -CUDART_INF_F; lrow[tid] = 0.f; }
   float acc[NV];
@@ -87,24 +106,29 @@ __global__ void __launch_bounds__(kThreads) attn_simt_kernel(const AttnParams p)
     const bool is_pool = tile < n_pool_tiles;
     const int key0 = (is_pool ? tile : tile - n_pool_tiles) * kBK;
     __syncthreads();
-    for (int idx = tid; idx < kBK * D; idx += kThreads) {
-      const int j = idx / D, e = idx % D;
-      float kv = 0.f, vv = 0.f;
+    for (int idx = tid; idx < kBK * D / VEC; idx += kThreads) {   // 16-byte loads
+      const int j = idx * VEC / D, e = idx * VEC % D;
+      float kv[VEC], vv[VEC];
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) kv[c] = vv[c] = 0.f;
       const int key = key0 + j;
       if (is_pool) {
         if (key < sg.n_slots && !(key >= sg.hole_lo && key < sg.hole_hi)) {
           const int64_t page = sg.pages[key / p.P];
           const int64_t off = (((layer * p.num_pages + page) * p.Hkv + wu.kv_head) * p.P + key % p.P) * D + e;
-          kv = ld_f(PK, off);
-          vv = ld_f(PV, off);
+          ld_vec16(PK, off, kv);
+          ld_vec16(PV, off, vv);
         }
       } else if (key < sg.tail_m) {
         const int64_t off = ((in_row0 + key) * p.Hkv + wu.kv_head) * D + e;
-        kv = ld_f(Kt, off);
-        vv = ld_f(Vt, off);
+        ld_vec16(Kt, off, kv);
+        ld_vec16(Vt, off, vv);
       }
-      Ks[j * KS + e] = kv;
-      Vs[j * D + e] = vv;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        Ks[j * KS + e + c] = kv[c];
+        Vs[j * D + e + c] = vv[c];
+      }
     }
     __syncthreads();
     for (int idx = tid; idx < kRT * kBK; idx += kThreads) {
@@ -385,12 +409,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherParams p) {
 template <typename T, int D>
 cudaError_t launch_simt_t(const AttnParams& p, int n_layers, cudaStream_t s) {
   const size_t smem = sizeof(float) * (kRT * D + kBK * (D + 1) + kBK * D + kRT * kBK + 3 * kRT);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_simt_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(attn_simt_kernel<T, D>), (int)smem);
+  if (e != cudaSuccess) return e;
   dim3 grid(p.n_units, n_layers);
   attn_simt_kernel<T, D><<<grid, kThreads, smem, s>>>(p);
   return cudaGetLastError();

@@ -190,6 +190,11 @@ struct SampleParams {
   int32_t* out_n_accept;   // device, used when draft != null
 };
 
+// cudaFuncSetAttribute(func, MaxDynamicSharedMemorySize, bytes) once per (device,
+// function): the attribute is per device, so a process with stores on several
+// devices sets it on each (store.cpp; thread-safe).
+cudaError_t set_smem_attr_once(const void* func, int bytes);
+
 // Kernel launchers (kernels_*.cu).  Return cudaGetLastError() after launch.
 // Fused data-plane projection (kernels_qkv.cu).
 struct QkvParams {
