@@ -1,6 +1,8 @@
 """Small, fast pass over every kernel of libssa for compute-sanitizer:
 SIMT fp32 (toy config), tcgen05 bf16 append / query / flash / batch, E4M3 store, scatter /
-gather / digest, retention + alias page copy, split-KV partials + merge, greedy sampling,
+gather / digest, retention + alias page copy, split-KV partials + merge, the peer-memory
+exchange over two rounds, single-layer cluster-merge launches (DSMEM reduce, merge kernel,
+in-kernel last-arriver merge, clusters of 1-8) and per-layer appends, greedy sampling,
 fused projection.  Exits non-zero on a parity failure against the fp64 oracle.
     compute-sanitizer --tool memcheck python tests/sanitize_run.py"""
 import os
@@ -112,6 +114,61 @@ stores[0].merge_rank_partials(2, 32, parts, Om)
 check("rank merge", from_dev(Om), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
 for s2 in stores:
     s2.close()
+
+# peer-memory exchange, two virtual ranks on one stream, two rounds (halves + acks)
+from paper_2605_13784_b200.sharding import chunk_floats  # noqa: E402
+ch = chunk_floats(32, L, hq, d)
+bufs = [torch.zeros(2 * 2 * ch, dtype=torch.float32, device=dev) for _ in range(2)]
+flags = [torch.zeros(4, dtype=torch.int32, device=dev) for _ in range(2)]
+stores, sids = [], []
+for r in range(2):
+    lo, hi = shard_range(n, r, 2)
+    s2 = ssa.Store(L, hq, hkv, d, page_size=64, num_pages=64)
+    sids.append(s2.session_create(None, to_dev(K[:, lo:hi], dev), to_dev(V[:, lo:hi], dev)))
+    s2.comm_attach_peers(r, 2, [b.data_ptr() for b in bufs], [f.data_ptr() for f in flags], 2 * 2 * ch * 4)
+    stores.append(s2)
+for rnd in range(3):
+    for r in range(2):
+        stores[r].sharded_push(sids[r], to_dev(Qq, dev), to_dev(Kq, dev), to_dev(Vq, dev))
+    for r in range(2):
+        Om = torch.empty(Qq.shape, dtype=torch.bfloat16, device=dev)
+        stores[r].sharded_merge(Om)
+        check(f"peer exchange round {rnd} rank {r}", from_dev(Om), ref.session_query(rsid, Qq, Kq, Vq), "bf16")
+for s2 in stores:
+    s2.close()
+
+# single-layer cluster-merge launches: C = 1..8 (DSMEM reduce), merge kernel / in-kernel merge
+for kv in (None, "e4m3"):
+    kw = dict(kv_format="e4m3", k_scale=1 / 16, v_scale=1 / 32) if kv else {}
+    L, hq, hkv, d, n = 2, 32, 8, 128, 3000
+    st = ssa.Store(L, hq, hkv, d, page_size=64, num_pages=64, **kw)
+    ref = oracle.OracleStore(L, hq, hkv, d, page_size=64, num_pages=64, **kw)
+    Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
+    sid = st.session_create(None, to_dev(K, dev), to_dev(V, dev))
+    rsid, _ = ref.session_create(n, Q, K, V, compute=False)
+    for nq in (1, 32):
+        Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, nq)
+        want = ref.session_query(rsid, Qq, Kq, Vq)
+        for C, merge in ((1, 1), (2, 1), (2, 0), (4, 1), (8, 1)):
+            st.set_option(ssa.OPT_CLUSTER, C)
+            st.set_option(ssa.OPT_CM_MERGE, merge)
+            Ol = torch.empty(Qq.shape, dtype=torch.bfloat16, device=dev)
+            for l in range(L):
+                st.session_query(sid, to_dev(Qq[l:l + 1], dev), to_dev(Kq[l:l + 1], dev), to_dev(Vq[l:l + 1], dev),
+                                 Ol[l:l + 1], layer=l)
+            check(f"{kv or 'bf16'} per-layer query {nq} C={C} merge={merge} plan={st.last_plan()}", from_dev(Ol), want,
+                  "bf16")
+    st.set_option(ssa.OPT_CLUSTER, 4)
+    Qa, Ka, Va = gen_qkv(spec, L, hq, hkv, d, 0, n, 200)
+    Oa = torch.empty(Qa.shape, dtype=torch.bfloat16, device=dev)
+    t = st.append_begin(sid, 200)
+    for l in range(L):
+        st.append_layer(sid, t, l, to_dev(Qa[l:l + 1], dev), to_dev(Ka[l:l + 1], dev), to_dev(Va[l:l + 1], dev),
+                        Oa[l:l + 1])
+    st.append_commit(sid, t)
+    wa, _ = ref.session_append(rsid, Qa, Ka, Va)
+    check(f"{kv or 'bf16'} per-layer append", from_dev(Oa), wa, "bf16")
+    st.close()
 
 # greedy sampling + fused projection
 st = ssa.Store(1, 8, 2, 128, page_size=64, num_pages=16)
