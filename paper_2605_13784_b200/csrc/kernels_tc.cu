@@ -239,12 +239,25 @@ constexpr int kXStride = 132;                 // fp32 row stride: 16-B aligned, 
 constexpr int kXFloats = kM * kXStride + kM;   // rows + lse
 
 // Barrier over every thread of the cluster (C > 1) or of the CTA (named barrier
-// 4; callers sit at different points of the warp-role branches).
+// 4; callers sit at different points of the warp-role branches, so the CTA
+// barriers are the non-.aligned `barrier.sync` / `barrier.arrive` forms).
 __device__ __forceinline__ void cm_sync(int C) {
+  __syncwarp();   // converged warps at the (non-.aligned) CTA barrier / the .aligned cluster barrier
   if (C > 1)
     cluster_sync_all();
   else
-    asm volatile("bar.sync 4, %0;" ::"n"(kThreads) : "memory");
+    asm volatile("barrier.sync 4, %0;" ::"n"(kThreads) : "memory");
+}
+// Named barrier 5 orders the end of every warp-0..3 role (TMA issue, E4M3
+// conversion writes into the ring) before the epilogue writes its exchange rows
+// into the same ring shared memory: warps 0-3 arrive, the softmax warps wait.
+__device__ __forceinline__ void ring_free_arrive() {
+  __syncwarp();
+  asm volatile("barrier.arrive 5, %0;" ::"n"(kThreads) : "memory");
+}
+__device__ __forceinline__ void ring_free_wait() {
+  __syncwarp();
+  asm volatile("barrier.sync 5, %0;" ::"n"(kThreads) : "memory");
 }
 
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t a) {
@@ -424,7 +437,7 @@ __device__ __forceinline__ void cm_reduce(const AttnParams& p, const WorkUnit& w
     // In-kernel variant of cm_merge_kernel: the last of the K clusters' rank-r CTAs to
     // arrive (atomic ticket, no spin waits) merges the K block partials of block r.
     __threadfence();
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
+    asm volatile("barrier.sync %0, 128;" ::"r"(1 + k) : "memory");
     __shared__ uint32_t last[2];
     if (t == 0) {
       int* cnt = p.cm_tickets + ((int64_t)ly * p.n_groups + w.group) * C + rank;
@@ -432,7 +445,7 @@ __device__ __forceinline__ void cm_reduce(const AttnParams& p, const WorkUnit& w
       last[k] = old == K - 1 ? 1u : 0u;
       if (old == K - 1) *cnt = 0;   // every arrival is in: ready for the next launch
     }
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + k) : "memory");
+    asm volatile("barrier.sync %0, 128;" ::"r"(1 + k) : "memory");
     GTRACE_T(true, 11);
     if (last[k]) {
       __threadfence();
@@ -633,6 +646,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   // epilogue writes O straight from the slots, no exchange buffer / reduce
   const bool cm_direct = p.cm_C == 1 && p.groups[w0.group].n_splits == 1 &&
                          (pr.ub < 0 || p.groups[w1.group].n_splits == 1);
+  // the epilogue stages rows in the ring (exchange buffer, or a split pair's slot merge)
+  const bool ring_stage = p.cm_C > 0 && (!cm_direct || (pr.same_q && pr.ub >= 0));
   const int NK = 3;
   const int NV = two_q ? 2 : 3;
   uint8_t* q_buf[2] = {tiles, two_q ? tiles + kSlotBytes : tiles};
@@ -860,6 +875,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         }
       }
     }
+    if (ring_stage) ring_free_arrive();
     if (p.cm_C > 0 && !cm_direct) {   // the two cluster barriers of the CM epilogue
       cm_sync(p.cm_C);
       cm_sync(p.cm_C);
@@ -1025,12 +1041,13 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         const int nt_o = k ? nt0 : nt1;
         if (pr.ub >= 0 && nt_o > 0) mbar_wait(&bar.o_final[k ^ 1], 0);
         tc_fence_after();
+        if (ring_stage) ring_free_wait();
         float* X0 = reinterpret_cast<float*>(k_base);
         __nv_bfloat16* orow_ptr = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD;
         if (pr.same_q && pr.ub >= 0) {
           // split pair: slot 1 stages its rows, slot 0 merges them into its own (R-11)
           if (k == 1) cm_stage_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f);
-          asm volatile("bar.sync 3, 256;" ::: "memory");
+          asm volatile("barrier.sync 3, 256;" ::: "memory");
           if (k == 0) cm_merge_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f, cm_direct ? orow_ptr : nullptr);
           GTRACE_T(true, 8);
         } else if (cm_direct) {
@@ -1085,6 +1102,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       if (w.group >= 0 && live) p.part_lse[pslot * kM + rr] = lse;
       }   // !cm
     }
+    if (!active && ring_stage) ring_free_arrive();
     if (p.cm_C > 0 && !cm_direct) {
       cm_sync(p.cm_C);   // every CTA of the cluster has staged its rows
       GTRACE_T(true, 9);

@@ -234,8 +234,11 @@ def test_flash_query_batch(cuda):
     assert st.digest(sid) == dg     # state neutrality
 
 
-def test_batch_run_snapshot(cuda):
-    """One launch: appends + queries of several sessions + stateless prompts (R-7)."""
+@pytest.mark.parametrize("per_layer", [False, True])
+def test_batch_run_snapshot(cuda, per_layer):
+    """One launch: appends + queries of several sessions + stateless prompts (R-7); per_layer:
+    the same batch as one single-layer launch per layer (cluster-merge plans over mixed
+    SHARED / SPLIT pair-items), the appends committed by the last layer's call."""
     import torch
     ssa = _ssa()
     L, hq, hkv, d, P = 2, 32, 8, 128, 64
@@ -263,8 +266,14 @@ def test_batch_run_snapshot(cuda):
         ref_items.append(dict(kind=kind, session=s, Q=Q, K=K, V=V))
         row += m
     Q, K, V = (np.concatenate(x, axis=1) for x in (Qs, Ks, Vs))
-    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=cuda)
-    st.batch_run(items, to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda), O)
+    O = torch.full(Q.shape, float("nan"), dtype=torch.bfloat16, device=cuda)
+    Qd, Kd, Vd = to_dev(Q, cuda), to_dev(K, cuda), to_dev(V, cuda)
+    if per_layer:
+        for l in range(L):
+            st.batch_run(items, Qd[l:l + 1], Kd[l:l + 1], Vd[l:l + 1], O[l:l + 1], layer=l)
+            assert st.last_plan()["cm_C"] >= 1
+    else:
+        st.batch_run(items, Qd, Kd, Vd, O)
     want = np.concatenate(ref.batch_run(ref_items), axis=1)
     ok, e = within(from_dev(O), want, "bf16")
     assert ok, e
