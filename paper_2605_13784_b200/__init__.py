@@ -377,10 +377,10 @@ class Store:
 
     def last_plan(self):
         """Shape of the last attention launch: units, groups, CTAs per layer, cluster size of a
-        cluster-merge launch (0: combine kernel / SIMT), largest split count."""
-        out = (ctypes.c_int64 * 5)()
+        cluster-merge launch (0: combine kernel / SIMT), largest split count, group-barrier merge."""
+        out = (ctypes.c_int64 * 6)()
         _check(lib.ssa_debug_last_plan(self._h, out), "debug_last_plan")
-        return dict(zip(("units", "groups", "ctas", "cm_C", "max_split"), list(out)))
+        return dict(zip(("units", "groups", "ctas", "cm_C", "max_split", "gbar"), list(out)))
 
     def timing(self, reset=False):
         """{kind: (ms_total, launches)} recorded under OPT_TIMING (syncs)."""

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   QKV_TRACE(0);
+  griddep_launch_dependents();   // the next grid's prologue may overlap this grid's tail
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* table = reinterpret_cast<float*>(tiles + kStages * kStageBytes);   // [rows][64] (cos, sin)
   double* inv_freq = reinterpret_cast<double*>(tiles + kStages * kStageBytes + kTableBytes);   // [64]
@@ -181,19 +182,30 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
+    // W is a weight no kernel of the stream writes: under programmatic dependent launch
+    // its first kStages stages are requested before griddepcontrol.wait, so the weight
+    // stream starts while the previous grid drains; X (the previous layer's output)
+    // only after it.
     if (elect_one()) {
+      auto load_w = [&](int i) {
+        const int s = i % kStages;
+        uint8_t* a = tiles + s * kStageBytes;
+        mbar_arrive_expect_tx(&bar.full[s], kStageBytes);
+        if (p.debug >= 2)   // experiments: contiguous 32 KB W blocks (wrong values, same bytes)
+          tma_load_2d(a + kABytes, &maps.w, &bar.full[s], 0, (tn * nkb + kb_lo + i) * kBN);
+        else
+          tma_load_2d(a + kABytes, &maps.w, &bar.full[s], (kb_lo + i) * kBK, tn * kBN);
+      };
+      const int n_early = p.debug == 5 ? 0 : min(n_kb, kStages);
+      for (int i = 0; i < n_early; ++i) load_w(i);
+      griddep_wait();
       for (int i = 0; i < n_kb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) mbar_wait(&bar.empty[s], ((i / kStages) - 1) & 1);
         uint8_t* a = tiles + s * kStageBytes;
         if (p.debug == 5) { mbar_arrive(&bar.full[s]); continue; }   // experiments: no loads
-        mbar_arrive_expect_tx(&bar.full[s], kStageBytes);
-        const int k0 = (kb_lo + i) * kBK;
-        tma_load_2d(a, &maps.x, &bar.full[s], k0, tm * kBM);
-        if (p.debug >= 2)   // experiments: contiguous 32 KB W blocks (wrong values, same bytes)
-          tma_load_2d(a + kABytes, &maps.w, &bar.full[s], 0, (tn * nkb + kb_lo + i) * kBN);
-        else
-          tma_load_2d(a + kABytes, &maps.w, &bar.full[s], k0, tn * kBN);
+        if (i >= n_early) load_w(i);
+        tma_load_2d(a, &maps.x, &bar.full[s], (kb_lo + i) * kBK, tm * kBM);
       }
     }
   } else if (warp == 1) {
@@ -251,6 +263,7 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
   // 128 of the 256 columns) into the owning CTA's receive buffer
   // recv[src rank][owner-local row] with distributed-shared-memory stores.
   mbar_wait(&bar.acc, 0);
+  griddep_wait();   // (returns at once by now) before any global write of this grid
   QKV_TRACE(2);
   tc_fence_after();
   cluster_sync_all();   // all mainloops done: stage memory is free cluster-wide
@@ -448,7 +461,7 @@ int qkv_max_active_clusters(int splits) {
   return n;
 }
 
-cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s) {
+cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s, bool pdl) {
   if (p.m <= 0) return cudaSuccess;
   if (!qkv_supported(p.D, p.hidden) || p.splits < 1 || p.splits > kMaxSplits || p.splits > p.hidden / kBK ||
       !qkv_exchange_fits(p.m, p.splits))
@@ -484,13 +497,15 @@ cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = p.splits;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, qkv_rope_kernel, p, maps);
 }
 

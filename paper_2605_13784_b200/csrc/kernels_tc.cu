@@ -284,32 +284,57 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* out, float4 v) {
   *reinterpret_cast<uint2*>(out) = u;
 }
 
-// Slot rows -> exchange buffer: O * inv_l (zeros for a row with no keys) and lse.
-__device__ __forceinline__ void cm_stage_rows(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
-                                              bool has) {
+// Slot rows -> exchange row `dst` (smem exchange buffer, or a global partial row in a
+// group-barrier launch): O * inv_l (zeros for a row with no keys), lse at *dst_lse.
+__device__ __forceinline__ void cm_stage_rows(float* dst, float* dst_lse, bool live, uint32_t o_col, float inv_l,
+                                              float lse, bool has) {
 #pragma unroll
   for (int q4 = 0; q4 < 4; ++q4) {
     uint32_t ro[32];
     tmem_ld32(o_col + q4 * 32, ro);
     tmem_wait_ld();
     if (live) {
-      float* dst = X + rr * kXStride + q4 * 32;
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
-        *reinterpret_cast<float4*>(dst + i) =
+        *reinterpret_cast<float4*>(dst + q4 * 32 + i) =
             has ? make_float4(__uint_as_float(ro[i]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l,
                               __uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l)
                 : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  if (live) X[kM * kXStride + rr] = has ? lse : -CUDART_INF_F;
+  if (live) *dst_lse = has ? lse : -CUDART_INF_F;
 }
+// The same rows into a global partial in the column-major float4 layout of
+// cm_merge_rows (group-barrier launches), lse at gpart_lse[rr].
+__device__ __forceinline__ void gm_stage_rows(float4* gpart, float* gpart_lse, int rr, bool live, uint32_t o_col,
+                                              float inv_l, float lse, bool has) {
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    uint32_t ro[32];
+    tmem_ld32(o_col + q4 * 32, ro);
+    tmem_wait_ld();
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        gpart[(q4 * 8 + i / 4) * kM + rr] =
+            has ? make_float4(__uint_as_float(ro[i]) * inv_l, __uint_as_float(ro[i + 1]) * inv_l,
+                              __uint_as_float(ro[i + 2]) * inv_l, __uint_as_float(ro[i + 3]) * inv_l)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (live) gpart_lse[rr] = has ? lse : -CUDART_INF_F;
+}
+__device__ __forceinline__ float* x_row(float* X, int rr) { return X + rr * kXStride; }
+__device__ __forceinline__ float* x_lse(float* X, int rr) { return X + kM * kXStride + rr; }
 
 // Split pair: slot 0 merges slot 1's staged rows with its own (R-11), in place --
 // or, with `out` (a CTA that holds its whole group: cluster of 1, one cluster per
-// group), straight into the bf16 output row.
+// group), straight into the bf16 output row, or with `gdst` (a group-barrier
+// launch) into this CTA's global partial (column-major float4 layout, element
+// (c, row) at gdst[c * kM + row]: a warp's stores are 512 contiguous bytes), lse at *glse.
 __device__ __forceinline__ void cm_merge_rows(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
-                                              bool has, __nv_bfloat16* out = nullptr) {
+                                              bool has, __nv_bfloat16* out = nullptr, float* gdst = nullptr,
+                                              float* glse = nullptr) {
   float a0 = 0.f, a1 = 0.f, lm = -CUDART_INF_F;
   if (live) {
     const float l1 = X[kM * kXStride + rr];
@@ -341,12 +366,61 @@ __device__ __forceinline__ void cm_merge_rows(float* X, int rr, bool live, uint3
         v.w = (a0 != 0.f ? a0 * __uint_as_float(ro[i + 3]) : 0.f) + a1 * x1.w;
         if (out)
           store_bf16x4(out + q4 * 32 + i, v);
+        else if (gdst)
+          reinterpret_cast<float4*>(gdst)[(q4 * 8 + i / 4) * kM + rr] = v;
         else
           *reinterpret_cast<float4*>(dst + i) = v;
       }
     }
   }
-  if (live && !out) X[kM * kXStride + rr] = lm;
+  if (live && !out) *(gdst ? glse : x_lse(X, rr)) = lm;
+}
+
+// Split pair without row duplication: slot 1's O rows sit in the same TMEM lanes as
+// slot 0's (columns +256), so slot 0 reads both straight from TMEM; slot 1 only
+// leaves its lse and 1/l per row in X (lse area and the next kM floats).  Output
+// as cm_merge_rows: bf16 `out`, the global partial `gdst` (+ *glse), or X in place.
+__device__ __forceinline__ void cm_merge_tmem(float* X, int rr, bool live, uint32_t o_col, float inv_l, float lse,
+                                              bool has, __nv_bfloat16* out, float* gdst, float* glse) {
+  float a0 = 0.f, a1 = 0.f, lm = -CUDART_INF_F;
+  if (live) {
+    const float l1 = *x_lse(X, rr);
+    const float il1 = *(x_lse(X, rr) + kM);
+    const float l0 = has ? lse : -CUDART_INF_F;
+    const float L = fmaxf(l0, l1);
+    if (L != -CUDART_INF_F) {
+      const float w0 = l0 == -CUDART_INF_F ? 0.f : exp2f(l0 - L);
+      const float w1 = l1 == -CUDART_INF_F ? 0.f : exp2f(l1 - L);
+      const float inv = 1.f / (w0 + w1);
+      a0 = w0 * inv * inv_l;
+      a1 = w1 * inv * il1;
+      lm = L + __log2f(w0 + w1);
+    }
+  }
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    uint32_t r0[32], r1[32];
+    tmem_ld32(o_col + q4 * 32, r0);
+    tmem_ld32(o_col + 256 + q4 * 32, r1);
+    tmem_wait_ld();
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 v;
+        v.x = (a0 != 0.f ? a0 * __uint_as_float(r0[i]) : 0.f) + (a1 != 0.f ? a1 * __uint_as_float(r1[i]) : 0.f);
+        v.y = (a0 != 0.f ? a0 * __uint_as_float(r0[i + 1]) : 0.f) + (a1 != 0.f ? a1 * __uint_as_float(r1[i + 1]) : 0.f);
+        v.z = (a0 != 0.f ? a0 * __uint_as_float(r0[i + 2]) : 0.f) + (a1 != 0.f ? a1 * __uint_as_float(r1[i + 2]) : 0.f);
+        v.w = (a0 != 0.f ? a0 * __uint_as_float(r0[i + 3]) : 0.f) + (a1 != 0.f ? a1 * __uint_as_float(r1[i + 3]) : 0.f);
+        if (out)
+          store_bf16x4(out + q4 * 32 + i, v);
+        else if (gdst)
+          reinterpret_cast<float4*>(gdst)[(q4 * 8 + i / 4) * kM + rr] = v;
+        else
+          *reinterpret_cast<float4*>(x_row(X, rr) + q4 * 32 + i) = v;
+      }
+    }
+  }
+  if (live && !out) *(gdst ? glse : x_lse(X, rr)) = lm;
 }
 
 __device__ __forceinline__ void store_bf16x8(__nv_bfloat16* out, const float* v) {
@@ -502,6 +576,103 @@ __device__ __forceinline__ void cm_reduce(const AttnParams& p, const WorkUnit& w
       }
     }
   }
+}
+
+// Group-barrier merge (AttnParams::cm_gbar; single-wave launches of clusters of
+// one CTA): every CTA of a group has written its (slot-merged, normalized) rows
+// as global partial `split` with their lse; the group's K CTAs meet at a barrier
+// in global memory (arrival counter + generation word per (layer, group), the
+// last arriver resets the counter and bumps the generation), then CTA `split`
+// merges row block `split` of the K partials (log-sum-exp, R-11) and writes O.
+// All CTAs of the launch are co-resident (grid <= SMs, one CTA per SM), so the
+// spin cannot wait on a CTA that is not running.  Warp wq takes rows
+// row0 + wq + 4i, lane l the partial l's lse (K <= 32) and columns [4l, 4l+4).
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+// t in [0, nthr): this thread's index among the nthr threads (one or both softmax
+// warpgroups, named barrier `bar_id`) that merge the group's row block.  Partial j
+// of the group is part_o[(s0 + j) * kM * kD ...] in the column-major float4 layout
+// of cm_merge_rows; item (row, c) = 4 output columns of one row, K loads in flight.
+template <int KMAX>
+__device__ __forceinline__ void gm_merge_items(const AttnParams& p, const WorkUnit& w, int K, int t, int nthr) {
+  const int ly = blockIdx.y;
+  const int G = p.G;
+  const int rows = w.q_ntok * G;
+  const int R = (rows + K - 1) / K;
+  const int row0 = w.split * R;
+  const int nr = min(row0 + R, rows) - row0;
+  const SegDesc sg = p.segs[w.seg];
+  const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+  const int64_t s0 = (int64_t)ly * p.n_units + p.groups[w.group].unit0;
+  const float4* po = reinterpret_cast<const float4*>(p.part_o) + s0 * (kM * kD / 4);
+  const float* pl = p.part_lse + s0 * kM;
+  // items: (row, c) with rows fastest within groups of 8, so a warp reads 4 x 128 B
+  for (int it = t; it < ((nr + 7) & ~7) * (kD / 4); it += nthr) {
+    const int row = row0 + (it & 7) + 8 * ((it >> 3) / (kD / 4));
+    const int c = (it >> 3) % (kD / 4);
+    if (row >= row0 + nr) continue;
+    float lj[KMAX];
+    float4 v[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < K) {
+        lj[j] = __ldcg(pl + (int64_t)j * kM + row);
+        v[j] = __ldcg(po + (int64_t)j * (kM * kD / 4) + c * kM + row);
+      }
+    float L = -CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < K) L = fmaxf(L, lj[j]);
+    float ws = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < K) {
+        const float wt = lj[j] == -CUDART_INF_F ? 0.f : exp2f(lj[j] - L);
+        ws += wt;
+        acc.x = fmaf(wt, v[j].x, acc.x);
+        acc.y = fmaf(wt, v[j].y, acc.y);
+        acc.z = fmaf(wt, v[j].z, acc.z);
+        acc.w = fmaf(wt, v[j].w, acc.w);
+      }
+    const float inv = ws > 0.f ? 1.f / ws : 0.f;
+    const int64_t orow = in_l + sg.row0 + w.q_tok0 + row / G;
+    store_bf16x4(static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + w.kv_head * G + row % G) * kD + 4 * c,
+                 make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+  }
+}
+
+__device__ __forceinline__ void gm_reduce(const AttnParams& p, const WorkUnit& w, int t, int nthr, int bar_id) {
+  const int ly = blockIdx.y;
+  const int K = p.groups[w.group].n_splits;
+  if (t == 0) {
+    // arrival: acq_rel atomic (releases this CTA's partial rows, ordered before it by the
+    // CTA barrier and the fence); the last arriver resets the counter for the next launch
+    // (relaxed: kernel boundaries order it) and releases the bumped generation
+    uint32_t* c = reinterpret_cast<uint32_t*>(p.cm_tickets) + ((int64_t)ly * p.n_groups + w.group) * 2;
+    const uint32_t gen0 = ld_acquire_u32(c + 1);
+    __threadfence();
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(c) : "memory");
+    if (old == (uint32_t)K - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(c) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(c + 1), "r"(gen0 + 1u) : "memory");
+    } else {
+      while (ld_acquire_u32(c + 1) == gen0) {
+      }
+    }
+  }
+  asm volatile("barrier.sync %0, %1;" ::"r"(bar_id), "r"(nthr) : "memory");
+  GTRACE_T(true, 11);
+  if (K <= 8)
+    gm_merge_items<8>(p, w, K, t, nthr);
+  else if (K <= 16)
+    gm_merge_items<16>(p, w, K, t, nthr);
+  else
+    gm_merge_items<24>(p, w, K, t, nthr);
 }
 
 // Groups spread over K > 1 clusters: merge the K block partials of every row
@@ -1023,6 +1194,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       if (nt > 0) {
         mbar_wait(&bar.o_final[k], 0);
         GTRACE(r == 0 && k == 0, 5);
+        GTRACE(r == 0 && k == 1, 14);
         tc_fence_after();
       }
       griddep_wait();   // before the first global write (O / partials of the previous grid's readers)
@@ -1044,11 +1216,37 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         if (ring_stage) ring_free_wait();
         float* X0 = reinterpret_cast<float*>(k_base);
         __nv_bfloat16* orow_ptr = static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + h) * kD;
-        if (pr.same_q && pr.ub >= 0) {
-          // split pair: slot 1 stages its rows, slot 0 merges them into its own (R-11)
-          if (k == 1) cm_stage_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f);
+        // group-barrier launch, group over several CTAs: this slot's rows go to the
+        // group's global partial `split` (merged after the group barrier, gm_reduce)
+        float* gdst = nullptr;
+        float* glse = nullptr;
+        if (p.cm_gbar && !cm_direct && p.groups[w.group].n_splits > 1) {
+          const int64_t ps = (int64_t)ly * p.n_units + p.groups[w.group].unit0 + w.split;
+          gdst = p.part_o + ps * kM * kD;
+          glse = p.part_lse + ps * kM;
+        }
+        if (pr.same_q && pr.ub >= 0 && !dup) {
+          // split pair: slot 1 leaves its lse and 1/l, slot 0 merges both slots' O rows
+          // straight from TMEM (R-11)
+          if (k == 1 && live) {
+            *x_lse(X0, rr) = l_run > 0.f ? lse : -CUDART_INF_F;
+            *(x_lse(X0, rr) + kM) = inv_l;
+          }
+          GTRACE(threadIdx.x == 256, 15);
           asm volatile("barrier.sync 3, 256;" ::: "memory");
-          if (k == 0) cm_merge_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f, cm_direct ? orow_ptr : nullptr);
+          if (k == 0)
+            cm_merge_tmem(X0, rr, live, o_col, inv_l, lse, l_run > 0.f, cm_direct ? orow_ptr : nullptr, gdst,
+                          glse ? glse + rr : nullptr);
+          GTRACE_T(true, 8);
+        } else if (pr.same_q && pr.ub >= 0) {
+          // duplicated small q tile (slot 1's rows in lanes 32..): slot 1 stages its rows,
+          // slot 0 merges them into its own (R-11)
+          if (k == 1) cm_stage_rows(x_row(X0, rr), x_lse(X0, rr), live, o_col, inv_l, lse, l_run > 0.f);
+          GTRACE(threadIdx.x == 256, 15);
+          asm volatile("barrier.sync 3, 256;" ::: "memory");
+          if (k == 0)
+            cm_merge_rows(X0, rr, live, o_col, inv_l, lse, l_run > 0.f, cm_direct ? orow_ptr : nullptr, gdst,
+                          glse ? glse + rr : nullptr);
           GTRACE_T(true, 8);
         } else if (cm_direct) {
 #pragma unroll
@@ -1065,8 +1263,11 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
                 store_bf16x8(orow_ptr + q4 * 32 + i, v);
               }
           }
+        } else if (gdst) {
+          gm_stage_rows(reinterpret_cast<float4*>(gdst), glse, rr, live, o_col, inv_l, lse, l_run > 0.f);
         } else {
-          cm_stage_rows(X0 + (pr.same_q ? 0 : k) * kXFloats, rr, live, o_col, inv_l, lse, l_run > 0.f);
+          float* Xk = X0 + (pr.same_q ? 0 : k) * kXFloats;
+          cm_stage_rows(x_row(Xk, rr), x_lse(Xk, rr), live, o_col, inv_l, lse, l_run > 0.f);
         }
       } else {
 #pragma unroll
@@ -1106,7 +1307,13 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     if (p.cm_C > 0 && !cm_direct) {
       cm_sync(p.cm_C);   // every CTA of the cluster has staged its rows
       GTRACE_T(true, 9);
-      if (k < (two_q ? 2 : 1)) {
+      const bool gm_k = p.cm_gbar && p.groups[(k && two_q ? w1 : w0).group].n_splits > 1;
+      if (gm_k) {
+        // group-barrier merge: two q tiles -> warpgroup k merges slot k's group; a split
+        // pair's single group is merged by both warpgroups
+        const int t = threadIdx.x - 128 - (two_q ? 128 * k : 0);
+        gm_reduce(p, two_q && k ? w1 : w0, t, two_q ? 128 : 256, two_q ? 1 + k : 3);
+      } else if (k < (two_q ? 2 : 1)) {
         const float* X = reinterpret_cast<const float*>(k_base) + k * kXFloats;
         const WorkUnit& wk = k ? w1 : w0;
         switch (p.cm_C) {

@@ -219,7 +219,7 @@ void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile
 namespace ssa {
 
 double plan_cm(const std::vector<SegDesc>& segs, const PlanConfig& c, int C, int max_clusters, Plan* plan,
-               std::vector<TcPair>* pairs) {
+               std::vector<TcPair>* pairs, bool gbar) {
   plan->units.clear();
   plan->groups.clear();
   pairs->clear();
@@ -274,7 +274,14 @@ double plan_cm(const std::vector<SegDesc>& segs, const PlanConfig& c, int C, int
   const int np = (int)pis.size();
   std::vector<int> K(np, 1);
   int used = np;
-  auto per_cta = [&](int i) { return pis[i].work / (double)(C * K[i]); };
+  // gbar: whole key tiles per slot (a split item's 2 C K ranges, a shared pair's C K
+  // ranges), so clusters that leave the largest range unchanged are given back
+  auto per_cta = [&](int i) {
+    if (!gbar) return pis[i].work / (double)(C * K[i]);
+    const PItem& pi = pis[i];
+    if (pi.b < 0) return (double)ceil_div(items[pi.a].tiles, 2 * C * K[i]);
+    return std::ceil(pi.work / (double)(C * K[i]) - 1e-9);
+  };
   if (np <= max_clusters) {
     std::priority_queue<std::pair<double, int>> q;
     for (int i = 0; i < np; ++i) q.push({per_cta(i), i});
@@ -291,16 +298,24 @@ double plan_cm(const std::vector<SegDesc>& segs, const PlanConfig& c, int C, int
     double mx = 0.0;
     for (int i = 0; i < np; ++i) mx = std::max(mx, per_cta(i));
     for (int i = 0; i < np; ++i)
-      while (K[i] > 1 && pis[i].work / (double)(C * (K[i] - 1)) <= mx) {
+      while (K[i] > 1) {
         --K[i];
+        if (per_cta(i) > mx) { ++K[i]; break; }
         --used;
       }
   }
   // cost: largest per-CTA range, with waves if the clusters do not fit at once
   double cost = 0.0;
   const double waves = std::ceil((double)used / (double)max_clusters);
+  if (gbar) {
+    // group-barrier merge: one wave of single CTAs, a group's partial lse fit a warp
+    if (C != 1 || used > max_clusters) return -1.0;
+    for (int i = 0; i < np; ++i)
+      if (K[i] > 32) return -1.0;
+  }
   for (int i = 0; i < np; ++i) {
-    const double merge = (C > 1 ? 0.25 : 0.0) + (K[i] > 1 ? 1.0 + 0.5 * (K[i] - 1) / (double)C : 0.0);
+    const double merge = gbar ? (K[i] > 1 ? 1.0 : 0.0)
+                              : (C > 1 ? 0.25 : 0.0) + (K[i] > 1 ? 1.0 + 0.5 * (K[i] - 1) / (double)C : 0.0);
     cost = std::max(cost, per_cta(i) + merge);
   }
   cost *= waves;

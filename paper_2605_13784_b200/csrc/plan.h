@@ -44,8 +44,10 @@ void pair_units(const std::vector<SegDesc>& segs, const Plan& plan, int key_tile
 // the clusters fit `max_clusters` and the largest per-CTA key range is smallest.
 // Returns the estimated makespan in key tiles (+ merge overheads), or -1 if the
 // plan does not apply.
+// gbar: the group-barrier merge (AttnParams::cm_gbar): C = 1, every CTA in one wave
+// (used <= max_clusters), at most 32 CTAs per group, a flat merge cost.
 double plan_cm(const std::vector<SegDesc>& segs, const PlanConfig& c, int C, int max_clusters, Plan* plan,
-               std::vector<TcPair>* pairs);
+               std::vector<TcPair>* pairs, bool gbar = false);
 
 // cm_regroup: turn an LPT plan (plan_units + pair_units) into a C = 1 CM plan:
 // every unit gets a group (singletons for unsplit units), Group::n_splits becomes

@@ -101,6 +101,10 @@ struct AttnParams {
   // groups over K > 1 clusters: merge tickets [layers][n_groups][cm_C] (zero between
   // launches) for the in-kernel last-arriver merge, or null: cm_merge_kernel
   int32_t* cm_tickets;
+  // 1: group-barrier merge (cm_C == 1, one wave): groups over K > 1 CTAs write global
+  // partials, meet at a barrier in cm_tickets ([layers][n_groups][2]: arrivals,
+  // generation; zero at allocation) and merge in the same kernel (gm_reduce)
+  int32_t cm_gbar;
   // pool tiles are loaded with an L2 evict-first hint (read once per launch)
   int32_t l2_evict_first;
   // FP8 KV variant (reading R-22): pools and Kt/Vt hold E4M3 codes; scale_log2
@@ -223,7 +227,7 @@ cudaError_t launch_combine(const CombineParams& p, int n_layers, bool bf16, cuda
 cudaError_t launch_scatter(const ScatterParams& p, int n_layers, cudaStream_t s);
 cudaError_t launch_quant_e4m3(const QuantParams& p, cudaStream_t s);
 cudaError_t launch_gather(const GatherParams& p, cudaStream_t s);
-cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s);
+cudaError_t launch_qkv_rope(const QkvParams& p, cudaStream_t s, bool pdl);
 bool qkv_supported(int D, int hidden);
 int qkv_choose_splits(int m, int n_heads, int hidden, int num_sms);
 int qkv_max_active_clusters(int splits);

@@ -553,7 +553,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   const bool cm = use_tc && !special;
   const bool cap = capturing(st);
   // ---- cache key: every input of the planner and of the uploaded lists
-  std::vector<int64_t> key = {compute_o, use_tc, cm, opt_cluster, n_layers, opt_max_splits, opt_fault,
+  std::vector<int64_t> key = {compute_o, use_tc, cm, opt_cluster, opt_cm_merge, n_layers, opt_max_splits, opt_fault,
                               opts.force_groups, (int64_t)segs.size()};
   for (const SegDesc& sg : segs)
     key.insert(key.end(), {sg.row0, sg.m, sg.tail_m, sg.n_slots, sg.hole_lo, sg.hole_hi, sg.append_slot0,
@@ -588,16 +588,25 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
       fresh.cm_C = 0;
       if (cm && n_layers == 1 && opt_cluster >= 0) {
         double best = -1.0;
-        for (int C : {1, 2, 3, 4, 5, 6, 7, 8, 16}) {
-          if (opt_cluster > 0 && C != opt_cluster) continue;
+        // candidates: clusters of C CTAs (DSMEM merge + merge kernel for groups over
+        // several clusters), and the group-barrier merge (C = 1, one wave, gm_reduce)
+        // (the group-barrier plan, when it applies, is taken without comparing costs:
+        // measured faster on the per-layer query, whose merge it keeps inside the kernel)
+        for (int C : {0, 1, 2, 3, 4, 5, 6, 7, 8, 16}) {
+          const bool gb = C == 0;
+          if (gb && (opt_cm_merge != 2 || opt_cluster > 0)) continue;
+          if (!gb && fresh.gbar) break;
+          const int Ck = gb ? 1 : C;
+          if (opt_cluster > 0 && Ck != opt_cluster) continue;
           Plan pl;
           std::vector<TcPair> prs;
-          const double cost = plan_cm(segs, pc, C, max_clusters(C), &pl, &prs);
+          const double cost = plan_cm(segs, pc, Ck, max_clusters(Ck), &pl, &prs, gb);
           if (cost >= 0.0 && (best < 0.0 || cost < best)) {
             best = cost;
             plan = std::move(pl);
             fresh.pairs = std::move(prs);
-            fresh.cm_C = C;
+            fresh.cm_C = Ck;
+            fresh.gbar = gb;
           }
         }
       }
@@ -800,18 +809,23 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     // before this one on the stream is one of the store's pool writers
     ap.pool_early = (opt_pdl != 0 && !opt_timing && !(pool_writer_last && last_kernel_stream == st)) ? 1 : 0;
     ap.l2_evict_first = opt_l2_hint == 2 || (opt_l2_hint == 0 && E.l2_hint) ? 1 : 0;
-    const bool merge_in_kernel = E.cm_C > 0 && E.max_split > 1 && opt_cm_merge == 0;
+    const bool gbar = E.gbar && E.max_split > 1;
+    const bool merge_in_kernel = E.cm_C > 0 && E.max_split > 1 && (opt_cm_merge == 0 || gbar);
+    ap.cm_gbar = gbar ? 1 : 0;
     if (merge_in_kernel) {
-      const size_t need = (size_t)n_layers * plan.groups.size() * E.cm_C;
-      if (need > tickets_cap) {
+      // zeroed counters: [layers][groups][C] tickets, or [layers][groups][2] group barriers
+      int32_t*& buf = gbar ? gb_tickets : tickets;
+      size_t& buf_cap = gbar ? gb_tickets_cap : tickets_cap;
+      const size_t need = (size_t)n_layers * plan.groups.size() * (gbar ? 2 : E.cm_C);
+      if (need > buf_cap) {
         if (cap) { ssa::set_error("CUDA-graph capture: warm up the call once before capturing (merge tickets)"); return SSA_ERR_STATE; }
-        if (tickets) SSA_CUDA(this, cudaFreeAsync(tickets, st));
-        tickets = nullptr;
-        tickets_cap = std::max(need, tickets_cap * 2);
-        SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&tickets), tickets_cap * sizeof(int32_t), st));
-        SSA_CUDA(this, cudaMemsetAsync(tickets, 0, tickets_cap * sizeof(int32_t), st));
+        if (buf) SSA_CUDA(this, cudaFreeAsync(buf, st));
+        buf = nullptr;
+        buf_cap = std::max(need, buf_cap * 2);
+        SSA_CUDA(this, cudaMallocAsync(reinterpret_cast<void**>(&buf), buf_cap * sizeof(int32_t), st));
+        SSA_CUDA(this, cudaMemsetAsync(buf, 0, buf_cap * sizeof(int32_t), st));
       }
-      ap.cm_tickets = tickets;
+      ap.cm_tickets = buf;
     }
     cudaEvent_t t0 = tick(st);
     if (use_tc) {
@@ -865,6 +879,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
   last_plan_groups = (int64_t)plan.groups.size();
   last_used_tc = use_tc;
   last_cm_C = E.cm_C;
+  last_gbar = E.gbar ? 1 : 0;
   last_max_split = E.max_split;
   last_n_ctas = (int64_t)E.pairs.size();
   return SSA_OK;
@@ -1019,6 +1034,7 @@ ssa_store::~ssa_store() {
   for (auto& e : plan_cache)
     if (e.dev) cudaFree(e.dev);
   if (tickets) cudaFree(tickets);
+  if (gb_tickets) cudaFree(gb_tickets);
   if (order_ev) cudaEventDestroy(order_ev);
   if (sample_part) cudaFree(sample_part);
   if (sample_cnt) cudaFree(sample_cnt);
@@ -1046,13 +1062,14 @@ ssa_status ssa_store_stats(ssa_store_t st, ssa_stats* out, int32_t reset) {
   return SSA_OK;
 }
 
-ssa_status ssa_debug_last_plan(ssa_store_t st, int64_t out[5]) {
+ssa_status ssa_debug_last_plan(ssa_store_t st, int64_t out[6]) {
   if (!st || !out) return SSA_ERR_INVALID_ARG;
   out[0] = st->last_plan_units;
   out[1] = st->last_plan_groups;
   out[2] = st->last_n_ctas;
   out[3] = st->last_cm_C;
   out[4] = st->last_max_split;
+  out[5] = st->last_gbar;
   return SSA_OK;
 }
 
@@ -1074,7 +1091,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
       st->opt_cluster = value;
       break;
     case SSA_OPT_PDL: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_pdl = value; break;
-    case SSA_OPT_CM_MERGE: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
+    case SSA_OPT_CM_MERGE: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
     case SSA_OPT_L2_HINT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_l2_hint = value; break;
     case SSA_OPT_PIPE_CHUNKS: if (value < -1 || value > 64) return SSA_ERR_INVALID_ARG; st->opt_pipe_chunks = value; break;
     case SSA_OPT_QKV_DEBUG: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_qkv_debug = value; break;
@@ -1875,7 +1892,7 @@ static ssa_status qkv_launch(ssa_store* st, int32_t n, int32_t hidden, int64_t p
   qp.debug = (int32_t)st->opt_qkv_debug;
   qp.trace = g_qkv_trace;
   cudaEvent_t t0 = st->tick(cs);
-  SSA_CUDA(st, launch_qkv_rope(qp, cs));
+  SSA_CUDA(st, launch_qkv_rope(qp, cs, st->opt_pdl != 0 && !t0));
   if (t0) st->timed_push(5, t0, st->tick(cs));
   st->stats.kernel_launches++;
   st->note_kernel(cs, qp.poolK != nullptr);   // K/V written straight into pages

@@ -120,6 +120,7 @@ struct ssa_store {
     std::vector<ssa::TcPair> pairs;
     int32_t cm_C = 0;          // cluster-merge launch (AttnParams::cm_C), 0 = combine kernel / SIMT
     int32_t max_split = 0;     // largest Group::n_splits
+    bool gbar = false;         // group-barrier merge (AttnParams::cm_gbar)
     bool l2_hint = false;      // every key tile is read by one CTA (no reuse in L2 to keep)
     int32_t n_app = 0;         // scatter segments
     int32_t app_tokens = 0;
@@ -158,10 +159,12 @@ struct ssa_store {
   int64_t opt_backend = 0, opt_max_splits = 0, opt_fault = 0, opt_tc_qtiles = 0;
   int64_t opt_cluster = 0;       // SSA_OPT_CLUSTER
   int64_t opt_pdl = 1;           // SSA_OPT_PDL
-  int64_t opt_cm_merge = 1;      // SSA_OPT_CM_MERGE
+  int64_t opt_cm_merge = 2;      // SSA_OPT_CM_MERGE
   int64_t opt_l2_hint = 0;       // SSA_OPT_L2_HINT
   int32_t* tickets = nullptr;    // CM merge tickets (zero between launches)
   size_t tickets_cap = 0;
+  int32_t* gb_tickets = nullptr; // group-barrier counters (arrivals reset by the last arriver)
+  size_t gb_tickets_cap = 0;
   int64_t opt_pipe_chunks = 0;   // SSA_OPT_PIPE_CHUNKS
   int64_t opt_qkv_debug = 0;     // SSA_OPT_QKV_DEBUG
   // Cross-stream ordering: the device work of a call waits for the previous
@@ -192,7 +195,7 @@ struct ssa_store {
   ssa_stats stats{};
   int32_t ticket_seq = 0;
   int64_t last_plan_units = 0, last_plan_groups = 0, last_n_ctas = 0;
-  int32_t last_cm_C = 0, last_max_split = 0;
+  int32_t last_cm_C = 0, last_max_split = 0, last_gbar = 0;
   bool last_used_tc = false;
   CommState* comm = nullptr;
   // SSA_OPT_TIMING

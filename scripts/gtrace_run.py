@@ -21,7 +21,8 @@ st = ssa.Store(L, C["hq"], C["hkv"], C["d"], page_size=C["P"], num_pages=C["n_ct
 spec = streams.StreamSpec("market", seed=2)
 sid = bench.build_session(st, torch, dev, spec, C["n_ctx"])
 buf = np.zeros(32 * 256 * 16, dtype=np.uint64)
-names = ["entry", "setup", "q", "k0", "s0", "o_fin", "end", None, "staged", "csync1", "reduced", "ticket", "merged", "csync2"]
+names = ["entry", "setup", "q", "k0", "s0", "o_fin", "end", None, "staged", "csync1", "reduced", "ticket", "merged",
+         "csync2", "o_fin1", "st1"]
 for qlen in (32, 1):
     q, k, v = bench.gen_new(torch, dev, spec, 1, 0, qlen)
     o = torch.empty_like(q)
@@ -30,8 +31,10 @@ for qlen in (32, 1):
         s = torch.cuda.current_stream()
         for l in range(L):
             st.session_query(sid, q[l:l + 1], k[l:l + 1], v[l:l + 1], o[l:l + 1], layer=l, stream=s)
-    for cl in (int(x) for x in os.environ.get("GT_CLUSTERS", "0,4,16").split(",")):
+    # GT_CFGS: "cluster,merge ..." (SSA_OPT_CLUSTER, SSA_OPT_CM_MERGE)
+    for cl, mk in (tuple(int(x) for x in c.split(",")) for c in os.environ.get("GT_CFGS", "0,1 4,1 0,2").split()):
         st.set_option(ssa.OPT_CLUSTER, cl)
+        st.set_option(ssa.OPT_CM_MERGE, mk)
         per_layer()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -44,7 +47,7 @@ for qlen in (32, 1):
         ssa.lib.ssa_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
         t = buf.reshape(32, 256, 16).astype(np.int64)
         nct = st.last_plan()["ctas"]
-        print(f"GT q={qlen} cluster={cl} plan={st.last_plan()}")
+        print(f"GT q={qlen} cluster={cl} merge={mk} plan={st.last_plan()}")
         prev_end = None
         spans = []
         for l in range(L):

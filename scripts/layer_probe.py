@@ -57,8 +57,9 @@ for q_len in (32, 1):
         s = torch.cuda.current_stream()
         for l in range(L):
             st.session_query(sid, q[l:l + 1], k[l:l + 1], v[l:l + 1], o[l:l + 1], layer=l, stream=s)
-    for cl in (0, 1, 2, 4, 6):
-        for pdl, mk in ((1, 0), (1, 1), (0, 0)):
+    for cl, pdl, mk in [tuple(int(x) for x in c.split(",")) for c in os.environ.get(
+            "LAYER_CFGS", "0,1,1 4,1,1 0,1,2 0,0,2").split()]:
+        if True:
             st.set_option(ssa.OPT_CLUSTER, cl)
             st.set_option(ssa.OPT_PDL, pdl)
             st.set_option(ssa.OPT_CM_MERGE, mk)
@@ -72,8 +73,9 @@ for q_len in (32, 1):
     print(f"LAYER q={q_len} all-layer call {ms * 1e3 / L:.1f} us/layer plan {st.last_plan()}", flush=True)
 
 st.set_option(ssa.OPT_PDL, 1)
-for cl in (0, 3, 4, 6):
+for cl, mk in ((0, 1), (4, 1), (0, 2)):
     st.set_option(ssa.OPT_CLUSTER, cl)
+    st.set_option(ssa.OPT_CM_MERGE, mk)
     st.session_truncate(sid, n0)
     reps = 10
     tot = 0.0
@@ -101,5 +103,5 @@ for cl in (0, 3, 4, 6):
         st.session_truncate(sid, n0)
     ms = tot / reps
     fl = bench.append_flops_per_layer(n0, C["m_append"], C["hq"], C["d"])
-    print(f"LAYER append cluster={cl} graph {ms * 1e3 / L:.1f} us/layer = {fl / (ms / L * 1e-3) / 1e12:.0f} TFLOP/s "
+    print(f"LAYER append cluster={cl} merge={mk} graph {ms * 1e3 / L:.1f} us/layer = {fl / (ms / L * 1e-3) / 1e12:.0f} TFLOP/s "
           f"plan {st.last_plan()}", flush=True)

@@ -540,7 +540,7 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
     want = ref.session_query(rsid, Qq, Kq, Vq)
     bound = _bound(ref, rsid, Qq, Kq, Vq, want)
     Qd, Kd, Vd = to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda)
-    for C, merge in ((0, 1), (-1, 1), (1, 1), (1, 0), (2, 1), (2, 0), (4, 1), (4, 0), (6, 1), (8, 1)):
+    for C, merge in ((0, 1), (-1, 1), (1, 1), (1, 0), (2, 1), (2, 0), (4, 1), (4, 0), (6, 1), (8, 1), (0, 2)):
         st.set_option(ssa.OPT_CLUSTER, C)
         st.set_option(ssa.OPT_CM_MERGE, merge)   # separate merge kernel / last-arriving CTA
         splits = []
@@ -555,22 +555,27 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
             assert ok, (C, rep, e)
             ok, r = within_bound(from_dev(O), want, bound)
             assert ok, (C, rep, "bound", r)
-        if C in (1, 2):
+        if C in (1, 2) or merge == 2:
             assert max(splits) > 1, (C, splits)     # the cross-cluster (last-arriver) merge ran
-    assert st.stats()["cm_launches"] >= 2 * L * 10
+        if merge == 2:
+            assert plan["gbar"] == 1, plan          # group-barrier merge inside the kernel
+    assert st.stats()["cm_launches"] >= 2 * L * 11
 
 
-@pytest.mark.parametrize("C", [1, 4, 8])
+@pytest.mark.parametrize("C", [1, 4, 8, "gbar"])
 def test_cluster_merge_empty_ranges(cuda, C):
-    """A short cache (2 key tiles per head) under a forced cluster size: most CTAs of the plan
-    get empty key ranges (lse = -inf, skipped by the merge)."""
+    """A short cache (2 key tiles per head) under a forced cluster size (or the group-barrier
+    merge): most CTAs of the plan get empty key ranges (lse = -inf, skipped by the merge)."""
     import torch
     ssa = _ssa()
     L, hq, hkv, d, P = 1, 32, 8, 128, 16
     spec = streams.StreamSpec("peaked", seed=62)
     for n in (1, 150, 300):
         st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
-        st.set_option(ssa.OPT_CLUSTER, C)
+        if C == "gbar":
+            st.set_option(ssa.OPT_CM_MERGE, 2)
+        else:
+            st.set_option(ssa.OPT_CLUSTER, C)
         ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
         Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, n)
         sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
@@ -584,7 +589,7 @@ def test_cluster_merge_empty_ranges(cuda, C):
         st.close()
 
 
-@pytest.mark.parametrize("C", [0, 1, 2, 4, 8])
+@pytest.mark.parametrize("C", [0, 1, 2, 4, 8, "gbar"])
 def test_cluster_merge_per_layer_append(cuda, C):
     """Per-layer data-plane steps (Alg. 1: append_begin / append_layer per layer / commit)
     under the cluster-merge plans: SHARED CTA pairs (two q tiles over the same keys), the key
@@ -594,7 +599,10 @@ def test_cluster_merge_per_layer_append(cuda, C):
     L, hq, hkv, d, P = 2, 32, 8, 128, 64
     spec = streams.StreamSpec("market", seed=63)
     st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=256)
-    st.set_option(ssa.OPT_CLUSTER, C)
+    if C == "gbar":
+        st.set_option(ssa.OPT_CM_MERGE, 2)
+    else:
+        st.set_option(ssa.OPT_CLUSTER, C)
     ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=256)
     Q, K, V = gen_qkv(spec, L, hq, hkv, d, 0, 0, 3000)
     sid = st.session_create(None, to_dev(K, cuda), to_dev(V, cuda))
