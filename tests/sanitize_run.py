@@ -149,7 +149,7 @@ for kv in (None, "e4m3"):
     for nq in (1, 32):
         Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, nq)
         want = ref.session_query(rsid, Qq, Kq, Vq)
-        for C, merge in ((1, 1), (2, 1), (2, 0), (4, 1), (8, 1)):
+        for C, merge in ((1, 1), (2, 1), (2, 0), (4, 1), (8, 1), (0, 2)):
             st.set_option(ssa.OPT_CLUSTER, C)
             st.set_option(ssa.OPT_CM_MERGE, merge)
             Ol = torch.empty(Qq.shape, dtype=torch.bfloat16, device=dev)
@@ -158,16 +158,20 @@ for kv in (None, "e4m3"):
                                  Ol[l:l + 1], layer=l)
             check(f"{kv or 'bf16'} per-layer query {nq} C={C} merge={merge} plan={st.last_plan()}", from_dev(Ol), want,
                   "bf16")
-    st.set_option(ssa.OPT_CLUSTER, 4)
-    Qa, Ka, Va = gen_qkv(spec, L, hq, hkv, d, 0, n, 200)
-    Oa = torch.empty(Qa.shape, dtype=torch.bfloat16, device=dev)
-    t = st.append_begin(sid, 200)
-    for l in range(L):
-        st.append_layer(sid, t, l, to_dev(Qa[l:l + 1], dev), to_dev(Ka[l:l + 1], dev), to_dev(Va[l:l + 1], dev),
-                        Oa[l:l + 1])
-    st.append_commit(sid, t)
-    wa, _ = ref.session_append(rsid, Qa, Ka, Va)
-    check(f"{kv or 'bf16'} per-layer append", from_dev(Oa), wa, "bf16")
+    tok = n
+    for C, merge in ((4, 1), (0, 2)):   # cluster plan / group-barrier merge
+        st.set_option(ssa.OPT_CLUSTER, C)
+        st.set_option(ssa.OPT_CM_MERGE, merge)
+        Qa, Ka, Va = gen_qkv(spec, L, hq, hkv, d, 0, tok, 200)
+        Oa = torch.empty(Qa.shape, dtype=torch.bfloat16, device=dev)
+        t = st.append_begin(sid, 200)
+        for l in range(L):
+            st.append_layer(sid, t, l, to_dev(Qa[l:l + 1], dev), to_dev(Ka[l:l + 1], dev), to_dev(Va[l:l + 1], dev),
+                            Oa[l:l + 1])
+        st.append_commit(sid, t)
+        wa, _ = ref.session_append(rsid, Qa, Ka, Va)
+        check(f"{kv or 'bf16'} per-layer append C={C} merge={merge} plan={st.last_plan()}", from_dev(Oa), wa, "bf16")
+        tok += 200
     st.close()
 
 # greedy sampling + fused projection
