@@ -403,13 +403,21 @@ def leg_flash(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_ctx):
 
 def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq):
     """BJ.configs[1] curves vs context n: the same session truncated (SeqRemove)
-    to n in {4k, 8k, 16k, 32,512}; per n the 32-token query and the 256-token append over
+    to n in {1k, 2k, 4k, 8k, 16k, 32,512}; per n the 32-token query and the 256-token append over
     32 layers (kernel CUDA events, as the headline), as GB/s and TFLOP/s of their algorithmic
-    bytes / FLOPs.  Runs right after the headline region (before the heavy legs)."""
+    bytes / FLOPs.  At 16k and 8k also the BJ.configs[3] batch (64 x 32-token
+    Flash Queries in one launch over 32 layers; 32k is the flash_queries leg).  Runs right
+    after the headline region (before the heavy legs)."""
     import paper_2605_13784_b200 as ssa
+    import streams
     L, hq, hkv, d = CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"]
-    out = {"workload": "BJ.configs[1] session truncated to n; 32-token query / 256-token append, 32 layers"}
-    for n in (n_top, 16384, 8192, 4096):
+    out = {"workload": "BJ.configs[1] session truncated to n; 32-token query / 256-token append, 32 layers; "
+                       "flash_64x32 = BJ.configs[3] batch at n"}
+    fq = [gen_new(torch, dev, spec, streams.FLASH_DOMAIN + i, 0, 32) for i in range(64)]
+    FQ, FK, FV = (torch.cat([x[j] for x in fq], dim=1).contiguous() for j in range(3))
+    FO = torch.empty_like(FQ)
+    del fq
+    for n in (n_top, 16384, 8192, 4096, 2048, 1024):
         st.session_truncate(sid, n)
         st.set_option(ssa.OPT_TIMING, 1)
         st.timing(reset=True)
@@ -434,7 +442,13 @@ def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Q
                         "query_hbm_frac": qb / (qms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                         "append_attn_ms": a_ms, "append_tflops": af / (a_ms * 1e-3) / 1e12,
                         "append_tc_frac": af / (a_ms * 1e-3) / 1e12 / peaks["bf16_tflops"]}
-    st.session_truncate(sid, 4096)
+        if n in (16384, 8192):
+            fms = _timed(torch, stream, lambda: st.flash_query_batch(sid, [32] * 64, FQ, FK, FV, FO, stream=stream),
+                         1, 1)
+            ff = 64 * append_flops_per_layer(n, 32, hq, d) * L
+            out[f"n{n}"]["flash_64x32"] = {"ms_32_layers": fms, "tflops": ff / (fms * 1e-3) / 1e12,
+                                           "tc_frac": ff / (fms * 1e-3) / 1e12 / peaks["bf16_tflops"]}
+    st.session_truncate(sid, 1024)
     return out
 
 

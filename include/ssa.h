@@ -433,15 +433,17 @@ typedef enum {
                                    pipelining, 0 default (2 layer chunks), n chunks */
     SSA_OPT_QKV_DEBUG = 12,     /* fused projection experiments: 0 off, 1 skip the epilogue */
     SSA_OPT_CM_MERGE = 13,      /* split-KV merge of single-layer tcgen05 calls: 2 (default)
-                                   group-barrier merge when the plan fits one wave of
-                                   single CTAs (every CTA of a group writes its partial,
-                                   meets the group at a barrier in global memory and
-                                   merges a row block; no cluster, no second kernel),
-                                   else as 1; 1 cluster plans, groups over several
-                                   clusters merged by a separate kernel (programmatic
-                                   launch right behind the attention kernel); 0 as 1 but
-                                   the last arriving CTA merges inside the attention
-                                   kernel.  With SSA_OPT_CLUSTER > 0 the cluster plans */
+                                   query-plane calls take the group-barrier merge when the
+                                   plan fits one wave of single CTAs (every CTA of a group
+                                   writes its partial, meets the group at a barrier in
+                                   global memory and merges a row block; no cluster, no
+                                   second kernel), other calls as 1; 3 the group-barrier
+                                   merge for data-plane calls too; 1 cluster plans, groups
+                                   over several clusters merged by a separate kernel
+                                   (programmatic launch right behind the attention
+                                   kernel); 0 as 1 but the last arriving CTA merges inside
+                                   the attention kernel.  With SSA_OPT_CLUSTER > 0 the
+                                   cluster plans */
     SSA_OPT_L2_HINT = 14,       /* KV pool tiles loaded with an L2 evict-first hint: 0 (default)
                                    when no key tile of the launch is read by two CTAs, 1 never,
                                    2 always */

@@ -591,10 +591,12 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
         // candidates: clusters of C CTAs (DSMEM merge + merge kernel for groups over
         // several clusters), and the group-barrier merge (C = 1, one wave, gm_reduce)
         // (the group-barrier plan, when it applies, is taken without comparing costs:
-        // measured faster on the per-layer query, whose merge it keeps inside the kernel)
+        // measured faster on the per-layer query, whose merge it keeps inside the kernel;
+        // the per-layer append (SHARED pairs) is faster on the cluster plans: 141-143 vs
+        // 148 us/layer, scripts/append_ab.py)
         for (int C : {0, 1, 2, 3, 4, 5, 6, 7, 8, 16}) {
           const bool gb = C == 0;
-          if (gb && (opt_cm_merge != 2 || opt_cluster > 0)) continue;
+          if (gb && (opt_cm_merge < 2 || opt_cluster > 0 || (opt_cm_merge == 2 && !query_plane))) continue;
           if (!gb && fresh.gbar) break;
           const int Ck = gb ? 1 : C;
           if (opt_cluster > 0 && Ck != opt_cluster) continue;
@@ -1091,7 +1093,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
       st->opt_cluster = value;
       break;
     case SSA_OPT_PDL: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_pdl = value; break;
-    case SSA_OPT_CM_MERGE: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
+    case SSA_OPT_CM_MERGE: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
     case SSA_OPT_L2_HINT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_l2_hint = value; break;
     case SSA_OPT_PIPE_CHUNKS: if (value < -1 || value > 64) return SSA_ERR_INVALID_ARG; st->opt_pipe_chunks = value; break;
     case SSA_OPT_QKV_DEBUG: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_qkv_debug = value; break;

@@ -159,7 +159,7 @@ for kv in (None, "e4m3"):
             check(f"{kv or 'bf16'} per-layer query {nq} C={C} merge={merge} plan={st.last_plan()}", from_dev(Ol), want,
                   "bf16")
     tok = n
-    for C, merge in ((4, 1), (0, 2)):   # cluster plan / group-barrier merge
+    for C, merge in ((4, 1), (0, 3)):   # cluster plan / group-barrier merge
         st.set_option(ssa.OPT_CLUSTER, C)
         st.set_option(ssa.OPT_CM_MERGE, merge)
         Qa, Ka, Va = gen_qkv(spec, L, hq, hkv, d, 0, tok, 200)

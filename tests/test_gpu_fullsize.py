@@ -157,3 +157,46 @@ def test_multitenant_full_size_sampled(cuda):
                         session=61)
     assert ok, ("stateless", e)
     st.close()
+
+
+@pytest.mark.parametrize("q_len", [1, 32])
+def test_per_layer_query_full_size_sampled(cuda, q_len):
+    """bench.py's per_layer leg: the 32-token (and 1-token) query at n=32,768 issued as 32
+    single-layer calls (Alg. 2 L295 layer by layer) captured in one CUDA graph and replayed
+    twice -- the launch configuration the bench times: group-barrier merge, 136 CTAs, 17
+    key ranges per KV head merged in the kernel (R-11).  Sampled rows of layers 0, 13, 31
+    against the fp64 oracle; the replay reproduces the eager call bit for bit."""
+    import torch
+    import paper_2605_13784_b200 as ssa
+    n = CFG["n_ctx"]
+    st = ssa.Store(L, HQ, HKV, D, page_size=P, num_pages=n // P + 16, max_sessions=2, dtype="bf16")
+    spec = streams.StreamSpec("market", seed=2)
+    sid = bench.build_session(st, torch, cuda, spec, n)
+    q, k, v = bench.gen_new(torch, cuda, spec, 1, 0, q_len)
+    o_eager = torch.empty_like(q)
+    s = torch.cuda.Stream(device=cuda)
+
+    def per_layer(o):
+        for l in range(L):
+            st.session_query(sid, q[l:l + 1], k[l:l + 1], v[l:l + 1], o[l:l + 1], layer=l, stream=s)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        per_layer(o_eager)
+    s.synchronize()
+    plan = st.last_plan()
+    assert plan["gbar"] == 1 and plan["max_split"] > 1, plan
+    o = torch.full_like(q, float("nan"))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        per_layer(o)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o.view(torch.int16), o_eager.view(torch.int16))
+    oh = from_dev(o)
+    toks = list(range(q_len)) if q_len <= 4 else [0, 1, 15, 31]
+    for layer in (0, 13, 31):
+        kc, vc = _cache(spec, layer, n)
+        ok, e = _check_rows(oh[layer], spec, layer, kc, vc, 1, 0, q_len, toks, [0, 3, 4, 17, 30, 31])
+        assert ok, (layer, e)
+    st.close()

@@ -600,7 +600,7 @@ def test_cluster_merge_per_layer_append(cuda, C):
     spec = streams.StreamSpec("market", seed=63)
     st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=256)
     if C == "gbar":
-        st.set_option(ssa.OPT_CM_MERGE, 2)
+        st.set_option(ssa.OPT_CM_MERGE, 3)   # group-barrier merge on the data plane too
     else:
         st.set_option(ssa.OPT_CLUSTER, C)
     ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=256)
@@ -616,6 +616,8 @@ def test_cluster_merge_per_layer_append(cuda, C):
         for l in range(L):
             st.append_layer(sid, t, l, Qd[l:l + 1], Kd[l:l + 1], Vd[l:l + 1], O[l:l + 1])
         st.append_commit(sid, t)
+        if C == "gbar":
+            assert st.last_plan()["gbar"] == 1, st.last_plan()
         Oref, _ = ref.session_append(rsid, Q, K, V)
         ok, e = within(from_dev(O), Oref, "bf16")
         assert ok, (m, e)
