@@ -20,7 +20,7 @@ for m in (256, 32):
     Q = torch.empty(m, hq, d, dtype=torch.bfloat16, device=dev)
     K = torch.empty(m, hkv, d, dtype=torch.bfloat16, device=dev)
     V = torch.empty_like(K)
-    for dbg, th in ((0, 5e5), (1, 5e5), (8, 5e5), (9, 5e5), (0, 5e5)):
+    for dbg, th in ((0, 5e5), (1, 5e5), (0, 0.0), (1, 0.0), (0, 5e5)):
         st.set_option(ssa.OPT_QKV_DEBUG, dbg)
         st.qkv_rope(X[0], W[0], Q, K, V, pos0=100, rope_theta=th, stream=gs)
         torch.cuda.synchronize()
