@@ -223,6 +223,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define SSA_POLY_PAIRS_OF_8 0
 #endif
 constexpr int kPolyPairsOf8 = SSA_POLY_PAIRS_OF_8;
+// Ring stages (per K / V ring) of pool tiles a programmatic launch requests before
+// griddepcontrol.wait.  The Q tile, requested after the wait, queues behind them: one
+// stage measured best on the per-layer query (31.7 vs 32.5 us/layer with a full ring,
+// 32.2 with none; scripts/r2b_early.sh)
+#ifndef SSA_EARLY_STAGES
+#define SSA_EARLY_STAGES 1
+#endif
 
 // ---------------------------------------------------------------- cluster merge (CM)
 // CM launches (AttnParams::cm_C = C >= 1): every unit belongs to a split group and
@@ -961,7 +968,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         // the previous layer finishes; Q and the tails (inputs) always come after it.
         int e0 = 0;
         if (p.pool_early)
-          while (e0 < E && e0 < NR && issue(e0, true)) ++e0;
+          while (e0 < E && e0 < min(NR, SSA_EARLY_STAGES) && issue(e0, true)) ++e0;
         griddep_wait();
         if (is_k && dup) {
           mbar_arrive_expect_tx(&bar.q_full, 2 * 2 * 32 * 128);

@@ -73,7 +73,7 @@ for q_len in (32, 1):
     print(f"LAYER q={q_len} all-layer call {ms * 1e3 / L:.1f} us/layer plan {st.last_plan()}", flush=True)
 
 st.set_option(ssa.OPT_PDL, 1)
-for cl, mk in ((0, 1), (4, 1), (0, 2)):
+for cl, mk in (((0, 1), (4, 1), (0, 2)) if os.environ.get("LAYER_APPEND", "1") != "0" else ()):
     st.set_option(ssa.OPT_CLUSTER, cl)
     st.set_option(ssa.OPT_CM_MERGE, mk)
     st.session_truncate(sid, n0)
