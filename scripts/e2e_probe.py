@@ -1,5 +1,6 @@
 """e2e query pieces on the bench session shape: device-only query, H2D / D2H copy times,
-and the host-buffer query with SSA_PIPE_CHUNKS (0 = unpipelined) from the environment."""
+and the host-buffer query under SSA_OPT_PIPE_CHUNKS settings (-1 unpipelined, 0 default,
+n chunks), interleaved over several rounds (tapered 1:3:3:1 chunks measured 1.14-1.19 ms vs 0.88-0.90 for 2, not kept)."""
 import os
 import sys
 
@@ -22,7 +23,7 @@ hO = torch.empty(O.shape, dtype=O.dtype).pin_memory()
 s = torch.cuda.Stream()
 
 
-def t(fn, n=10):
+def t(fn, n=20):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -35,12 +36,14 @@ def t(fn, n=10):
     return a.elapsed_time(b) / n
 
 
-print("device query ms", t(lambda: st.session_query(sid, Q, K, V, O, stream=s)))
-os.environ["SSA_PIPE_FORCE"] = "1"
-print("device query, chunked ms", t(lambda: st.session_query(sid, Q, K, V, O, stream=s)))
-del os.environ["SSA_PIPE_FORCE"]
+print("E2E device query ms", t(lambda: st.session_query(sid, Q, K, V, O, stream=s)))
 with torch.cuda.stream(s):
-    print("H2D Q,K,V ms", t(lambda: [x.copy_(h, non_blocking=True) for x, h in ((Q, hQ), (K, hK), (V, hV))]))
-    print("D2H O ms", t(lambda: hO.copy_(O, non_blocking=True)))
-print("host query ms (SSA_PIPE_CHUNKS=%s)" % os.environ.get("SSA_PIPE_CHUNKS"),
-      t(lambda: st.session_query(sid, hQ, hK, hV, hO, stream=s)))
+    print("E2E H2D Q,K,V ms", t(lambda: [x.copy_(h, non_blocking=True) for x, h in ((Q, hQ), (K, hK), (V, hV))]))
+    print("E2E D2H O ms", t(lambda: hO.copy_(O, non_blocking=True)))
+res = {}
+for rnd in range(3):
+    for pc in (0, 4, 8, -1):
+        st.set_option(ssa.OPT_PIPE_CHUNKS, pc)
+        res.setdefault(pc, []).append(t(lambda: st.session_query(sid, hQ, hK, hV, hO, stream=s)))
+for pc, v in res.items():
+    print(f"E2E host query pipe_chunks={pc}: " + " ".join(f"{x:.3f}" for x in v) + " ms")
