@@ -15,8 +15,10 @@ import paper_2605_13784_b200 as ssa  # noqa: E402
 CFG = bench.CFG
 dev = torch.device("cuda:0")
 n0 = CFG["n_ctx"] - CFG["m_append"]
+KV = os.environ.get("KV", "bf16")   # "e4m3": an E4M3 KV store (bench fp8_kv leg scales)
+kvkw = dict(kv_format="e4m3", k_scale=1 / 32, v_scale=1 / 32) if KV == "e4m3" else {}
 st = ssa.Store(CFG["L"], CFG["hq"], CFG["hkv"], CFG["d"], page_size=CFG["P"], num_pages=CFG["n_ctx"] // CFG["P"] + 16,
-               max_sessions=4, dtype="bf16")
+               max_sessions=4, dtype="bf16", **kvkw)
 spec = streams.StreamSpec("market", seed=2)
 sid = bench.build_session(st, torch, dev, spec, n0)
 Qa, Ka, Va = bench.gen_new(torch, dev, spec, 0, n0, CFG["m_append"])
@@ -37,6 +39,6 @@ for kind in ("append", "query"):
     n = lib.ssa_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
     print(kind, "trace bytes", n)
     os.makedirs("gpurun_out", exist_ok=True)
-    np.save(f"gpurun_out/trace_{kind}.npy", buf[:n1].reshape(4, 12, 256, 2).copy())
-    np.save(f"gpurun_out/trace2_{kind}.npy", buf[n1:].reshape(4, 2, 4, 256, 2).copy())
+    np.save(f"gpurun_out/trace_{KV}_{kind}.npy", buf[:n1].reshape(4, 12, 256, 2).copy())
+    np.save(f"gpurun_out/trace2_{KV}_{kind}.npy", buf[n1:].reshape(4, 2, 4, 256, 2).copy())
     buf[:] = 0
