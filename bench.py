@@ -403,7 +403,8 @@ def leg_flash(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_ctx):
 
 def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Qa, Ka, Va, Oa, Qq, Kq, Vq, Oq):
     """BJ.configs[1] curves vs context n: the same session truncated (SeqRemove)
-    to n in {1k, 2k, 4k, 8k, 16k, 32,512}; per n the 32-token query and the 256-token append over
+    to n in {4k, 8k, 16k, 32,512} (a fresh n-token session for 1k and 2k: the bench session's
+    Region 0 is its first 4k tokens, R-17); per n the 32-token query and the 256-token append over
     32 layers (kernel CUDA events, as the headline), as GB/s and TFLOP/s of their algorithmic
     bytes / FLOPs.  At 16k and 8k also the BJ.configs[3] batch (64 x 32-token
     Flash Queries in one launch over 32 layers; 32k is the flash_queries leg).  Runs right
@@ -417,8 +418,14 @@ def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Q
     FQ, FK, FV = (torch.cat([x[j] for x in fq], dim=1).contiguous() for j in range(3))
     FO = torch.empty_like(FQ)
     del fq
+    sid_main = sid
     for n in (n_top, 16384, 8192, 4096, 2048, 1024):
-        st.session_truncate(sid, n)
+        if n >= 4096:
+            st.session_truncate(sid_main, n)
+        else:   # below the bench session's 4k Region 0 (R-17): a fresh n-token session
+            if sid != sid_main:
+                st.session_destroy(sid)
+            sid = build_session_n(st, torch, dev, spec, n)
         st.set_option(ssa.OPT_TIMING, 1)
         st.timing(reset=True)
         _timed(torch, stream, lambda: st.session_query(sid, Qq, Kq, Vq, Oq, stream=stream), steps, 0)
@@ -448,7 +455,8 @@ def leg_nsweep(st, sid, torch, dev, spec, stream, peaks, steps, warmup, n_top, Q
             ff = 64 * append_flops_per_layer(n, 32, hq, d) * L
             out[f"n{n}"]["flash_64x32"] = {"ms_32_layers": fms, "tflops": ff / (fms * 1e-3) / 1e12,
                                            "tc_frac": ff / (fms * 1e-3) / 1e12 / peaks["bf16_tflops"]}
-    st.session_truncate(sid, 1024)
+    if sid != sid_main:
+        st.session_destroy(sid)
     return out
 
 

@@ -652,7 +652,14 @@ __device__ __forceinline__ void gm_merge_items(const AttnParams& p, const WorkUn
   }
 }
 
-__device__ __forceinline__ void gm_reduce(const AttnParams& p, const WorkUnit& w, int t, int nthr, int bar_id) {
+// gen0: the group's generation word, read by thread t == 0 before this CTA's partial
+// rows were written (any time after griddepcontrol.wait and before the arrival: only
+// this launch's last arriver changes it), so the read is off the barrier's critical path.
+__device__ __forceinline__ uint32_t gm_generation(const AttnParams& p, int group) {
+  return ld_acquire_u32(reinterpret_cast<uint32_t*>(p.cm_tickets) + ((int64_t)blockIdx.y * p.n_groups + group) * 2 + 1);
+}
+__device__ __forceinline__ void gm_reduce(const AttnParams& p, const WorkUnit& w, int t, int nthr, int bar_id,
+                                          uint32_t gen0) {
   const int ly = blockIdx.y;
   const int K = p.groups[w.group].n_splits;
   if (t == 0) {
@@ -660,7 +667,6 @@ __device__ __forceinline__ void gm_reduce(const AttnParams& p, const WorkUnit& w
     // CTA barrier and the fence); the last arriver resets the counter for the next launch
     // (relaxed: kernel boundaries order it) and releases the bumped generation
     uint32_t* c = reinterpret_cast<uint32_t*>(p.cm_tickets) + ((int64_t)ly * p.n_groups + w.group) * 2;
-    const uint32_t gen0 = ld_acquire_u32(c + 1);
     __threadfence();
     uint32_t old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(c) : "memory");
@@ -800,12 +806,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     g_gtrace[(p.layer0 + blockIdx.y) & 31][blockIdx.x][7] = smid;
   }
 #endif
-  const TcPair pr = p.pairs[blockIdx.x];
-  const WorkUnit w0 = p.units[pr.ua];
+  const TcPair& pr = p.pairs[blockIdx.x];   // units, segments, split counts in one place
+  const WorkUnit w0 = pr.wa;
   WorkUnit w1 = w0;
   int nt1 = 0;
   if (pr.ub >= 0) {
-    w1 = p.units[pr.ub];
+    w1 = pr.wb;
     nt1 = w1.tile_hi - w1.tile_lo;
   }
   const int nt0 = w0.tile_hi - w0.tile_lo;
@@ -822,8 +828,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
   // independently (K loads run further ahead).
   // CM CTA whose groups it holds alone (cluster of 1, one cluster per group): the
   // epilogue writes O straight from the slots, no exchange buffer / reduce
-  const bool cm_direct = p.cm_C == 1 && p.groups[w0.group].n_splits == 1 &&
-                         (pr.ub < 0 || p.groups[w1.group].n_splits == 1);
+  const bool cm_direct = p.cm_C == 1 && pr.splits_a == 1 && (pr.ub < 0 || pr.splits_b == 1);
   // the epilogue stages rows in the ring (exchange buffer, or a split pair's slot merge)
   const bool ring_stage = p.cm_C > 0 && (!cm_direct || (pr.same_q && pr.ub >= 0));
   const int NK = 3;
@@ -908,7 +913,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         if (p.pool_early)
           for (int k = 0; k < (pr.ub >= 0 ? 2 : 1); ++k) {
             const WorkUnit& w = k ? w1 : w0;
-            const SegDesc sg = p.segs[w.seg];
+            const SegDesc& sg = k ? pr.sb : pr.sa;
             if (w.tile_hi > w.tile_lo && w.tile_lo * kBN < sg.n_slots)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(sg.pages + (w.tile_lo * kBN) / p.P));
           }
@@ -930,7 +935,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           else if (e - nsh < 2 * m01) { k = (e - nsh) & 1; j = nsh + ((e - nsh) >> 1); }
           else { k = nt0 > nt1 ? 0 : 1; j = nsh + m01 + (e - nsh - 2 * m01); }
           const WorkUnit& w = k ? w1 : w0;
-          const SegDesc sg = p.segs[w.seg];
+          const SegDesc& sg = k ? pr.sb : pr.sa;
           const int tile = w.tile_lo + j;
           const int n_pool_tiles = (sg.n_slots + kBN - 1) / kBN;
           if (pool_only && tile >= n_pool_tiles) return false;
@@ -972,7 +977,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         griddep_wait();
         if (is_k && dup) {
           mbar_arrive_expect_tx(&bar.q_full, 2 * 2 * 32 * 128);
-          const int32_t qrow = (int32_t)(in_l + p.segs[w0.seg].row0 + w0.q_tok0);
+          const int32_t qrow = (int32_t)(in_l + pr.sa.row0 + w0.q_tok0);
           for (int c = 0; c < 2; ++c)
             for (int rb = 0; rb < 2; ++rb)
               tma_load_3d(q_buf[0] + c * kChunkBytes + rb * 32 * 128, &maps.q32, &bar.q_full, c * 64,
@@ -982,7 +987,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
           mbar_arrive_expect_tx(&bar.q_full, nq * kSlotBytes);
           for (int k = 0; k < nq; ++k) {
             const WorkUnit& w = k ? w1 : w0;
-            const int32_t qrow = (int32_t)(in_l + p.segs[w.seg].row0 + w.q_tok0);
+            const int32_t qrow = (int32_t)(in_l + (k ? pr.sb : pr.sa).row0 + w.q_tok0);
             for (int c = 0; c < 2; ++c)
               tma_load_3d(q_buf[k] + c * kChunkBytes, &maps.q, &bar.q_full, c * 64, w.kv_head * p.G, qrow);
           }
@@ -1065,8 +1070,9 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     const bool active = (k == 0) || pr.ub >= 0;
     const WorkUnit w = k ? w1 : w0;
     const int nt = k ? nt1 : nt0;
+    uint32_t gm_gen0 = 0;   // group-barrier generation (thread t == 0 of a merging group)
     if (active) {
-      const SegDesc sg = p.segs[w.seg];
+      const SegDesc sg = k ? pr.sb : pr.sa;
       const int r = threadIdx.x - 128 - 128 * k;   // TMEM lane
       const int roff = (dup && k == 1) ? 32 : 0;    // tile row of this slot's first live row
       const int rr = r - roff;                      // row of the unit's q tile
@@ -1205,6 +1211,9 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         tc_fence_after();
       }
       griddep_wait();   // before the first global write (O / partials of the previous grid's readers)
+      // group-barrier launch: the arriving thread of this slot's group reads its generation now
+      if (p.cm_gbar && (k ? pr.splits_b : pr.splits_a) > 1 && (threadIdx.x == 128 || (two_q && threadIdx.x == 256)))
+        gm_gen0 = gm_generation(p, w.group);
       const float inv_l = (l_run > 0.f ? 1.f / l_run : 0.f) * (F8 ? p.o_scale : 1.f);   // F8: V scale
       const float lse = l_run > 0.f ? m_run * c + __log2f(l_run) : -CUDART_INF_F;
       const int h = w.kv_head * G + (rr >= 0 ? rr : 0) % G;
@@ -1227,8 +1236,8 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         // group's global partial `split` (merged after the group barrier, gm_reduce)
         float* gdst = nullptr;
         float* glse = nullptr;
-        if (p.cm_gbar && !cm_direct && p.groups[w.group].n_splits > 1) {
-          const int64_t ps = (int64_t)ly * p.n_units + p.groups[w.group].unit0 + w.split;
+        if (p.cm_gbar && !cm_direct && (k ? pr.splits_b : pr.splits_a) > 1) {
+          const int64_t ps = (int64_t)ly * p.n_units + (k ? pr.unit0_b : pr.unit0_a) + w.split;
           gdst = p.part_o + ps * kM * kD;
           glse = p.part_lse + ps * kM;
         }
@@ -1314,12 +1323,12 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
     if (p.cm_C > 0 && !cm_direct) {
       cm_sync(p.cm_C);   // every CTA of the cluster has staged its rows
       GTRACE_T(true, 9);
-      const bool gm_k = p.cm_gbar && p.groups[(k && two_q ? w1 : w0).group].n_splits > 1;
+      const bool gm_k = p.cm_gbar && (k && two_q ? pr.splits_b : pr.splits_a) > 1;
       if (gm_k) {
         // group-barrier merge: two q tiles -> warpgroup k merges slot k's group; a split
         // pair's single group is merged by both warpgroups
         const int t = threadIdx.x - 128 - (two_q ? 128 * k : 0);
-        gm_reduce(p, two_q && k ? w1 : w0, t, two_q ? 128 : 256, two_q ? 1 + k : 3);
+        gm_reduce(p, two_q && k ? w1 : w0, t, two_q ? 128 : 256, two_q ? 1 + k : 3, gm_gen0);
       } else if (k < (two_q ? 2 : 1)) {
         const float* X = reinterpret_cast<const float*>(k_base) + k * kXFloats;
         const WorkUnit& wk = k ? w1 : w0;

@@ -58,10 +58,17 @@ struct Group {
 // Flash Queries over one cached pool).  Later tiles are private to a slot and
 // loaded separately (own-token tails; the two halves of a split).  same_q: both
 // slots use one q tile (a split pair), so only one Q buffer is needed.
+// The host fills the copies below before the upload: a CTA reads its units, their
+// segments and their groups' split counts in one round of independent loads (no
+// pairs -> units -> segments / groups dependency chain in the kernel prologue).
 struct TcPair {
   int32_t ua, ub;     // unit indices (ub = -1: single slot)
   int32_t n_shared;   // leading tiles shared by both slots
   int32_t same_q;
+  int32_t splits_a, splits_b;   // Group::n_splits of the units' groups (0: no group)
+  int32_t unit0_a, unit0_b;     // Group::unit0 of the units' groups
+  WorkUnit wa, wb;              // units[ua], units[ub] (wb = wa for a single slot)
+  SegDesc sa, sb;               // segs[wa.seg], segs[wb.seg]
 };
 
 struct AttnParams {

@@ -621,6 +621,17 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
         }
       }
       for (auto& g : plan.groups) fresh.max_split = std::max(fresh.max_split, g.n_splits);
+      // per-CTA copies of the units, segments and group split counts (TcPair)
+      for (TcPair& pr : fresh.pairs) {
+        pr.wa = plan.units[pr.ua];
+        pr.wb = pr.ub >= 0 ? plan.units[pr.ub] : pr.wa;
+        pr.sa = segs[pr.wa.seg];
+        pr.sb = segs[pr.wb.seg];
+        pr.splits_a = pr.wa.group >= 0 ? plan.groups[pr.wa.group].n_splits : 0;
+        pr.splits_b = pr.wb.group >= 0 ? plan.groups[pr.wb.group].n_splits : 0;
+        pr.unit0_a = pr.wa.group >= 0 ? plan.groups[pr.wa.group].unit0 : 0;
+        pr.unit0_b = pr.wb.group >= 0 ? plan.groups[pr.wb.group].unit0 : 0;
+      }
       // L2 evict-first pays only when no key tile of the launch is read twice: one q-tile
       // group per (cached pool, KV head) -- not appends, multi-tile queries or Flash batches
       {
