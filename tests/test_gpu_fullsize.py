@@ -200,3 +200,56 @@ def test_per_layer_query_full_size_sampled(cuda, q_len):
         ok, e = _check_rows(oh[layer], spec, layer, kc, vc, 1, 0, q_len, toks, [0, 3, 4, 17, 30, 31])
         assert ok, (layer, e)
     st.close()
+
+
+def test_fp8_bench_config_full_size_sampled(cuda):
+    """bench.py's fp8_kv leg: BJ.configs[1] on an E4M3 KV store (k_scale = v_scale = 1/32,
+    reading R-22): n=32,512 bulk-loaded -> 256-token append (all layers, one call) ->
+    32-token query at n=32,768.  Sampled rows of layers 0 and 31 against the fp64 oracle
+    over the dequantized stream (codes computed by the oracle's own e4m3_encode); the
+    appended codes read back from the pages equal the oracle's codes bit for bit."""
+    import torch
+    import paper_2605_13784_b200 as ssa
+    ks = vs = 1.0 / 32
+    n0, m_app, q_len = CFG["n_ctx"] - CFG["m_append"], CFG["m_append"], CFG["q_len"]
+    st = ssa.Store(L, HQ, HKV, D, page_size=P, num_pages=CFG["n_ctx"] // P + 16, max_sessions=4, dtype="bf16",
+                   kv_format="e4m3", k_scale=ks, v_scale=vs)
+    spec = streams.StreamSpec("market", seed=2)
+    sid = bench.build_session(st, torch, cuda, spec, n0)
+    Qa, Ka, Va = bench.gen_new(torch, cuda, spec, 0, n0, m_app)
+    Oa = torch.empty_like(Qa)
+    Qq, Kq, Vq = bench.gen_new(torch, cuda, spec, 1, 0, q_len)
+    Oq = torch.empty_like(Qq)
+    st.session_append(sid, Qa, Ka, Va, Oa)
+    st.session_query(sid, Qq, Kq, Vq, Oq)
+    torch.cuda.synchronize()
+    Oa_h, Oq_h = from_dev(Oa), from_dev(Oq)
+
+    def deq(bits, scale):
+        return oracle.e4m3_decode(oracle.e4m3_encode(bits, scale)) * scale
+
+    heads = [0, 5, 13, 31]
+    for layer in (0, 31):
+        kc_b, vc_b = _cache(spec, layer, n0)
+        kc, vc = deq(kc_b, ks), deq(vc_b, vs)
+        qa = _np(spec, 0, 0, layer, streams.TENSOR_Q, n0, m_app, HQ)
+        ka = _np(spec, 0, 0, layer, streams.TENSOR_K, n0, m_app, HKV)
+        va = _np(spec, 0, 0, layer, streams.TENSOR_V, n0, m_app, HKV)
+        toks = [0, 1, 31, 32, 127, 128, 200, 255]
+        want, _ = oracle.segment_rows(kc, vc, qa, deq(ka, ks), deq(va, vs), HKV, oracle.default_scale(D), toks,
+                                      heads)
+        ok, e = within(Oa_h[layer][np.ix_(toks, heads)], want, "bf16")
+        assert ok, ("append", layer, e)
+        kb, vb = st.read_kv(sid, layer, n0, m_app)   # E4M3 codes
+        assert np.array_equal(kb, oracle.e4m3_encode(ka, ks))
+        assert np.array_equal(vb, oracle.e4m3_encode(va, vs))
+        kc2 = np.concatenate([kc, deq(ka, ks)])
+        vc2 = np.concatenate([vc, deq(va, vs)])
+        qq = _np(spec, 0, 1, layer, streams.TENSOR_Q, 0, q_len, HQ)
+        kq = _np(spec, 0, 1, layer, streams.TENSOR_K, 0, q_len, HKV)
+        vq = _np(spec, 0, 1, layer, streams.TENSOR_V, 0, q_len, HKV)
+        want, _ = oracle.segment_rows(kc2, vc2, qq, deq(kq, ks), deq(vq, vs), HKV, oracle.default_scale(D),
+                                      list(range(q_len)), heads)
+        ok, e = within(Oq_h[layer][:, heads], want, "bf16")
+        assert ok, ("query", layer, e)
+    st.close()
