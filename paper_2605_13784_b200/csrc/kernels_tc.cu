@@ -226,7 +226,7 @@ constexpr int kPolyPairsOf8 = SSA_POLY_PAIRS_OF_8;
 // Ring stages (per K / V ring) of pool tiles a programmatic launch requests before
 // griddepcontrol.wait.  The Q tile, requested after the wait, queues behind them: one
 // stage measured best on the per-layer query (31.7 vs 32.5 us/layer with a full ring,
-// 32.2 with none; scripts/r2b_early.sh)
+// 32.2 with none; scripts/early_stages_ab.sh)
 #ifndef SSA_EARLY_STAGES
 #define SSA_EARLY_STAGES 1
 #endif
