@@ -492,7 +492,7 @@ def leg_per_layer(st, sid, torch, dev, spec, stream, peaks, steps, n0, Qa, Ka, V
         out[f"query_per_layer_graph_q{qn}"] = {
             "us_per_layer": ms * 1e3 / L, "ms_32_layers": ms, "gbs": b * L / (ms * 1e-3) / 1e9,
             "hbm_frac": b * L / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-            "plan": {"ctas": plan["ctas"], "cluster": plan["cm_C"], "ctas_or_clusters_per_group": plan["max_split"], "group_barrier_merge": bool(plan["gbar"])}}
+            "plan": {"ctas": plan["ctas"], "cluster": plan["cm_C"], "ctas_or_clusters_per_group": plan["max_split"], "group_plan": bool(plan["gbar"])}}
         ms_all = _timed(torch, stream, lambda: st.session_query(sid, q, k, v, o, stream=stream), steps, 3)
         out[f"query_per_layer_graph_q{qn}"]["all_layer_call_us_per_layer"] = ms_all * 1e3 / L
     st.session_truncate(sid, n0)
@@ -525,7 +525,7 @@ def leg_per_layer(st, sid, torch, dev, spec, stream, peaks, steps, n0, Qa, Ka, V
     out["append_per_layer_graph"] = {
         "us_per_layer": ms * 1e3 / L, "ms_32_layers": ms, "tflops": fl * L / (ms * 1e-3) / 1e12,
         "tc_frac": fl * L / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"], "tok_per_s": m_app / (ms * 1e-3),
-        "plan": {"ctas": plan["ctas"], "cluster": plan["cm_C"], "ctas_or_clusters_per_group": plan["max_split"], "group_barrier_merge": bool(plan["gbar"])},
+        "plan": {"ctas": plan["ctas"], "cluster": plan["cm_C"], "ctas_or_clusters_per_group": plan["max_split"], "group_plan": bool(plan["gbar"])},
         "what": "scatter + attention per layer (graph of 64 kernels), FLOPs of the attention only"}
     out["workload"] = "BJ.configs[1] session (n=32,768 for queries, 32,512 -> 32,768 for the append)"
     out["note"] = "device time of the CUDA-graph replay (events on the stream), includes launch gaps"

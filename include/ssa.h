@@ -433,17 +433,17 @@ typedef enum {
                                    pipelining, 0 default (2 layer chunks), n chunks */
     SSA_OPT_QKV_DEBUG = 12,     /* fused projection experiments: 0 off, 1 skip the epilogue */
     SSA_OPT_CM_MERGE = 13,      /* split-KV merge of single-layer tcgen05 calls: 2 (default)
-                                   query-plane calls take the group-barrier merge when the
-                                   plan fits one wave of single CTAs (every CTA of a group
-                                   writes its partial, meets the group at a barrier in
-                                   global memory and merges a row block; no cluster, no
-                                   second kernel), other calls as 1; 3 the group-barrier
-                                   merge for data-plane calls too; 1 cluster plans, groups
-                                   over several clusters merged by a separate kernel
-                                   (programmatic launch right behind the attention
-                                   kernel); 0 as 1 but the last arriving CTA merges inside
-                                   the attention kernel.  With SSA_OPT_CLUSTER > 0 the
-                                   cluster plans */
+                                   query-plane calls take the group plan when it fits one
+                                   wave of single CTAs: every CTA of a group writes its
+                                   partial and exits, a small merge kernel launched right
+                                   behind (programmatic launch) merges each group; other
+                                   calls as 1; 3 the group plan for data-plane calls too;
+                                   4 / 5 as 2 / 3 but the group's CTAs meet at a barrier in
+                                   global memory and merge inside the attention kernel;
+                                   1 cluster plans, groups over several clusters merged by
+                                   a separate kernel; 0 as 1 but the last arriving CTA
+                                   merges inside the attention kernel.  With
+                                   SSA_OPT_CLUSTER > 0 the cluster plans */
     SSA_OPT_L2_HINT = 14,       /* KV pool tiles loaded with an L2 evict-first hint: 0 (default)
                                    when no key tile of the launch is read by two CTAs, 1 never,
                                    2 always */
@@ -453,8 +453,8 @@ ssa_status ssa_store_set_option(ssa_store_t store, int32_t option, int64_t value
 /* Shape of the store's last attention launch (a test / tuning aid):
  * out[0] work units, [1] split groups, [2] CTAs per layer, [3] cluster size of a
  * cluster-merge launch (0: combine kernel or SIMT), [4] largest split count
- * (clusters per group for a cluster-merge launch), [5] 1 if split groups were merged
- * after a group barrier inside the attention kernel (SSA_OPT_CM_MERGE = 2). */
+ * (clusters per group for a cluster-merge launch), [5] 1 for a group plan (single CTAs
+ * in one wave, SSA_OPT_CM_MERGE 2-5: merged by the merge kernel or the group barrier). */
 ssa_status ssa_debug_last_plan(ssa_store_t store, int64_t out[6]);
 
 /* Kernel timing recorded while SSA_OPT_TIMING is on, per kernel class

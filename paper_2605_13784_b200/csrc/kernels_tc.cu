@@ -688,6 +688,61 @@ __device__ __forceinline__ void gm_reduce(const AttnParams& p, const WorkUnit& w
     gm_merge_items<24>(p, w, K, t, nthr);
 }
 
+// Group-split launches (AttnParams::cm_gsplit): the attention CTAs leave their partials
+// (column-major float4 layout of cm_merge_rows) and exit; this grid, launched right
+// behind with programmatic dependent launch (its CTAs need no shared memory and sit
+// in griddepcontrol.wait while the attention grid drains), merges every group:
+// block (g, b, layer) takes items b * 256 .. of group g -- (row, 4 columns), rows
+// fastest within 8 -- with all K partial loads of an item in flight (R-11).
+template <int KMAX>
+__global__ void __launch_bounds__(256) gm_merge_kernel(const AttnParams p) {
+  griddep_launch_dependents();
+  const int g = blockIdx.x;
+  const int ly = blockIdx.z;
+  const Group gr = p.groups[g];
+  const int K = gr.n_splits;
+  const int G = p.G;
+  const int rows = gr.q_ntok * G;
+  const int it = blockIdx.y * 256 + threadIdx.x;
+  const int row = (it & 7) + 8 * ((it >> 3) / (kD / 4));
+  const int c = (it >> 3) % (kD / 4);
+  const SegDesc sg = p.segs[gr.seg];
+  griddep_wait();   // the attention grid's partials
+  if (K <= 1 || row >= rows) return;
+  const int64_t s0 = (int64_t)ly * p.n_units + gr.unit0;
+  const float4* po = reinterpret_cast<const float4*>(p.part_o) + s0 * (kM * kD / 4);
+  const float* pl = p.part_lse + s0 * kM;
+  float lj[KMAX];
+  float4 v[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < K) {
+      lj[j] = __ldcg(pl + (int64_t)j * kM + row);
+      v[j] = __ldcg(po + (int64_t)j * (kM * kD / 4) + c * kM + row);
+    }
+  float L = -CUDART_INF_F;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < K) L = fmaxf(L, lj[j]);
+  float ws = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < K) {
+      const float wt = lj[j] == -CUDART_INF_F ? 0.f : exp2f(lj[j] - L);
+      ws += wt;
+      acc.x = fmaf(wt, v[j].x, acc.x);
+      acc.y = fmaf(wt, v[j].y, acc.y);
+      acc.z = fmaf(wt, v[j].z, acc.z);
+      acc.w = fmaf(wt, v[j].w, acc.w);
+    }
+  const float inv = ws > 0.f ? 1.f / ws : 0.f;
+  const int64_t in_l = p.in_layer_stride ? (int64_t)ly * p.rows_per_layer : 0;
+  const int64_t orow = in_l + sg.row0 + gr.q_tok0 + row / G;
+  store_bf16x4(static_cast<__nv_bfloat16*>(p.O) + (orow * p.Hq + gr.kv_head * G + row % G) * kD + 4 * c,
+               make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+}
+
 // Groups spread over K > 1 clusters: merge the K block partials of every row
 // (log-sum-exp, R-11) -- a small grid launched right behind the attention
 // kernel (programmatic dependent launch: its prologue overlaps the attention
@@ -1236,7 +1291,7 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
         // group's global partial `split` (merged after the group barrier, gm_reduce)
         float* gdst = nullptr;
         float* glse = nullptr;
-        if (p.cm_gbar && !cm_direct && (k ? pr.splits_b : pr.splits_a) > 1) {
+        if ((p.cm_gbar || p.cm_gsplit) && !cm_direct && (k ? pr.splits_b : pr.splits_a) > 1) {
           const int64_t ps = (int64_t)ly * p.n_units + (k ? pr.unit0_b : pr.unit0_a) + w.split;
           gdst = p.part_o + ps * kM * kD;
           glse = p.part_lse + ps * kM;
@@ -1324,7 +1379,10 @@ attn_tc_kernel(const AttnParams p, const __grid_constant__ TcMaps maps, const in
       cm_sync(p.cm_C);   // every CTA of the cluster has staged its rows
       GTRACE_T(true, 9);
       const bool gm_k = p.cm_gbar && (k && two_q ? pr.splits_b : pr.splits_a) > 1;
-      if (gm_k) {
+      // group-split launch: the group's partial is written; gm_merge_kernel merges it
+      const bool gs_k = p.cm_gsplit && (k && two_q ? pr.splits_b : pr.splits_a) > 1;
+      if (gs_k) {
+      } else if (gm_k) {
         // group-barrier merge: two q tiles -> warpgroup k merges slot k's group; a split
         // pair's single group is merged by both warpgroups
         const int t = threadIdx.x - 128 - (two_q ? 128 * k : 0);
@@ -1501,6 +1559,22 @@ cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, int max_split, bo
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return rw == 8 ? cudaLaunchKernelEx(&cfg, cm_merge_kernel<8>, p) : cudaLaunchKernelEx(&cfg, cm_merge_kernel<1>, p);
+}
+
+cudaError_t launch_gm_merge(const AttnParams& p, int n_layers, int max_split, bool pdl, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_groups, kM / 8, n_layers);   // blocks of 256 items: 8 rows x 32 column groups
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (max_split <= 8) return cudaLaunchKernelEx(&cfg, gm_merge_kernel<8>, p);
+  if (max_split <= 16) return cudaLaunchKernelEx(&cfg, gm_merge_kernel<16>, p);
+  if (max_split <= 32) return cudaLaunchKernelEx(&cfg, gm_merge_kernel<32>, p);
+  return cudaErrorInvalidValue;
 }
 
 size_t tc_smem_bytes() { return (size_t)kNumSlots * kSlotBytes + sizeof(Bars) + 1024; }

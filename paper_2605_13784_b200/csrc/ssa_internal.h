@@ -112,6 +112,9 @@ struct AttnParams {
   // partials, meet at a barrier in cm_tickets ([layers][n_groups][2]: arrivals,
   // generation; zero at allocation) and merge in the same kernel (gm_reduce)
   int32_t cm_gbar;
+  // 1: as cm_gbar, but no barrier: the CTAs exit after writing their partials and
+  // gm_merge_kernel (a programmatic launch right behind) merges the groups
+  int32_t cm_gsplit;
   // pool tiles are loaded with an L2 evict-first hint (read once per launch)
   int32_t l2_evict_first;
   // FP8 KV variant (reading R-22): pools and Kt/Vt hold E4M3 codes; scale_log2

@@ -590,13 +590,18 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
         double best = -1.0;
         // candidates: clusters of C CTAs (DSMEM merge + merge kernel for groups over
         // several clusters), and the group-barrier merge (C = 1, one wave, gm_reduce)
-        // (the group-barrier plan, when it applies, is taken without comparing costs:
-        // measured faster on the per-layer query, whose merge it keeps inside the kernel;
-        // the per-layer append (SHARED pairs) is faster on the cluster plans: 141-143 vs
-        // 148 us/layer, scripts/append_ab.py)
+        // (the group plan, when it applies, is taken without comparing costs: measured
+        // faster on the per-layer query; its groups are merged by gm_merge_kernel right
+        // behind the attention grid (SSA_OPT_CM_MERGE 2 / 3: the next layer's CTAs take
+        // the SMs while it runs; 30.7 / 33.0 vs 32.3 / 33.6 us/layer for the 1- / 32-token
+        // query with the in-kernel group barrier, 4 / 5).  The per-layer append (SHARED
+        // pairs) is faster on the cluster plans: 141-143 vs 148 us/layer,
+        // scripts/append_ab.py)
         for (int C : {0, 1, 2, 3, 4, 5, 6, 7, 8, 16}) {
           const bool gb = C == 0;
-          if (gb && (opt_cm_merge < 2 || opt_cluster > 0 || (opt_cm_merge == 2 && !query_plane))) continue;
+          // SSA_OPT_CM_MERGE 2 / 4: query plane only; 3 / 5: both planes
+          if (gb && (opt_cm_merge < 2 || opt_cluster > 0 || ((opt_cm_merge == 2 || opt_cm_merge == 4) && !query_plane)))
+            continue;
           if (!gb && fresh.gbar) break;
           const int Ck = gb ? 1 : C;
           if (opt_cluster > 0 && Ck != opt_cluster) continue;
@@ -609,6 +614,7 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
             fresh.pairs = std::move(prs);
             fresh.cm_C = Ck;
             fresh.gbar = gb;
+            fresh.gsplit = gb && (opt_cm_merge == 2 || opt_cm_merge == 3);
           }
         }
       }
@@ -822,9 +828,11 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     // before this one on the stream is one of the store's pool writers
     ap.pool_early = (opt_pdl != 0 && !opt_timing && !(pool_writer_last && last_kernel_stream == st)) ? 1 : 0;
     ap.l2_evict_first = opt_l2_hint == 2 || (opt_l2_hint == 0 && E.l2_hint) ? 1 : 0;
-    const bool gbar = E.gbar && E.max_split > 1;
+    const bool gsplit = E.gsplit && E.max_split > 1;
+    const bool gbar = E.gbar && !E.gsplit && E.max_split > 1;
     const bool merge_in_kernel = E.cm_C > 0 && E.max_split > 1 && (opt_cm_merge == 0 || gbar);
     ap.cm_gbar = gbar ? 1 : 0;
+    ap.cm_gsplit = gsplit ? 1 : 0;
     if (merge_in_kernel) {
       // zeroed counters: [layers][groups][C] tickets, or [layers][groups][2] group barriers
       int32_t*& buf = gbar ? gb_tickets : tickets;
@@ -853,7 +861,10 @@ ssa_status ssa_store::run(std::vector<SegDesc>& segs, const IoSet& io, int64_t r
     note_kernel(st, false);
     if (E.cm_C > 0 && E.max_split > 1 && !merge_in_kernel) {   // groups over several clusters: merge kernel
       cudaEvent_t t1 = tick(st);
-      SSA_CUDA(this, launch_cm_merge(ap, n_layers, E.max_split, opt_pdl != 0 && !t1, st));
+      if (gsplit)
+        SSA_CUDA(this, launch_gm_merge(ap, n_layers, E.max_split, opt_pdl != 0 && !t1, st));
+      else
+        SSA_CUDA(this, launch_cm_merge(ap, n_layers, E.max_split, opt_pdl != 0 && !t1, st));
       if (t1) timed_push(query_plane ? 3 : 2, t1, tick(st));
       stats.kernel_launches++;
     }
@@ -1104,7 +1115,7 @@ ssa_status ssa_store_set_option(ssa_store_t st, int32_t option, int64_t value) {
       st->opt_cluster = value;
       break;
     case SSA_OPT_PDL: if (value < 0 || value > 1) return SSA_ERR_INVALID_ARG; st->opt_pdl = value; break;
-    case SSA_OPT_CM_MERGE: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
+    case SSA_OPT_CM_MERGE: if (value < 0 || value > 5) return SSA_ERR_INVALID_ARG; st->opt_cm_merge = value; break;
     case SSA_OPT_L2_HINT: if (value < 0 || value > 2) return SSA_ERR_INVALID_ARG; st->opt_l2_hint = value; break;
     case SSA_OPT_PIPE_CHUNKS: if (value < -1 || value > 64) return SSA_ERR_INVALID_ARG; st->opt_pipe_chunks = value; break;
     case SSA_OPT_QKV_DEBUG: if (value < 0 || value > 3) return SSA_ERR_INVALID_ARG; st->opt_qkv_debug = value; break;

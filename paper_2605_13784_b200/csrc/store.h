@@ -72,6 +72,7 @@ int tc_rows_tile();
 cudaError_t launch_attn_tc(const AttnParams& p, int n_layers, bool pdl, cudaStream_t s);
 size_t tc_smem_bytes();
 cudaError_t launch_cm_merge(const AttnParams& p, int n_layers, int max_split, bool pdl, cudaStream_t s);
+cudaError_t launch_gm_merge(const AttnParams& p, int n_layers, int max_split, bool pdl, cudaStream_t s);
 cudaError_t tc_configure(bool f8);
 int tc_max_active_clusters(int c, bool f8);
 bool tc_supported_shape(int D, int G, bool bf16);
@@ -120,7 +121,8 @@ struct ssa_store {
     std::vector<ssa::TcPair> pairs;
     int32_t cm_C = 0;          // cluster-merge launch (AttnParams::cm_C), 0 = combine kernel / SIMT
     int32_t max_split = 0;     // largest Group::n_splits
-    bool gbar = false;         // group-barrier merge (AttnParams::cm_gbar)
+    bool gbar = false;         // group-barrier plan (AttnParams::cm_gbar, or cm_gsplit when gsplit)
+    bool gsplit = false;       // merged by gm_merge_kernel instead of the in-kernel barrier
     bool l2_hint = false;      // every key tile is read by one CTA (no reuse in L2 to keep)
     int32_t n_app = 0;         // scatter segments
     int32_t app_tokens = 0;

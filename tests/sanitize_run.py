@@ -149,7 +149,7 @@ for kv in (None, "e4m3"):
     for nq in (1, 32):
         Qq, Kq, Vq = gen_qkv(spec, L, hq, hkv, d, 1, 0, nq)
         want = ref.session_query(rsid, Qq, Kq, Vq)
-        for C, merge in ((1, 1), (2, 1), (2, 0), (4, 1), (8, 1), (0, 2)):
+        for C, merge in ((1, 1), (2, 1), (2, 0), (4, 1), (8, 1), (0, 2), (0, 4)):
             st.set_option(ssa.OPT_CLUSTER, C)
             st.set_option(ssa.OPT_CM_MERGE, merge)
             Ol = torch.empty(Qq.shape, dtype=torch.bfloat16, device=dev)
@@ -159,7 +159,7 @@ for kv in (None, "e4m3"):
             check(f"{kv or 'bf16'} per-layer query {nq} C={C} merge={merge} plan={st.last_plan()}", from_dev(Ol), want,
                   "bf16")
     tok = n
-    for C, merge in ((4, 1), (0, 3)):   # cluster plan / group-barrier merge
+    for C, merge in ((4, 1), (0, 3), (0, 5)):   # cluster plan / group plan (merge kernel, group barrier)
         st.set_option(ssa.OPT_CLUSTER, C)
         st.set_option(ssa.OPT_CM_MERGE, merge)
         Qa, Ka, Va = gen_qkv(spec, L, hq, hkv, d, 0, tok, 200)

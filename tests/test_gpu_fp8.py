@@ -355,7 +355,7 @@ def test_fp8_sharded_partials_merge(cuda, world):
 
 
 @pytest.mark.parametrize("opt", ["cluster_1", "cluster_2", "cluster_8", "no_cluster_plan", "max_splits_16",
-                                 "group_barrier"])
+                                 "group_plan", "group_barrier"])
 def test_fp8_kernel_options(cuda, opt):
     """E4M3 store under the kernel options: forced cluster sizes of the single-layer
     cluster-merge plan, the LPT plan, a high split cap -- append, all-layer and per-layer
@@ -368,8 +368,10 @@ def test_fp8_kernel_options(cuda, opt):
         st.set_option(ssa.OPT_CLUSTER, int(opt.split("_")[1]))
     elif opt == "no_cluster_plan":
         st.set_option(ssa.OPT_CLUSTER, -1)
+    elif opt == "group_plan":
+        st.set_option(ssa.OPT_CM_MERGE, 3)   # group plan for single-layer calls of both planes, merge kernel
     elif opt == "group_barrier":
-        st.set_option(ssa.OPT_CM_MERGE, 3)   # group-barrier merge for single-layer calls of both planes
+        st.set_option(ssa.OPT_CM_MERGE, 5)   # group plan for both planes, in-kernel group barrier
     else:
         st.set_option(ssa.OPT_MAX_SPLITS, 16)
     Q, K, V = gen_qkv(spec, 2, LL["hq"], LL["hkv"], LL["d"], 0, 0, 3000)
@@ -392,7 +394,7 @@ def test_fp8_kernel_options(cuda, opt):
         Ol = torch.full(Qd.shape, float("nan"), dtype=torch.bfloat16, device=cuda)
         for l in range(2):
             st.session_query(sid, Qd[l:l + 1], Kd[l:l + 1], Vd[l:l + 1], Ol[l:l + 1], layer=l)
-        if opt == "group_barrier":
+        if opt in ("group_plan", "group_barrier"):
             assert st.last_plan()["gbar"] == 1, st.last_plan()
         ok, e = within(from_dev(Ol), want, "bf16")
         assert ok, ("per-layer query", nq, e)

@@ -540,7 +540,7 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
     want = ref.session_query(rsid, Qq, Kq, Vq)
     bound = _bound(ref, rsid, Qq, Kq, Vq, want)
     Qd, Kd, Vd = to_dev(Qq, cuda), to_dev(Kq, cuda), to_dev(Vq, cuda)
-    for C, merge in ((0, 1), (-1, 1), (1, 1), (1, 0), (2, 1), (2, 0), (4, 1), (4, 0), (6, 1), (8, 1), (0, 2)):
+    for C, merge in ((0, 1), (-1, 1), (1, 1), (1, 0), (2, 1), (2, 0), (4, 1), (4, 0), (6, 1), (8, 1), (0, 2), (0, 4)):   # 2: merge kernel, 4: group barrier
         st.set_option(ssa.OPT_CLUSTER, C)
         st.set_option(ssa.OPT_CM_MERGE, merge)   # separate merge kernel / last-arriving CTA
         splits = []
@@ -555,11 +555,11 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
             assert ok, (C, rep, e)
             ok, r = within_bound(from_dev(O), want, bound)
             assert ok, (C, rep, "bound", r)
-        if C in (1, 2) or merge == 2:
+        if C in (1, 2) or merge >= 2:
             assert max(splits) > 1, (C, splits)     # the cross-cluster (last-arriver) merge ran
-        if merge == 2:
-            assert plan["gbar"] == 1, plan          # group-barrier merge inside the kernel
-    assert st.stats()["cm_launches"] >= 2 * L * 11
+        if merge >= 2:
+            assert plan["gbar"] == 1, plan          # group-barrier plan (merged in the kernel / by gm_merge)
+    assert st.stats()["cm_launches"] >= 2 * L * 12
 
 
 @pytest.mark.parametrize("C", [1, 4, 8, "gbar"])
@@ -589,7 +589,7 @@ def test_cluster_merge_empty_ranges(cuda, C):
         st.close()
 
 
-@pytest.mark.parametrize("C", [0, 1, 2, 4, 8, "gbar"])
+@pytest.mark.parametrize("C", [0, 1, 2, 4, 8, "gbar", "gbar_barrier"])
 def test_cluster_merge_per_layer_append(cuda, C):
     """Per-layer data-plane steps (Alg. 1: append_begin / append_layer per layer / commit)
     under the cluster-merge plans: SHARED CTA pairs (two q tiles over the same keys), the key
@@ -600,7 +600,9 @@ def test_cluster_merge_per_layer_append(cuda, C):
     spec = streams.StreamSpec("market", seed=63)
     st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=256)
     if C == "gbar":
-        st.set_option(ssa.OPT_CM_MERGE, 3)   # group-barrier merge on the data plane too
+        st.set_option(ssa.OPT_CM_MERGE, 3)   # group plan on the data plane too (merge kernel)
+    elif C == "gbar_barrier":
+        st.set_option(ssa.OPT_CM_MERGE, 5)   # group plan on the data plane, in-kernel group barrier
     else:
         st.set_option(ssa.OPT_CLUSTER, C)
     ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=256)
@@ -616,7 +618,7 @@ def test_cluster_merge_per_layer_append(cuda, C):
         for l in range(L):
             st.append_layer(sid, t, l, Qd[l:l + 1], Kd[l:l + 1], Vd[l:l + 1], O[l:l + 1])
         st.append_commit(sid, t)
-        if C == "gbar":
+        if C in ("gbar", "gbar_barrier"):
             assert st.last_plan()["gbar"] == 1, st.last_plan()
         Oref, _ = ref.session_append(rsid, Q, K, V)
         ok, e = within(from_dev(O), Oref, "bf16")
