@@ -20,8 +20,9 @@ for m in (256, 32):
     Q = torch.empty(m, hq, d, dtype=torch.bfloat16, device=dev)
     K = torch.empty(m, hkv, d, dtype=torch.bfloat16, device=dev)
     V = torch.empty_like(K)
-    for dbg, th in ((0, 5e5), (1, 5e5), (0, 0.0), (1, 0.0), (0, 5e5)):
+    for dbg, th, pdl in ((0, 5e5, 1), (1, 5e5, 1), (0, 5e5, 0), (1, 5e5, 0)):
         st.set_option(ssa.OPT_QKV_DEBUG, dbg)
+        st.set_option(ssa.OPT_PDL, pdl)
         st.qkv_rope(X[0], W[0], Q, K, V, pos0=100, rope_theta=th, stream=gs)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -37,5 +38,5 @@ for m in (256, 32):
             g.replay()
         b.record()
         b.synchronize()
-        print(f"QKVDBG m={m} debug={dbg} theta={th} {a.elapsed_time(b) / 5 / L * 1e3:.1f} us/layer", flush=True)
+        print(f"QKVDBG m={m} debug={dbg} theta={th} pdl={pdl} {a.elapsed_time(b) / 5 / L * 1e3:.1f} us/layer", flush=True)
 st.close()
