@@ -562,7 +562,7 @@ def test_cluster_merge_per_layer_query(cuda, nq, stream_name):
     assert st.stats()["cm_launches"] >= 2 * L * 12
 
 
-@pytest.mark.parametrize("C", [1, 4, 8, "gbar"])
+@pytest.mark.parametrize("C", [1, 4, 8, "gbar", "gbar_barrier"])
 def test_cluster_merge_empty_ranges(cuda, C):
     """A short cache (2 key tiles per head) under a forced cluster size (or the group-barrier
     merge): most CTAs of the plan get empty key ranges (lse = -inf, skipped by the merge)."""
@@ -573,7 +573,9 @@ def test_cluster_merge_empty_ranges(cuda, C):
     for n in (1, 150, 300):
         st = ssa.Store(L, hq, hkv, d, page_size=P, num_pages=64)
         if C == "gbar":
-            st.set_option(ssa.OPT_CM_MERGE, 2)
+            st.set_option(ssa.OPT_CM_MERGE, 2)   # group plan, merge kernel (the default)
+        elif C == "gbar_barrier":
+            st.set_option(ssa.OPT_CM_MERGE, 4)   # group plan, in-kernel group barrier
         else:
             st.set_option(ssa.OPT_CLUSTER, C)
         ref = oracle.OracleStore(L, hq, hkv, d, page_size=P, num_pages=64)
