@@ -122,6 +122,21 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_
                : "memory");
 }
 
+// Shared-memory accesses by 32-bit shared address: the tile pointers are derived from the
+// dynamic smem base by integer arithmetic, so plain dereferences compile to generic
+// LD.E / ST.E (longer latency than LDS / STS).
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ void sts_f2(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+
 __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
   __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
   __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
@@ -246,7 +261,7 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
         rope_cs(p.pos0 + tm * kBM + own_lo + r0, inv_freq[j], &cs, &sn);
         rope_cs(1, inv_freq[j], &cd, &sd);
         for (int r = r0; r < r1; ++r) {
-          *reinterpret_cast<float2*>(table + (r * 64 + j) * 2) = make_float2(cs, sn);
+          sts_f2(smem_u32(table + (r * 64 + j) * 2), cs, sn);
           const float cn = fmaf(cs, cd, -sn * sd);
           sn = fmaf(sn, cd, cs * sd);
           cs = cn;
@@ -273,7 +288,7 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
     const int q = warp & 3;
     const int ch = warp >> 2;
     const int r = q * 32 + lane;
-    float* d = part + (size_t)r * 256;
+    const uint32_t d = smem_u32(part + (size_t)r * 256);
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       uint32_t v0[32], v1[32];
@@ -287,10 +302,8 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int f0 = ch * 32 + h2 * 16 + e, f1 = f0 + 8;
-          *reinterpret_cast<uint4*>(d + 4 * (f0 ^ (r & 7))) =
-              make_uint4(v0[4 * e], v0[4 * e + 1], v0[4 * e + 2], v0[4 * e + 3]);
-          *reinterpret_cast<uint4*>(d + 4 * (f1 ^ (r & 7))) =
-              make_uint4(v1[4 * e], v1[4 * e + 1], v1[4 * e + 2], v1[4 * e + 3]);
+          sts_u4(d + 16u * (uint32_t)(f0 ^ (r & 7)), v0[4 * e], v0[4 * e + 1], v0[4 * e + 2], v0[4 * e + 3]);
+          sts_u4(d + 16u * (uint32_t)(f1 ^ (r & 7)), v1[4 * e], v1[4 * e + 1], v1[4 * e + 2], v1[4 * e + 3]);
         }
       }
     }
@@ -334,10 +347,10 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
       a = make_float4(0.f, 0.f, 0.f, 0.f);
       b = a;
       for (int sp = 0; sp < S; ++sp) {   // fixed order of ranks: deterministic sums
-        const float* src = sp == rank ? part + (size_t)ra * 256
-                                      : recv + (size_t)((sp < rank ? sp : sp - 1) * rows_max + rl) * 256;
-        const float4 x = *reinterpret_cast<const float4*>(src + 4 * (lane ^ (ra & 7)));
-        const float4 y = *reinterpret_cast<const float4*>(src + 4 * ((32 + lane) ^ (ra & 7)));
+        const uint32_t src = smem_u32(sp == rank ? part + (size_t)ra * 256
+                                                 : recv + (size_t)((sp < rank ? sp : sp - 1) * rows_max + rl) * 256);
+        const float4 x = lds_f4(src + 16u * (uint32_t)(lane ^ (ra & 7)));
+        const float4 y = lds_f4(src + 16u * (uint32_t)((32 + lane) ^ (ra & 7)));
         a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
         b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
       }
@@ -350,8 +363,8 @@ qkv_rope_kernel(const QkvParams p, const __grid_constant__ QkvMaps maps) {
       if (rl + kThreads / 32 < own_rows) load_row(rl + kThreads / 32, na, nb);
       float cs[4], sn[4];
       if (use_table) {
-        const float4* e = reinterpret_cast<const float4*>(table + (rl * 64 + j0) * 2);
-        const float4 c01 = e[0], c23 = e[1];
+        const uint32_t e = smem_u32(table + (rl * 64 + j0) * 2);
+        const float4 c01 = lds_f4(e), c23 = lds_f4(e + 16);
         cs[0] = c01.x; sn[0] = c01.y; cs[1] = c01.z; sn[1] = c01.w;
         cs[2] = c23.x; sn[2] = c23.y; cs[3] = c23.z; sn[3] = c23.w;
       } else if (rope) {

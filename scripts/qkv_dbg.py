@@ -15,12 +15,13 @@ L, hq, hkv, d, hidden = 32, 32, 8, 128, 4096
 st = ssa.Store(1, hq, hkv, d, page_size=64, num_pages=4, dtype="bf16")
 W = [streams.gen_qkv_weight(9, l, 6144, hidden, device=dev) for l in range(L)]
 gs = torch.cuda.Stream(device=dev)
-for m in (256, 32):
+for m in [int(x) for x in os.environ.get("QKV_MS", "256 32").split()]:
     X = [streams.gen_hidden(9, 0, 0, l, 0, m, hidden, device=dev) for l in range(L)]
     Q = torch.empty(m, hq, d, dtype=torch.bfloat16, device=dev)
     K = torch.empty(m, hkv, d, dtype=torch.bfloat16, device=dev)
     V = torch.empty_like(K)
-    for dbg, th, pdl in ((0, 5e5, 1), (1, 5e5, 1), (0, 5e5, 0), (1, 5e5, 0)):
+    for dbg, th, pdl in (((0, 5e5, 1), (1, 5e5, 1)) if os.environ.get("QKV_SHORT") else
+                         ((0, 5e5, 1), (1, 5e5, 1), (0, 5e5, 0), (1, 5e5, 0))):
         st.set_option(ssa.OPT_QKV_DEBUG, dbg)
         st.set_option(ssa.OPT_PDL, pdl)
         st.qkv_rope(X[0], W[0], Q, K, V, pos0=100, rope_theta=th, stream=gs)
