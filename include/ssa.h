@@ -80,7 +80,7 @@
 extern "C" {
 #endif
 
-#define SSA_ABI_VERSION 2
+#define SSA_ABI_VERSION 3   /* 3: ssa_debug_last_plan fills out[6]; SSA_OPT_CM_MERGE 2-5 */
 
 typedef enum {
     SSA_OK = 0,

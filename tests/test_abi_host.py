@@ -35,7 +35,7 @@ def test_library_is_sm100a_only():
 
 def test_abi_version_and_status_strings():
     import paper_2605_13784_b200 as ssa
-    assert ssa.lib.ssa_abi_version() == 2
+    assert ssa.lib.ssa_abi_version() == 3
     assert ssa.lib.ssa_status_str(-3) == b"SSA_ERR_POOL_EXHAUSTED"
 
 
