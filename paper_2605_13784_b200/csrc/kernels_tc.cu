@@ -20,6 +20,14 @@
 // softmax slot 0, warps 8-11 softmax slot 1.  A warp whose 32 rows are all
 // padding (a 1-token GQA query fills 4 of 128 rows) skips its softmax.
 //
+// Split-KV epilogues (AttnParams::cm_C, cm_gbar, cm_gsplit): a CTA holding its
+// whole group writes O (a split pair merges its two slots straight from TMEM);
+// a group split over several CTAs of a single-layer call leaves fp32 partials,
+// merged through DSMEM inside a thread-block cluster (cm_reduce), by a merge
+// kernel right behind the grid (gm_merge_kernel for the one-wave group plan,
+// the default of query-plane calls; cm_merge_kernel for groups over several
+// clusters), or after a group barrier in global memory (gm_reduce, an option).
+//
 // FP8 KV variant (template F8, reading R-22): the pools and
 // the call's own K/V hold E4M3 codes.  Lanes 0 / 1 of warp 0 load the K / V
 // tiles (16 KB of codes) into the upper half of their 32 KB ring slots; warp 2
