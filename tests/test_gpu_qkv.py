@@ -54,8 +54,8 @@ def _proj_case(cuda, st, hq, hkv, hidden, n, pos0, theta, seed=11):
     (5, 1, 256, 64, 3, 500000.0),        # odd head count: half-empty last column tile
     (6, 1, 256, 130, 5, 0.0),            # no rotary embedding: the plain GEMM
     (4, 2, 256, 300, 131000, 500000.0),  # large positions (angle reduction)
-    (32, 8, 4096, 256, 32512, 500000.0),  # BJ.configs[1] append shape, split-K 3
-    (32, 8, 4096, 32, 32768, 500000.0),   # BJ.configs[1] query shape, split-K 6
+    (32, 8, 4096, 256, 32512, 500000.0),  # BJ.configs[1] append shape (split-K 2)
+    (32, 8, 4096, 32, 32768, 500000.0),   # BJ.configs[1] query shape (split-K 5)
     (32, 8, 4096, 1024, 0, 500000.0),     # 192 tiles, no split
 ])
 def test_qkv_rope_parity(cuda, hq, hkv, hidden, n, pos0, theta):
